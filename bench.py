@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""bench.py -- KS matmul on B200 (arXiv 2405.15013 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload fft] [--impl ours|reference]
+
+Default workload = BASELINE.json configs[1]: the FFT-style butterfly chain,
+N = 4096, 12 factors (2^{l-1},2,2,2^{12-l}), B = 8192 per GPU, FP32, BSF.
+One *step* = one pass of the whole hot path over one batch: the 12 fused
+factor launches of the chain (K_12 first), inputs resident in HBM.
+
+metric: achieved GB/s with the paper's byte model (read X + nnz(K) + write Y
+per factor), summed over the factors, divided
+by device time.  Multi-GPU (torchrun): the batch is partitioned (weak scaling,
+each rank runs its own B), no collective on the compute path, value = all
+ranks' bytes / max over ranks of the device time.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KS matmul achieved HBM GB/s (% peak) & median speedup vs bmm+permute over sweep"
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback ("of fallback")
+
+
+# ----------------------------------------------------------------- helpers --
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="fft",
+                    choices=["fft", "tiny", "vit_up", "vit_down", "gpt2_down", "gpt2_up"])
+    ap.add_argument("--layout", choices=["bsf", "bsl"], default="bsf")
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch override")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also run the configs[2] sweep vs bmm+permute")
+    return ap.parse_args(argv)
+
+
+def workload(name: str):
+    from ksgen import configs
+    if name == "fft":
+        return dict(name=f"fft_chain_N4096_L{configs.FFT_L}", patterns=configs.dyadic_patterns(configs.FFT_L),
+                    batch=configs.FFT_BATCH, cfg_index=1)
+    if name == "tiny":
+        return dict(name="tiny_(2,4,4,2)", patterns=[configs.TINY_PATTERNS[0]], batch=configs.TINY_BATCH, cfg_index=0)
+    table = {"vit_up": (configs.VIT_UP, configs.VIT_BATCH, 3), "vit_down": (configs.VIT_DOWN, configs.VIT_BATCH, 3),
+             "gpt2_down": (configs.GPT2_DOWN, configs.GPT2_BATCH, 4), "gpt2_up": (configs.GPT2_UP, configs.GPT2_BATCH, 4)}
+    pats, B, idx = table[name]
+    return dict(name=name, patterns=pats, batch=B, cfg_index=idx)
+
+
+def model_bytes(p, B):
+    a, b, c, d = p
+    return 4 * (B * a * c * d + a * b * c * d + B * a * b * d)
+
+
+def model_flops(p, B):
+    a, b, c, d = p
+    return 2 * B * a * b * c * d
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": FALLBACK_HBM_GBS}, "fallback"
+
+
+def ncu_traffic(workload_name, layout):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(f"{workload_name}:{layout}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled in the background."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.window = None
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [s for (t, s) in self.samples if t0 - 0.05 <= t <= t1 + 0.05] or \
+               [s for (_, s) in self.samples[-5:]]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- our arm ----
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import ksgen
+    import paper_2405_15013_b200 as ksb
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ksb.load_library()
+
+    wl = workload(args.workload)
+    pats = wl["patterns"]
+    B = args.batch or wl["batch"]
+    L = len(pats)
+    lay = args.layout
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    facs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    dims = [pats[-1][0] * pats[-1][2] * pats[-1][3]] + [p[0] * p[1] * p[3] for p in reversed(pats)]
+    X_host = ksgen.x_normal(B, dims[0], seed=rank)
+    X_host_l = X_host if lay == "bsf" else ksgen.to_bsl(X_host)
+    X = torch.from_numpy(X_host_l).to(dev)
+    shape = (lambda n: (B, n)) if lay == "bsf" else (lambda n: (n, B))
+    bufs = [torch.empty(shape(max(dims[1:-1] or [1])), device=dev) for _ in range(2)]
+    Y = torch.empty(shape(dims[-1]), device=dev)
+    stream = torch.cuda.current_stream()
+    props = torch.cuda.get_device_properties(dev)
+    flush = torch.empty(2 * props.L2_cache_size, dtype=torch.uint8, device=dev)
+
+    def step(evs=None):
+        """The chain, K_L first, each factor one fused launch."""
+        src = X
+        for t, l in enumerate(range(L - 1, -1, -1)):
+            n_out = dims[t + 1]
+            if l == 0:
+                dst = Y
+            else:
+                dst = bufs[t % 2].view(-1)[: B * n_out].view(shape(n_out))
+            if evs is not None:
+                evs[t][0].record(stream)
+            ksb.matmul(facs[l], src, dst, layout=lay, B=B)
+            if evs is not None:
+                evs[t][1].record(stream)
+            src = dst
+
+    # warm-up
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev_k = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+            for _ in range(K)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ksb.launch_count()
+    t0 = time.time()
+    for s in range(K):
+        flush.fill_(s & 0xFF)                 # evict L2 between timed steps (not timed)
+        ev_step[s][0].record(stream)
+        step(ev_k[s])
+        ev_step[s][1].record(stream)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    launches = ksb.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    time.sleep(0.1)
+    sampler.stop()
+    clocks = sampler.summary(t0, t1)
+
+    step_ms = [a.elapsed_time(b) for a, b in ev_step]
+    tot_ms = sum(step_ms)
+    k_ms = [[a.elapsed_time(b) for a, b in row] for row in ev_k]
+    # dominant kernel: the factor family; all factors here run one family per plan
+    plans = [facs[l].plan(B, lay) for l in range(L - 1, -1, -1)]
+    per_factor_bytes = [model_bytes(pats[l], B) for l in range(L - 1, -1, -1)]
+    fam_time, fam_bytes, fam_n = {}, {}, {}
+    for s in range(K):
+        for t in range(L):
+            fam_time[plans[t]] = fam_time.get(plans[t], 0.0) + k_ms[s][t]
+            fam_bytes[plans[t]] = fam_bytes.get(plans[t], 0) + per_factor_bytes[t]
+            fam_n[plans[t]] = fam_n.get(plans[t], 0) + 1
+    dom = max(fam_time, key=fam_time.get)
+
+    tot_t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot_t, op=dist.ReduceOp.MAX)
+    tot_ms_max = float(tot_t.item())
+    step_bytes = sum(model_bytes(p, B) for p in pats)
+    value = world * K * step_bytes / (tot_ms_max * 1e-3) / 1e9
+
+    # e2e through the C ABI with HOST buffers (pinned), copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X_host_l).pin_memory()
+        Yh = torch.empty(shape(dims[-1]), dtype=torch.float32).pin_memory()
+        ke = max(3, min(K, 20))
+        for _ in range(2):
+            ksb.chain_host(facs, Xh, Yh, layout=lay)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ke)]
+        if world > 1:
+            dist.barrier()
+        for s in range(ke):
+            evs[s][0].record(stream)
+            ksb.chain_host(facs, Xh, Yh, layout=lay)
+            evs[s][1].record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * ke * step_bytes / (float(e_ms.item()) * 1e-3) / 1e9, 2),
+               "unit": "GB/s", "h2d_bytes_per_step": int(Xh.numel() * 4),
+               "d2h_bytes_per_step": int(Yh.numel() * 4), "api": "ks_chain_host", "steps": ke}
+        # the e2e result must equal the device-resident one
+        if world == 1:
+            step()
+            torch.cuda.synchronize()
+            if not torch.equal(Yh, Y.cpu()):
+                raise RuntimeError("e2e result differs from device-resident result")
+
+    # chain API device-resident timing (same launches as `step`, via ks_chain_ex)
+    kc = min(K, 50)
+    evc = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kc)]
+    for s in range(kc):
+        flush.fill_(s & 0xFF)
+        evc[s][0].record(stream)
+        ksb.chain(facs, X, Y, layout=lay)
+        evc[s][1].record(stream)
+    torch.cuda.synchronize()
+    chain_api_ms = statistics.median(a.elapsed_time(b) for a, b in evc)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return None
+
+    peaks, src = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    avg_launch_ms = fam_time[dom] / fam_n[dom]
+    bytes_per_launch = fam_bytes[dom] / fam_n[dom]
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(tot_ms_max / K, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (X ~ N(0,1), K ~ U[-1/sqrt(c),1/sqrt(c)], PAPER.md:1220), seeded",
+        "config": {"workload": wl["name"], "baseline_config_index": wl["cfg_index"],
+                   "patterns": [list(p) for p in pats], "batch_per_gpu": B, "global_batch": B * world,
+                   "layout": lay, "parallelism": f"batch-partitioned x{world}, no collective",
+                   "l2": "flushed between timed steps (2x L2 write, untimed)",
+                   "bytes_per_step_per_gpu": step_bytes},
+        "hbm_frac_of_" + src: round(value / world / peak, 4),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                     "peak_source": src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(wl["name"], lay),
+                     "algorithmic_bytes_per_launch": int(bytes_per_launch),
+                     "avg_launch_us": round(avg_launch_ms * 1e3, 3),
+                     "share_of_step": round(fam_time[dom] / tot_ms, 4)},
+        "gpu_launches": int(launches),
+        "launches_per_step": launches / K,
+        "chain_api_ms_per_step": round(chain_api_ms, 5),
+        "clocks": clocks,
+        "e2e": e2e,
+        "plans": plans,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(pats, K4s, X_host, B, budget_s=15.0)
+    if args.sweep:
+        from bench_sweep import run_sweep
+        line["sweep"] = run_sweep(dev)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def cpu_baseline(pats, K4s, X_host, B, budget_s=15.0):
+    """The oracle as it stands, on this host's cores, on a bounded row sample."""
+    import oracle
+    import numpy as np
+    threads = oracle.default_threads()
+    t = time.time()
+    oracle.chain(pats, K4s, X_host, rows=[0], threads=threads)
+    t1 = max(time.time() - t, 1e-3)
+    R = int(max(1, min(B, budget_s / t1)))
+    rows = np.arange(R)
+    t = time.time()
+    oracle.chain(pats, K4s, X_host, rows=rows, threads=threads)
+    dt = time.time() - t
+    byts = sum(model_bytes(p, R) for p in pats)
+    return {"value": round(byts / dt / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"{R} of {B} batch rows of the workload, FP64 naive dense triple loop (oracle/ks_oracle.c)",
+            "seconds": round(dt, 3)}
+
+
+# --------------------------------------------------------- reference arm ----
+def run_reference(args):
+    """The CPU oracle timed as the reference arm (this tier has no reference code)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import numpy as np
+    import ksgen
+    import oracle
+    wl = workload(args.workload)
+    pats = wl["patterns"]
+    B = args.batch or wl["batch"]
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    N = pats[-1][0] * pats[-1][2] * pats[-1][3]
+    threads = oracle.default_threads()
+    budget = 150.0
+    steps, warm = max(args.steps, 1), max(args.warmup, 0)
+    # rows per step: fill the threads once if the budget allows, else 1
+    t = time.time()
+    X1 = ksgen.x_rows_normal([0], N, seed=0)
+    oracle.chain(pats, K4s, X1, threads=threads)
+    t1 = max(time.time() - t, 1e-4)
+    R = max(1, min(threads, int(budget / (steps + warm) / t1)))
+    Xs = ksgen.x_rows_normal(np.arange(R), N, seed=0)
+    for _ in range(warm):
+        oracle.chain(pats, K4s, Xs, threads=threads)
+    t = time.time()
+    for _ in range(steps):
+        oracle.chain(pats, K4s, Xs, threads=threads)
+    dt = time.time() - t
+    byts = sum(model_bytes(p, R) for p in pats)
+    v = steps * byts / dt / 1e9
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, seeded", "config": {"workload": wl["name"], "baseline_config_index": wl["cfg_index"],
+                                                     "batch_per_step": R, "layout": "bsf"},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{R} of {B} batch rows per step"},
+            "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * ks.h -- C ABI of the B200-native Kronecker-sparse (KS) matmul library
+ *         (libks.so, built from paper_2405_15013_b200/csrc/).
+ *
+ * The operation (§1 "Scope of This Work"):
+ *
+ *     Y = X K^T,    K in R^{M x N},  M = a b d,  N = a c d,
+ *
+ * where K is (a,b,c,d)-Kronecker-sparse: supp(K) is contained in
+ * I_a (x) 1_{b x c} (x) I_d  (Def. 1).  K is fixed and may be
+ * preprocessed offline (ks_pack_weights); X and Y are dense and keep the
+ * caller's layout, batch-size-first or batch-size-last
+ * (§2.2).  Chains K_1 ... K_L (Table 3,
+ * PAPER.md:936-962) are applied as Y = X K_L^T ... K_1^T.
+ *
+ * Conventions shared by every entry point
+ *  - Element type: IEEE float32 for X, K, Y.  Arithmetic is FP32 FFMA on
+ *    CUDA cores (KS_MATH_FP32, default) or TF32 tensor cores with FP32
+ *    accumulation (KS_MATH_TF32; only where b,c >= 16).
+ *  - Indexing is 64-bit throughout.  B = 0 is a no-op returning KS_OK.
+ *  - Pointers named X / Y below are CUDA DEVICE pointers (e.g. a torch
+ *    tensor's data_ptr()) on the device the handle was packed on, contiguous,
+ *    at least 4-byte aligned (16-byte alignment enables the vector paths).
+ *    X and Y must not overlap.  Y is fully overwritten (every element written
+ *    exactly once; PAPER.md:354-374 row sets partition [0, M)).
+ *  - Streams: ks_stream_t is a cudaStream_t passed as void*; NULL is the
+ *    legacy default stream.  Calls are asynchronous w.r.t. the host unless
+ *    stated; launch errors are reported by the return value, asynchronous
+ *    device faults surface at the caller's next synchronisation.
+ *  - Errors: every call returns a ks_status_t and never aborts; the status
+ *    and a message are also kept per host thread (ks_last_error*).
+ *  - Threading: handles are immutable after ks_pack_weights (ks_set_math /
+ *    ks_set_kernel excepted: do not call them concurrently with a matmul on
+ *    the same handle); concurrent ks_matmul / ks_chain calls on different
+ *    streams are safe.
+ */
+#ifndef KS_H_
+#define KS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KS_ABI_VERSION 1
+
+typedef struct ks_handle_s* ks_handle_t;   /* opaque packed factor           */
+typedef void* ks_stream_t;                 /* cudaStream_t                    */
+
+/* Batch layouts.
+ *  BSF: X is B x N row-major, X(n,s) = X[n*N + s];  Y(n,r) = Y[n*M + r].
+ *  BSL: X is N x B row-major, X(n,s) = X[s*B + n];  Y(n,r) = Y[r*B + n].      */
+typedef enum { KS_LAYOUT_BSF = 0, KS_LAYOUT_BSL = 1 } ks_layout_t;
+
+/* Arithmetic.  TF32: operands rounded to TF32 (K: round-to-nearest-away at
+ * pack time; X: per kernel), products accumulated in FP32. */
+typedef enum { KS_MATH_FP32 = 0, KS_MATH_TF32 = 1 } ks_math_t;
+
+/* Kernel families; KS_KERNEL_AUTO lets the plan table choose (default).    */
+typedef enum {
+    KS_KERNEL_AUTO = 0,
+    KS_KERNEL_GENERIC = 1,  /* one thread per output element, any pattern   */
+    KS_KERNEL_STREAM = 2,   /* vectorised streaming kernel, b,c in {1,2,4}  */
+    KS_KERNEL_FFMA = 3,     /* register-tiled FP32 kernel, larger b,c       */
+    KS_KERNEL_TF32 = 4      /* tcgen05 TF32 tensor-core kernel              */
+} ks_kernel_t;
+
+typedef enum {
+    KS_OK = 0,
+    KS_ERR_INVALID_ARG = 1,  /* null pointer, negative size, overlap, bad enum */
+    KS_ERR_PATTERN = 2,      /* a,b,c,d < 1 or sizes overflow 64-bit           */
+    KS_ERR_CHAIN_SHAPE = 3,  /* a_l c_l d_l != a_{l+1} b_{l+1} d_{l+1}         */
+    KS_ERR_UNSUPPORTED = 4,  /* requested kernel/math cannot run this pattern  */
+    KS_ERR_DEVICE = 5,       /* no CUDA device / wrong current device / not sm_100 */
+    KS_ERR_ALIGNMENT = 6,    /* pointer not 4-byte aligned                     */
+    KS_ERR_OOM = 7,          /* device or pinned allocation failed             */
+    KS_ERR_CUDA = 8          /* any other CUDA runtime error (see message)     */
+} ks_status_t;
+
+/* ---------------------------------------------------------------------------
+ * ks_pack_weights -- offline preprocessing of one KS factor (PAPER.md:434-436:
+ * "preprocessed and stored so that every tile K^T[col_ij, row_ij] is already
+ * contiguous"; excluded from timing).
+ *   a,b,c,d : the pattern (Def. 1), each >= 1.
+ *   K       : a*b*c*d floats in canonical order (a,b,c,d), d fastest
+ *             (einsum packing): K[((i*b+k)*c+l)*d+j] is
+ *             the entry at row i*b*d + k*d + j, column i*c*d + l*d + j.
+ *             Host or device memory (copied through UVA).  Not retained.
+ * Synchronous.  The handle owns device copies of K in every layout the
+ * kernels read (canonical, tile-contiguous K^T, TF32 operand tiles) on the
+ * device current at call time.  Returns NULL on error (see ks_last_error).
+ * ------------------------------------------------------------------------- */
+ks_handle_t ks_pack_weights(int64_t a, int64_t b, int64_t c, int64_t d, const float* K);
+
+/* Release a handle (NULL is ignored).  Synchronises the handle's device. */
+void ks_free(ks_handle_t h);
+
+/* Pattern of a handle: out[0..3] = a,b,c,d.                               */
+ks_status_t ks_get_pattern(ks_handle_t h, int64_t out[4]);
+
+/* Select the arithmetic.  KS_MATH_TF32 needs b >= 16 and c >= 16
+ * (north star: tensor cores only where each block is a dense contraction);
+ * otherwise KS_ERR_UNSUPPORTED and the math is unchanged.                  */
+ks_status_t ks_set_math(ks_handle_t h, ks_math_t m);
+
+/* Force a kernel family (tests / benchmarks).  KS_KERNEL_AUTO restores the
+ * plan table.  A forced family that cannot run a given call makes that call
+ * return KS_ERR_UNSUPPORTED (no silent fallback).                          */
+ks_status_t ks_set_kernel(ks_handle_t h, ks_kernel_t k);
+
+/* The kernel family ks_matmul would launch for (B, layout) on this handle. */
+ks_status_t ks_plan(ks_handle_t h, int64_t B, ks_layout_t layout, ks_kernel_t* out);
+
+/* ---------------------------------------------------------------------------
+ * ks_matmul -- Y = X K^T for one factor: ONE fused kernel launch on `stream`,
+ * no permutation passes (Alg. 2/3).
+ *   X : device, B*N floats in `layout`;  Y : device, B*M floats in `layout`.
+ * ------------------------------------------------------------------------- */
+ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B,
+                      ks_layout_t layout, ks_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * ks_chain -- Y = X K_L^T ... K_1^T (PAPER.md:53-54 with the Y = X K^T form of
+ * PAPER.md:86), batch-size-first.  handles[0] = K_1, ..., handles[L-1] = K_L
+ * (paper order); K_L is applied first.  Requires N(K_l) == M(K_{l+1}), i.e.
+ * a_l c_l d_l == a_{l+1} b_{l+1} d_{l+1} (Table 3), else
+ * KS_ERR_CHAIN_SHAPE.  X: B*N(K_L) floats, Y: B*M(K_1) floats, device.
+ * Intermediates live in a stream-ordered workspace owned by the library
+ * (allocated and freed on `stream`).  L launches.
+ * ------------------------------------------------------------------------- */
+ks_status_t ks_chain(const ks_handle_t* handles, int L, const float* X, float* Y,
+                     int64_t B, ks_stream_t stream);
+
+/* Same as ks_chain with an explicit layout for X, Y and the intermediates. */
+ks_status_t ks_chain_ex(const ks_handle_t* handles, int L, const float* X, float* Y,
+                        int64_t B, ks_layout_t layout, ks_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * ks_chain_host -- end-to-end form of ks_chain_ex for HOST buffers: X_host and
+ * Y_host are host memory (pinned for full PCIe speed; pageable works but the
+ * copies then serialise).  Enqueues host->device copy of X, the chain, and
+ * device->host copy of Y on `stream`; device buffers come from the library's
+ * stream-ordered pool.  Asynchronous: Y_host is valid after the caller
+ * synchronises `stream`.  A single factor is L = 1.
+ * ------------------------------------------------------------------------- */
+ks_status_t ks_chain_host(const ks_handle_t* handles, int L, const float* X_host,
+                          float* Y_host, int64_t B, ks_layout_t layout, ks_stream_t stream);
+
+/* Copy one packed variant of K back to host (tests check the index maps
+ * bit-exactly).  variant 0: canonical a*b*c*d;  1: tile-contiguous K^T,
+ * [i*d+j][l][k] (a*d*c*b floats);  2: TF32-rounded tiles [i*d+j][k][l]
+ * (a*d*b*c floats).  count must equal the variant's element count.         */
+ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst_host, int64_t count);
+
+/* Diagnostics. */
+ks_status_t ks_last_error(void);                /* per host thread           */
+const char* ks_last_error_message(void);        /* per host thread, static   */
+const char* ks_status_string(ks_status_t s);
+uint64_t    ks_kernel_launch_count(void);       /* kernels launched so far   */
+int         ks_abi_version(void);               /* KS_ABI_VERSION            */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_H_ */

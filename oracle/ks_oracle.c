@@ -19,8 +19,9 @@
  *       X(n,s) is addressed through the layout: batch-size-first X[n*N+s],
  *       batch-size-last X[s*B+n] (§2.2).  It also returns
  *       the error envelope  A(n,r) = sum_s |X(n,s)| |D[r][s]|.
- *       OpenMP over output rows n; each row has one owner, so the result is
- *       independent of the thread count.
+ *       OpenMP over the (n, r) output elements; each element has one owner
+ *       and a fixed summation order, so the result is independent of the
+ *       thread count.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -71,11 +72,15 @@ int ks_oracle_matmul_dense(int64_t M, int64_t N, const double* D,
     (void)threads;
 #endif
     int bad = 0;
-#pragma omp parallel for schedule(dynamic, 1)
     for (int64_t t = 0; t < nrows; ++t) {
         const int64_t n = rows ? rows[t] : t;
-        if (n < 0 || n >= B) { bad = 1; continue; }
+        if (n < 0 || n >= B) bad = 1;
+    }
+    if (bad) return KS_ORACLE_EINVAL;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t t = 0; t < nrows; ++t) {
         for (int64_t r = 0; r < M; ++r) {
+            const int64_t n = rows ? rows[t] : t;
             double acc = 0.0, env = 0.0;
             for (int64_t s = 0; s < N; ++s) {
                 const double x = layout == 0 ? X[n * N + s] : X[s * B + n];

@@ -390,6 +390,15 @@ def normwise_error(Y_hat, Y_ref) -> float:
     return num / den
 
 
+def round_tf32_rna(x) -> np.ndarray:
+    """Round float32 values to TF32 (10 explicit mantissa bits), to nearest with
+    ties away from zero (the RNA rounding SURVEY §8c-11 fixes for packed K).
+    Sign-magnitude encoding: adding half an ulp (bit 12) to the magnitude bits
+    and truncating the low 13 bits rounds |x| half-up.  Finite inputs only."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    return ((b + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
 def envelope_delta(c: int, u_in: float, u: float = 2.0 ** -24) -> float:
     """Per-hop relative factor delta = 2 u_in + u_in^2 + gamma_{2c}
     (SURVEY §8c O-6): standard order-independent summation bound with slack."""

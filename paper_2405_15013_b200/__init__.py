@@ -1,0 +1,10 @@
+"""B200-native Kronecker-sparse matmul (arXiv 2405.15013 hot path).
+
+The product is libks.so (C ABI in include/ks.h, CUDA for sm_100a in csrc/);
+``ks`` is its thin Python binding.
+"""
+from .ks import (  # noqa: F401
+    BSF, BSL, MATH_FP32, MATH_TF32,
+    KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STREAM, KERNEL_FFMA, KERNEL_TF32,
+    Factor, KSError, matmul, chain, chain_host, launch_count, load_library, LIB_PATH, EXPORTS,
+)

@@ -1,0 +1,64 @@
+// Generic KS kernel: one thread per output element, any pattern, any layout,
+// any B.  The correctness floor of the library and the
+// fallback for shapes no specialised family covers.
+//
+// For output (n, r) with r = i*b*d + k*d + j (row_{i,j}[k], Alg. 2 line 3,
+// PAPER.md:356) the reduction runs over col_{i,j} = {i*c*d + l*d + j}
+// (Alg. 2 line 4), l ascending, FP32 FMA:
+//     Y(n, r) = sum_l X(n, i*c*d + l*d + j) * K4[i][k][l][j].
+// Every output is written exactly once (row sets partition [0,M)).
+#include "ks_internal.h"
+
+namespace {
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(256) ks_generic_kernel(
+    const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
+    int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
+    const int64_t M = a * b * d, N = a * c * d;
+    const int64_t total = B * M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t n, r;
+        if (LAYOUT == KS_LAYOUT_BSF) { n = e / M; r = e - n * M; }
+        else                         { r = e / B; n = e - r * B; }
+        const int64_t i = r / (b * d);
+        const int64_t rem = r - i * b * d;
+        const int64_t k = rem / d;
+        const int64_t j = rem - k * d;
+        const int64_t s0 = i * c * d + j;                // col_{i,j}[0]
+        const float* kp = K4 + ((i * b + k) * c) * d + j;  // K4[i][k][0][j]
+        float acc = 0.f;
+        for (int64_t l = 0; l < c; ++l) {
+            const int64_t s = s0 + l * d;
+            const float x = LAYOUT == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n];
+            acc = fmaf(x, kp[l * d], acc);
+        }
+        Y[e] = acc;
+    }
+}
+
+}  // namespace
+
+namespace ks {
+
+bool generic_supports(const ks_handle_s&, const KsCall&) { return true; }
+
+cudaError_t generic_launch(const ks_handle_s& h, const KsCall& call) {
+    const int threads = 256;
+    const int64_t total = call.B * h.M;
+    int64_t blocks = (total + threads - 1) / threads;
+    const int64_t cap = (int64_t)num_sms(h.device) * 8 * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (call.layout == KS_LAYOUT_BSF)
+        ks_generic_kernel<KS_LAYOUT_BSF><<<(unsigned)blocks, threads, 0, call.stream>>>(
+            call.X, h.k_canon, call.Y, call.B, h.a, h.b, h.c, h.d);
+    else
+        ks_generic_kernel<KS_LAYOUT_BSL><<<(unsigned)blocks, threads, 0, call.stream>>>(
+            call.X, h.k_canon, call.Y, call.B, h.a, h.b, h.c, h.d);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace ks

@@ -1,0 +1,54 @@
+// Internal interfaces between the host runtime (ks_runtime.cpp) and the
+// kernel translation units.  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ks.h"
+
+struct ks_handle_s {
+    int64_t a, b, c, d;   // pattern (Def. 1)
+    int64_t M, N, nnz;    // abd, acd, abcd
+    int device;
+    float* k_canon;       // [a][b][c][d]            (boundary order)
+    float* k_tile;        // [i*d+j][l][k]  = K^T tiles
+    float* k_tf32;        // [i*d+j][k][l]  TF32-rounded, K-major B operand
+    ks_math_t math;
+    ks_kernel_t forced;
+};
+
+struct KsCall {
+    const float* X;
+    float* Y;
+    int64_t B;
+    int layout;           // ks_layout_t
+    cudaStream_t stream;
+};
+
+namespace ks {
+
+// Process-wide launch counter (ks_kernel_launch_count).
+void count_launch();
+
+// ---- packing (ks_pack.cu) --------------------------------------------------
+cudaError_t pack_tiles(const ks_handle_s& h, cudaStream_t s);
+
+// ---- kernel families ---------------------------------------------------------
+// Each family exposes `supports` (pure host predicate, no CUDA calls) and
+// `launch` (exactly one kernel launch on call.stream).
+bool generic_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t generic_launch(const ks_handle_s& h, const KsCall& call);
+
+bool stream_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t stream_launch(const ks_handle_s& h, const KsCall& call);
+
+bool ffma_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call);
+
+bool tf32_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);
+
+int num_sms(int device);
+
+}  // namespace ks

@@ -1,0 +1,51 @@
+// Offline repacking of a KS factor (ks_pack_weights).  An integer permutation
+// of the abcd canonical values into the layouts the kernels read:
+//   k_tile[(i*d+j)][l][k]  = K4[i][k][l][j]   K^T[col_ij, row_ij] contiguous per
+//                                            tile, k fastest
+//   k_tf32[(i*d+j)][k][l]  = rna_tf32(K4[i][k][l][j])   K-major B operand of the
+//                                            tcgen05 TF32 kernel, pre-rounded
+// Excluded from timing.
+#include "ks_internal.h"
+
+namespace {
+
+__device__ __forceinline__ float round_tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__global__ void pack_kernel(const float* __restrict__ k4, float* __restrict__ tile,
+                            float* __restrict__ tf32, int64_t a, int64_t b, int64_t c,
+                            int64_t d) {
+    const int64_t nnz = a * b * c * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        // e = ((i*b + k)*c + l)*d + j
+        const int64_t j = e % d;
+        int64_t t = e / d;
+        const int64_t l = t % c;
+        t /= c;
+        const int64_t k = t % b;
+        const int64_t i = t / b;
+        const float v = k4[e];
+        const int64_t q = i * d + j;
+        tile[(q * c + l) * b + k] = v;
+        tf32[(q * b + k) * c + l] = round_tf32_rna(v);
+    }
+}
+
+}  // namespace
+
+namespace ks {
+
+cudaError_t pack_tiles(const ks_handle_s& h, cudaStream_t s) {
+    const int threads = 256;
+    int64_t blocks = (h.nnz + threads - 1) / threads;
+    if (blocks > 65535 * 8) blocks = 65535 * 8;
+    pack_kernel<<<(unsigned)blocks, threads, 0, s>>>(h.k_canon, h.k_tile, h.k_tf32, h.a, h.b, h.c, h.d);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace ks

@@ -1,0 +1,392 @@
+// Host runtime behind the C ABI of include/ks.h: validation, handles and
+// packing, per-call plan selection, chain orchestration with a stream-ordered
+// workspace, error state.  Every compute step runs in the kernels of the
+// other translation units; nothing here touches X, K or Y on the host.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "ks_internal.h"
+
+namespace {
+
+thread_local ks_status_t t_status = KS_OK;
+thread_local char t_msg[512] = "ok";
+
+std::atomic<uint64_t> g_launches{0};
+
+ks_status_t fail(ks_status_t s, const char* fmt, ...) {
+    t_status = s;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(t_msg, sizeof(t_msg), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+ks_status_t ok() {
+    t_status = KS_OK;
+    std::snprintf(t_msg, sizeof(t_msg), "ok");
+    return KS_OK;
+}
+
+ks_status_t fail_cuda(cudaError_t e, const char* where) {
+    if (e == cudaErrorMemoryAllocation)
+        return fail(KS_ERR_OOM, "%s: %s", where, cudaGetErrorString(e));
+    return fail(KS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool mul_ok(int64_t x, int64_t y, int64_t* out) {
+    return !__builtin_mul_overflow(x, y, out) && *out < (int64_t(1) << 62);
+}
+
+// ---- per-device stream-ordered memory pool (chain workspace, host staging) ---
+std::mutex g_pool_mu;
+std::vector<cudaMemPool_t> g_pools;
+
+cudaError_t get_pool(int dev, cudaMemPool_t* out) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1, nullptr);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props;
+        std::memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p;
+        cudaError_t e = cudaMemPoolCreate(&p, &props);
+        if (e != cudaSuccess) return e;
+        uint64_t keep = ~uint64_t(0);   // keep freed blocks: steady state is allocation-free
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_pools[dev] = p;
+    }
+    *out = g_pools[dev];
+    return cudaSuccess;
+}
+
+ks_status_t check_device(const ks_handle_s* h) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaGetDevice");
+    if (dev != h->device)
+        return fail(KS_ERR_DEVICE, "handle packed on device %d but current device is %d",
+                    h->device, dev);
+    return KS_OK;
+}
+
+bool overlap(const void* x, int64_t xbytes, const void* y, int64_t ybytes) {
+    auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+    return xa < ya + (uintptr_t)ybytes && ya < xa + (uintptr_t)xbytes;
+}
+
+ks_kernel_t choose(const ks_handle_s& h, const KsCall& call) {
+    if (h.forced != KS_KERNEL_AUTO) {
+        switch (h.forced) {
+            case KS_KERNEL_GENERIC: return ks::generic_supports(h, call) ? KS_KERNEL_GENERIC : KS_KERNEL_AUTO;
+            case KS_KERNEL_STREAM:  return ks::stream_supports(h, call) ? KS_KERNEL_STREAM : KS_KERNEL_AUTO;
+            case KS_KERNEL_FFMA:    return ks::ffma_supports(h, call) ? KS_KERNEL_FFMA : KS_KERNEL_AUTO;
+            case KS_KERNEL_TF32:    return ks::tf32_supports(h, call) ? KS_KERNEL_TF32 : KS_KERNEL_AUTO;
+            default: return KS_KERNEL_AUTO;
+        }
+    }
+    if (h.math == KS_MATH_TF32 && ks::tf32_supports(h, call)) return KS_KERNEL_TF32;
+    if (ks::stream_supports(h, call)) return KS_KERNEL_STREAM;
+    if (ks::ffma_supports(h, call)) return KS_KERNEL_FFMA;
+    return KS_KERNEL_GENERIC;
+}
+
+cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
+    switch (k) {
+        case KS_KERNEL_GENERIC: return ks::generic_launch(h, call);
+        case KS_KERNEL_STREAM:  return ks::stream_launch(h, call);
+        case KS_KERNEL_FFMA:    return ks::ffma_launch(h, call);
+        case KS_KERNEL_TF32:    return ks::tf32_launch(h, call);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// One factor, arguments already validated.
+ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, int layout,
+                    cudaStream_t s) {
+    KsCall call{X, Y, B, layout, s};
+    ks_kernel_t k = choose(h, call);
+    if (k == KS_KERNEL_AUTO)
+        return fail(KS_ERR_UNSUPPORTED, "forced kernel %d cannot run pattern (%lld,%lld,%lld,%lld) "
+                    "B=%lld layout=%d", (int)h.forced, (long long)h.a, (long long)h.b,
+                    (long long)h.c, (long long)h.d, (long long)B, layout);
+    cudaError_t e = launch(k, h, call);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "kernel launch");
+    return KS_OK;
+}
+
+ks_status_t validate_chain(const ks_handle_t* hs, int L, int64_t B, int layout) {
+    if (!hs || L < 1) return fail(KS_ERR_INVALID_ARG, "need L >= 1 handles");
+    if (B < 0) return fail(KS_ERR_INVALID_ARG, "B must be >= 0");
+    if (layout != KS_LAYOUT_BSF && layout != KS_LAYOUT_BSL)
+        return fail(KS_ERR_INVALID_ARG, "bad layout %d", layout);
+    for (int l = 0; l < L; ++l) {
+        if (!hs[l]) return fail(KS_ERR_INVALID_ARG, "handles[%d] is NULL", l);
+        ks_status_t s = check_device(hs[l]);
+        if (s != KS_OK) return s;
+    }
+    for (int l = 0; l + 1 < L; ++l)
+        if (hs[l]->N != hs[l + 1]->M)
+            return fail(KS_ERR_CHAIN_SHAPE, "factor %d has N=%lld but factor %d has M=%lld "
+                        "(need a_l c_l d_l == a_{l+1} b_{l+1} d_{l+1})", l + 1,
+                        (long long)hs[l]->N, l + 2, (long long)hs[l + 1]->M);
+    int64_t t;
+    for (int l = 0; l < L; ++l)
+        if (!mul_ok(B, hs[l]->M, &t) || !mul_ok(B, hs[l]->N, &t))
+            return fail(KS_ERR_INVALID_ARG, "B * dim overflows");
+    return KS_OK;
+}
+
+// Chain on device buffers; X, Y validated by the caller.
+ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
+                      int layout, cudaStream_t s) {
+    if (L == 1) return run_one(*hs[0], X, Y, B, layout, s);
+    int64_t maxdim = 0;
+    for (int l = 1; l < L; ++l) maxdim = hs[l]->M > maxdim ? hs[l]->M : maxdim;
+    cudaMemPool_t pool;
+    cudaError_t e = get_pool(hs[0]->device, &pool);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
+    const size_t bytes = sizeof(float) * (size_t)(B * maxdim);
+    void* buf[2] = {nullptr, nullptr};
+    const int nbuf = L >= 3 ? 2 : 1;
+    for (int i = 0; i < nbuf; ++i) {
+        e = cudaMallocFromPoolAsync(&buf[i], bytes, pool, s);
+        if (e != cudaSuccess) {
+            for (int k = 0; k < i; ++k) cudaFreeAsync(buf[k], s);
+            return fail_cuda(e, "chain workspace");
+        }
+    }
+    ks_status_t st = KS_OK;
+    const float* in = X;
+    for (int l = L - 1; l >= 0 && st == KS_OK; --l) {
+        float* out = (l == 0) ? Y : static_cast<float*>(buf[(L - 1 - l) % nbuf]);
+        st = run_one(*hs[l], in, out, B, layout, s);
+        in = out;
+    }
+    for (int i = 0; i < nbuf; ++i) cudaFreeAsync(buf[i], s);
+    return st;
+}
+
+}  // namespace
+
+namespace ks {
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int num_sms(int device) {
+    static std::mutex mu;
+    static std::vector<int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)cache.size() <= device) cache.resize(device + 1, 0);
+    if (!cache[device]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+        cache[device] = n > 0 ? n : 148;
+    }
+    return cache[device];
+}
+}  // namespace ks
+
+extern "C" {
+
+ks_handle_t ks_pack_weights(int64_t a, int64_t b, int64_t c, int64_t d, const float* K) {
+    if (a < 1 || b < 1 || c < 1 || d < 1) {
+        fail(KS_ERR_PATTERN, "pattern entries must be >= 1, got (%lld,%lld,%lld,%lld)",
+             (long long)a, (long long)b, (long long)c, (long long)d);
+        return nullptr;
+    }
+    int64_t ab, abd, ac, acd, abc, nnz;
+    if (!mul_ok(a, b, &ab) || !mul_ok(ab, d, &abd) || !mul_ok(a, c, &ac) || !mul_ok(ac, d, &acd) ||
+        !mul_ok(ab, c, &abc) || !mul_ok(abc, d, &nnz) || nnz > (int64_t(1) << 40)) {
+        fail(KS_ERR_PATTERN, "pattern sizes overflow");
+        return nullptr;
+    }
+    if (!K) { fail(KS_ERR_INVALID_ARG, "K is NULL"); return nullptr; }
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) { fail(KS_ERR_DEVICE, "no CUDA device: %s", cudaGetErrorString(e)); return nullptr; }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) {
+        fail(KS_ERR_DEVICE, "libks is built for sm_100a (B200); device %d is sm_%d%d", dev, major, minor);
+        return nullptr;
+    }
+    auto* h = new ks_handle_s();
+    h->a = a; h->b = b; h->c = c; h->d = d;
+    h->M = abd; h->N = acd; h->nnz = nnz;
+    h->device = dev;
+    h->math = KS_MATH_FP32;
+    h->forced = KS_KERNEL_AUTO;
+    const size_t bytes = sizeof(float) * (size_t)nnz;
+    if ((e = cudaMalloc(&h->k_canon, bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&h->k_tile, bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&h->k_tf32, bytes)) != cudaSuccess) {
+        fail_cuda(e, "ks_pack_weights alloc");
+        ks_free(h);
+        return nullptr;
+    }
+    if ((e = cudaMemcpy(h->k_canon, K, bytes, cudaMemcpyDefault)) != cudaSuccess ||
+        (e = ks::pack_tiles(*h, 0)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(0)) != cudaSuccess) {
+        fail_cuda(e, "ks_pack_weights copy/pack");
+        ks_free(h);
+        return nullptr;
+    }
+    ok();
+    return h;
+}
+
+void ks_free(ks_handle_t h) {
+    if (!h) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != h->device) cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    cudaFree(h->k_canon);
+    cudaFree(h->k_tile);
+    cudaFree(h->k_tf32);
+    if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
+    delete h;
+}
+
+ks_status_t ks_get_pattern(ks_handle_t h, int64_t out[4]) {
+    if (!h || !out) return fail(KS_ERR_INVALID_ARG, "NULL argument");
+    out[0] = h->a; out[1] = h->b; out[2] = h->c; out[3] = h->d;
+    return ok();
+}
+
+ks_status_t ks_set_math(ks_handle_t h, ks_math_t m) {
+    if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (m != KS_MATH_FP32 && m != KS_MATH_TF32) return fail(KS_ERR_INVALID_ARG, "bad math %d", (int)m);
+    if (m == KS_MATH_TF32 && (h->b < 16 || h->c < 16))
+        return fail(KS_ERR_UNSUPPORTED, "TF32 needs b,c >= 16 (pattern has b=%lld c=%lld)",
+                    (long long)h->b, (long long)h->c);
+    h->math = m;
+    return ok();
+}
+
+ks_status_t ks_set_kernel(ks_handle_t h, ks_kernel_t k) {
+    if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (k < KS_KERNEL_AUTO || k > KS_KERNEL_TF32) return fail(KS_ERR_INVALID_ARG, "bad kernel %d", (int)k);
+    h->forced = k;
+    return ok();
+}
+
+ks_status_t ks_plan(ks_handle_t h, int64_t B, ks_layout_t layout, ks_kernel_t* out) {
+    if (!h || !out || B < 0) return fail(KS_ERR_INVALID_ARG, "bad argument");
+    if (layout != KS_LAYOUT_BSF && layout != KS_LAYOUT_BSL) return fail(KS_ERR_INVALID_ARG, "bad layout");
+    // Plans assume 256-byte aligned (allocator) pointers.
+    KsCall call{reinterpret_cast<const float*>(uintptr_t(256)), reinterpret_cast<float*>(uintptr_t(256)),
+                B, (int)layout, nullptr};
+    ks_kernel_t k = choose(*h, call);
+    if (k == KS_KERNEL_AUTO) return fail(KS_ERR_UNSUPPORTED, "forced kernel cannot run this call");
+    *out = k;
+    return ok();
+}
+
+ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B, ks_layout_t layout,
+                      ks_stream_t stream) {
+    if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (B < 0) return fail(KS_ERR_INVALID_ARG, "B must be >= 0");
+    if (layout != KS_LAYOUT_BSF && layout != KS_LAYOUT_BSL) return fail(KS_ERR_INVALID_ARG, "bad layout %d", (int)layout);
+    ks_status_t s = check_device(h);
+    if (s != KS_OK) return s;
+    if (B == 0) return ok();
+    if (!X || !Y) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 3)
+        return fail(KS_ERR_ALIGNMENT, "X and Y must be 4-byte aligned");
+    int64_t xb, yb;
+    if (!mul_ok(B, h->N * 4, &xb) || !mul_ok(B, h->M * 4, &yb)) return fail(KS_ERR_INVALID_ARG, "B too large");
+    if (overlap(X, xb, Y, yb)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
+    s = run_one(*h, X, Y, B, layout, static_cast<cudaStream_t>(stream));
+    return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_chain_ex(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
+                        ks_layout_t layout, ks_stream_t stream) {
+    ks_status_t s = validate_chain(hs, L, B, (int)layout);
+    if (s != KS_OK) return s;
+    if (B == 0) return ok();
+    if (!X || !Y) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 3)
+        return fail(KS_ERR_ALIGNMENT, "X and Y must be 4-byte aligned");
+    if (overlap(X, B * hs[L - 1]->N * 4, Y, B * hs[0]->M * 4)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
+    s = run_chain(hs, L, X, Y, B, (int)layout, static_cast<cudaStream_t>(stream));
+    return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
+                     ks_stream_t stream) {
+    return ks_chain_ex(hs, L, X, Y, B, KS_LAYOUT_BSF, stream);
+}
+
+ks_status_t ks_chain_host(const ks_handle_t* hs, int L, const float* Xh, float* Yh, int64_t B,
+                          ks_layout_t layout, ks_stream_t stream) {
+    ks_status_t s = validate_chain(hs, L, B, (int)layout);
+    if (s != KS_OK) return s;
+    if (B == 0) return ok();
+    if (!Xh || !Yh) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaMemPool_t pool;
+    cudaError_t e = get_pool(hs[0]->device, &pool);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
+    const size_t xbytes = sizeof(float) * (size_t)(B * hs[L - 1]->N);
+    const size_t ybytes = sizeof(float) * (size_t)(B * hs[0]->M);
+    void *dX = nullptr, *dY = nullptr;
+    if ((e = cudaMallocFromPoolAsync(&dX, xbytes, pool, st)) != cudaSuccess) return fail_cuda(e, "staging X");
+    if ((e = cudaMallocFromPoolAsync(&dY, ybytes, pool, st)) != cudaSuccess) {
+        cudaFreeAsync(dX, st);
+        return fail_cuda(e, "staging Y");
+    }
+    e = cudaMemcpyAsync(dX, Xh, xbytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        s = run_chain(hs, L, static_cast<const float*>(dX), static_cast<float*>(dY), B, (int)layout, st);
+        if (s == KS_OK) e = cudaMemcpyAsync(Yh, dY, ybytes, cudaMemcpyDeviceToHost, st);
+    }
+    cudaFreeAsync(dX, st);
+    cudaFreeAsync(dY, st);
+    if (e != cudaSuccess) return fail_cuda(e, "host<->device copy");
+    return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst, int64_t count) {
+    if (!h || !dst) return fail(KS_ERR_INVALID_ARG, "NULL argument");
+    if (count != h->nnz) return fail(KS_ERR_INVALID_ARG, "count must be a*b*c*d = %lld", (long long)h->nnz);
+    const float* src = variant == 0 ? h->k_canon : variant == 1 ? h->k_tile : variant == 2 ? h->k_tf32 : nullptr;
+    if (!src) return fail(KS_ERR_INVALID_ARG, "variant must be 0, 1 or 2");
+    cudaError_t e = cudaMemcpy(dst, src, sizeof(float) * (size_t)count, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail_cuda(e, "ks_read_packed");
+    return ok();
+}
+
+ks_status_t ks_last_error(void) { return t_status; }
+const char* ks_last_error_message(void) { return t_msg; }
+
+const char* ks_status_string(ks_status_t s) {
+    switch (s) {
+        case KS_OK: return "KS_OK";
+        case KS_ERR_INVALID_ARG: return "KS_ERR_INVALID_ARG";
+        case KS_ERR_PATTERN: return "KS_ERR_PATTERN";
+        case KS_ERR_CHAIN_SHAPE: return "KS_ERR_CHAIN_SHAPE";
+        case KS_ERR_UNSUPPORTED: return "KS_ERR_UNSUPPORTED";
+        case KS_ERR_DEVICE: return "KS_ERR_DEVICE";
+        case KS_ERR_ALIGNMENT: return "KS_ERR_ALIGNMENT";
+        case KS_ERR_OOM: return "KS_ERR_OOM";
+        case KS_ERR_CUDA: return "KS_ERR_CUDA";
+    }
+    return "KS_ERR_UNKNOWN";
+}
+
+uint64_t ks_kernel_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+int ks_abi_version(void) { return KS_ABI_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+"""Thin Python binding of libks.so (include/ks.h).  Argument marshalling only:
+every step of the KS path runs in the library's CUDA kernels.  PyTorch
+supplies device memory and streams.
+
+There is no CPU fallback: if libks.so is missing or cannot run on the current
+device, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libks.so")
+
+BSF, BSL = 0, 1
+MATH_FP32, MATH_TF32 = 0, 1
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STREAM, KERNEL_FFMA, KERNEL_TF32 = range(5)
+KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32"}
+
+STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_CHAIN_SHAPE",
+          4: "KS_ERR_UNSUPPORTED", 5: "KS_ERR_DEVICE", 6: "KS_ERR_ALIGNMENT", 7: "KS_ERR_OOM",
+          8: "KS_ERR_CUDA"}
+
+# Every symbol include/ks.h declares (tests check the .so exports them all).
+EXPORTS = ["ks_pack_weights", "ks_free", "ks_get_pattern", "ks_set_math", "ks_set_kernel",
+           "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_chain_host", "ks_read_packed",
+           "ks_last_error", "ks_last_error_message", "ks_status_string",
+           "ks_kernel_launch_count", "ks_abi_version"]
+
+
+class KSError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libks.so and declare the ABI.  Raises loudly if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libks.so not built ({path}); run `python -m paper_2405_15013_b200.build`")
+    lib = ctypes.CDLL(path)
+    i64, vp, fp = ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p
+    st = ctypes.c_int
+    lib.ks_pack_weights.argtypes = [i64, i64, i64, i64, fp]
+    lib.ks_pack_weights.restype = vp
+    lib.ks_free.argtypes = [vp]
+    lib.ks_free.restype = None
+    lib.ks_get_pattern.argtypes = [vp, ctypes.POINTER(i64)]
+    lib.ks_get_pattern.restype = st
+    lib.ks_set_math.argtypes = [vp, ctypes.c_int]
+    lib.ks_set_math.restype = st
+    lib.ks_set_kernel.argtypes = [vp, ctypes.c_int]
+    lib.ks_set_kernel.restype = st
+    lib.ks_plan.argtypes = [vp, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    lib.ks_plan.restype = st
+    lib.ks_matmul.argtypes = [vp, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_matmul.restype = st
+    lib.ks_chain.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, vp]
+    lib.ks_chain.restype = st
+    lib.ks_chain_ex.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_chain_ex.restype = st
+    lib.ks_chain_host.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_chain_host.restype = st
+    lib.ks_read_packed.argtypes = [vp, ctypes.c_int, fp, i64]
+    lib.ks_read_packed.restype = st
+    lib.ks_last_error.argtypes = []
+    lib.ks_last_error.restype = st
+    lib.ks_last_error_message.argtypes = []
+    lib.ks_last_error_message.restype = ctypes.c_char_p
+    lib.ks_status_string.argtypes = [ctypes.c_int]
+    lib.ks_status_string.restype = ctypes.c_char_p
+    lib.ks_kernel_launch_count.argtypes = []
+    lib.ks_kernel_launch_count.restype = ctypes.c_uint64
+    lib.ks_abi_version.argtypes = []
+    lib.ks_abi_version.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise KSError(status, _lib.ks_last_error_message().decode())
+
+
+def _layout(layout) -> int:
+    if layout in (BSF, "bsf", "BSF"):
+        return BSF
+    if layout in (BSL, "bsl", "BSL"):
+        return BSL
+    raise ValueError(f"layout must be 'bsf' or 'bsl', got {layout!r}")
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(load_library().ks_kernel_launch_count())
+
+
+class Factor:
+    """One packed KS factor (opaque handle of ks_pack_weights)."""
+
+    def __init__(self, a: int, b: int, c: int, d: int, K):
+        lib = load_library()
+        self.pattern = (int(a), int(b), int(c), int(d))
+        self.M = a * b * d
+        self.N = a * c * d
+        self.nnz = a * b * c * d
+        self._keep = None
+        if isinstance(K, np.ndarray):
+            arr = np.ascontiguousarray(K, dtype=np.float32).reshape(-1)
+            if arr.size != self.nnz:
+                raise ValueError(f"K must have a*b*c*d = {self.nnz} values")
+            ptr = arr.ctypes.data
+            self._keep = arr
+        else:  # torch tensor (host or device)
+            if K.numel() != self.nnz or not K.is_contiguous():
+                raise ValueError(f"K must be contiguous with a*b*c*d = {self.nnz} values")
+            import torch
+            if K.dtype != torch.float32:
+                raise TypeError("K must be float32")
+            ptr = K.data_ptr()
+        h = lib.ks_pack_weights(a, b, c, d, ctypes.c_void_p(ptr))
+        if not h:
+            _check(lib.ks_last_error())
+        self._h = ctypes.c_void_p(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_math(self, math: int):
+        _check(_lib.ks_set_math(self._h, int(math)))
+        return self
+
+    def set_kernel(self, kernel: int):
+        _check(_lib.ks_set_kernel(self._h, int(kernel)))
+        return self
+
+    def plan(self, B: int, layout="bsf") -> str:
+        out = ctypes.c_int(0)
+        _check(_lib.ks_plan(self._h, int(B), _layout(layout), ctypes.byref(out)))
+        return KERNEL_NAMES[out.value]
+
+    def get_pattern(self):
+        out = (ctypes.c_int64 * 4)()
+        _check(_lib.ks_get_pattern(self._h, out))
+        return tuple(out)
+
+    def read_packed(self, variant: int) -> np.ndarray:
+        out = np.empty(self.nnz, dtype=np.float32)
+        _check(_lib.ks_read_packed(self._h, int(variant), ctypes.c_void_p(out.ctypes.data), self.nnz))
+        return out
+
+    def free(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.ks_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _dev_ptr(t, what):
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None):
+    """Y = X K^T through ks_matmul.  X: CUDA float32, (B, N) for BSF or (N, B) for BSL."""
+    import torch
+    lay = _layout(layout)
+    if B is None:
+        B = X.shape[0] if lay == BSF else X.shape[1]
+    if Y is None:
+        Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=torch.float32)
+    _check(_lib.ks_matmul(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), int(B), lay, _stream_ptr(stream)))
+    return Y
+
+
+def _handles(factors):
+    arr = (ctypes.c_void_p * len(factors))(*[f.handle.value for f in factors])
+    return arr
+
+
+def chain(factors, X, Y=None, layout="bsf", stream=None):
+    """Y = X K_L^T ... K_1^T through ks_chain_ex; factors in paper order K_1..K_L."""
+    import torch
+    lay = _layout(layout)
+    B = X.shape[0] if lay == BSF else X.shape[1]
+    M = factors[0].M
+    if Y is None:
+        Y = torch.empty((B, M) if lay == BSF else (M, B), device=X.device, dtype=torch.float32)
+    _check(_lib.ks_chain_ex(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"),
+                            int(B), lay, _stream_ptr(stream)))
+    return Y
+
+
+def chain_host(factors, X_host, Y_host, layout="bsf", stream=None):
+    """ks_chain_host: host X in, host Y out (copies enqueued on `stream`)."""
+    lay = _layout(layout)
+    B = X_host.shape[0] if lay == BSF else X_host.shape[1]
+    for t, w in ((X_host, "X_host"), (Y_host, "Y_host")):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{w} must be a contiguous host tensor")
+    _check(_lib.ks_chain_host(_handles(factors), len(factors), ctypes.c_void_p(X_host.data_ptr()),
+                              ctypes.c_void_p(Y_host.data_ptr()), int(B), lay, _stream_ptr(stream)))
+    return Y_host

@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path through the C ABI vs the FP64 CPU oracle.
+
+Contract (north star): normwise error max|Y^-Y|/max|Y| <= 1e-5
+for FP32 (5e-3 for TF32), every element inside the O-6 envelope, and
+bit-exact results on small-integer data, one-hot probes and packed index maps.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import ksgen
+from ksgen import configs
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+FP32_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ksb():
+    import paper_2405_15013_b200 as ksb
+    ksb.load_library()          # raises if libks.so is missing: no fallback
+    return ksb
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+def run(ksb, f, X_bsf, layout):
+    """Run ks_matmul in `layout` on BSF host data; return BSF host result."""
+    if layout == "bsf":
+        Y = ksb.matmul(f, to_dev(X_bsf), layout="bsf")
+        torch.cuda.synchronize()
+        return Y.cpu().numpy()
+    Y = ksb.matmul(f, to_dev(ksgen.to_bsl(X_bsf)), layout="bsl")
+    torch.cuda.synchronize()
+    return Y.cpu().numpy().T
+
+
+def check_fp32(Yg, Yref, env, c):
+    err = O.normwise_error(Yg, Yref)
+    assert err <= FP32_TOL, err
+    bound = O.envelope_delta(c, 0.0) * env
+    assert np.all(np.abs(Yg.astype(np.float64) - Yref) <= bound + 1e-300), "outside envelope"
+    return err
+
+
+TINY = list(itertools.product(range(1, 5), repeat=4))
+
+
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+def test_exhaustive_tiny_patterns(ksb, kernel):
+    """All 256 patterns with a,b,c,d in {1..4} x B in {1,7,8,33} x both layouts."""
+    for p in TINY:
+        a, b, c, d = p
+        M, N, _ = O.dims(p)
+        K4 = ksgen.k4_uniform(*p, seed=1000 + a + 4 * b)
+        X = ksgen.x_normal(33, N, seed=0)
+        Yref, env = O.matmul(p, K4, X, want_env=True)
+        f = ksb.Factor(*p, K4)
+        if kernel == "generic":
+            f.set_kernel(ksb.KERNEL_GENERIC)
+        for B in (1, 7, 8, 33):
+            for layout in ("bsf", "bsl"):
+                Yg = run(ksb, f, X[:B], layout)
+                check_fp32(Yg, Yref[:B], env[:B], c)
+
+
+@pytest.mark.parametrize("p", [(2, 4, 4, 2), (2, 4, 4, 4), (4, 4, 4, 2), (1, 2, 2, 1), (3, 3, 5, 7),
+                               (2048, 2, 2, 1), (1, 2, 2, 2048), (5, 1, 1, 3), (1, 1, 9, 1), (1, 9, 1, 4)])
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+def test_integer_data_bit_exact(ksb, p, layout):
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_int(*p, seed=2001)
+    for B in (1, 5, 64):
+        X = ksgen.x_int(B, N, seed=2000)
+        Yref = O.matmul(p, K4, X)
+        f = ksb.Factor(*p, K4)
+        for kern in (ksb.KERNEL_AUTO, ksb.KERNEL_GENERIC):
+            f.set_kernel(kern)
+            assert np.array_equal(run(ksb, f, X, layout).astype(np.float64), Yref)
+
+
+@pytest.mark.parametrize("p", [(2, 3, 2, 3), (2, 4, 4, 2), (3, 2, 2, 5), (1, 4, 4, 8)])
+def test_one_hot_probe_reads_support(ksb, p):
+    """X = I_N reveals K^T exactly: device support and value mapping."""
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_labels(*p)
+    D = O.dense(p, K4)
+    f = ksb.Factor(*p, K4)
+    for layout in ("bsf", "bsl"):
+        assert np.array_equal(run(ksb, f, np.eye(N, dtype=np.float32), layout), D.T)
+
+
+@pytest.mark.parametrize("p", [(2, 3, 2, 3), (1, 48, 48, 4), (3, 16, 32, 2)])
+def test_packed_layouts_bit_exact(ksb, p):
+    a, b, c, d = p
+    K4 = ksgen.k4_uniform(*p, seed=7)
+    f = ksb.Factor(*p, K4)
+    assert np.array_equal(f.read_packed(0), K4.reshape(-1))
+    Kb = O.bmm_weights(p, K4)                                  # (ad, b, c)
+    assert np.array_equal(f.read_packed(1), Kb.transpose(0, 2, 1).astype(np.float32).reshape(-1))
+    assert np.array_equal(f.read_packed(2).view(np.uint32),
+                          O.round_tf32_rna(Kb.astype(np.float32)).view(np.uint32).reshape(-1))
+
+
+def test_fft_chain_full_size_sampled_rows(ksb):
+    """configs[1] in bench.py's launch configuration (B=8192, BSF, ks_chain):
+    sampled rows vs the oracle computed row by row."""
+    L, B = configs.FFT_L, configs.FFT_BATCH
+    pats = configs.dyadic_patterns(L)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    X = ksgen.x_normal(B, 2 ** L, seed=0)
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    Y = ksb.chain(fs, to_dev(X))
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 2, 3, 4095, 4096, 8190, 8191] + list(np.random.default_rng(1).integers(0, B, 8)))
+    Yref, env = O.chain(pats, K4s, X, rows=rows, want_env=True)
+    Yg = Y.cpu().numpy()[rows]
+    err = O.normwise_error(Yg, Yref)
+    assert err <= FP32_TOL, err
+    delta = O.envelope_delta(2, 0.0)
+    assert np.all(np.abs(Yg - Yref) <= ((1 + delta) ** L - 1) * env)
+
+
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+@pytest.mark.parametrize("L", [1, 3, 8, 12])
+def test_hadamard_chain_bit_exact(ksb, L, layout):
+    pats, K4s = O.hadamard_factors(L)
+    N = 2 ** L
+    X = ksgen.x_int(37, N, seed=2002)
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    Xd = to_dev(X if layout == "bsf" else ksgen.to_bsl(X))
+    Y = ksb.chain(fs, Xd, layout=layout)
+    torch.cuda.synchronize()
+    Yg = Y.cpu().numpy() if layout == "bsf" else Y.cpu().numpy().T
+    assert np.array_equal(Yg.astype(np.float64), O.chain(pats, K4s, X))
+
+
+def test_dft_chain_real_imag_split_matches_numpy_fft(ksb):
+    """Fig. 1 worked example on the GPU: complex factors split into real
+    handles, two real ks_matmul launches per factor on the stacked batch."""
+    L, B = 12, 16
+    N = 2 ** L
+    pats, K4c = O.dft_factors(L)
+    Zr = ksgen.x_normal(B, N, seed=20)
+    Zi = ksgen.x_normal(B, N, seed=21)
+    ref = np.fft.fft((Zr.astype(np.float64) + 1j * Zi)[:, O.bitrev(L)], axis=1)
+    Z = to_dev(np.concatenate([Zr, Zi]))
+    for p, K in zip(reversed(pats), reversed(K4c)):
+        Kr, Ki = O.split_complex_factor(K)
+        U = ksb.matmul(ksb.Factor(*p, Kr), Z)
+        V = ksb.matmul(ksb.Factor(*p, Ki), Z)
+        Z = torch.cat([U[:B] - V[B:], V[:B] + U[B:]])
+    torch.cuda.synchronize()
+    Zh = Z.cpu().numpy().astype(np.float64)
+    got = Zh[:B] + 1j * Zh[B:]
+    assert O.normwise_error(got, ref) < 1e-5
+
+
+@pytest.mark.parametrize("name", ["VIT_UP", "VIT_DOWN", "GPT2_DOWN", "GPT2_UP"])
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+def test_model_chains_small_batch(ksb, name, layout):
+    pats = getattr(configs, name)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    N = configs.chain_dims(pats)[0]
+    B = 67
+    X = ksgen.x_normal(B, N, seed=0)
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    Xd = to_dev(X if layout == "bsf" else ksgen.to_bsl(X))
+    Y = ksb.chain(fs, Xd, layout=layout)
+    torch.cuda.synchronize()
+    Yg = Y.cpu().numpy() if layout == "bsf" else Y.cpu().numpy().T
+    assert O.normwise_error(Yg, O.chain(pats, K4s, X)) <= FP32_TOL
+
+
+def test_chain_host_equals_device(ksb):
+    pats = configs.dyadic_patterns(10)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    X = ksgen.x_normal(300, 1024, seed=0)
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh = torch.empty((300, 1024), dtype=torch.float32).pin_memory()
+    ksb.chain_host(fs, Xh, Yh)
+    torch.cuda.synchronize()
+    Yd = ksb.chain(fs, to_dev(X))
+    torch.cuda.synchronize()
+    assert np.array_equal(Yh.numpy(), Yd.cpu().numpy())
+
+
+def test_deterministic_and_misaligned(ksb):
+    p = (4, 2, 2, 16)
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_uniform(*p, seed=3)
+    f = ksb.Factor(*p, K4)
+    X = ksgen.x_normal(129, N, seed=4)
+    Y1 = run(ksb, f, X, "bsf")
+    Y2 = run(ksb, f, X, "bsf")
+    assert np.array_equal(Y1, Y2)
+    # 4-byte but not 16-byte aligned views take the narrower vector path
+    buf = torch.zeros(129 * N + 1, device=dev())
+    buf[1:].copy_(to_dev(X).reshape(-1))
+    Xv = buf[1:].view(129, N)
+    out = torch.zeros(129 * M + 1, device=dev())
+    Yv = out[1:].view(129, M)
+    ksb.matmul(f, Xv, Yv)
+    torch.cuda.synchronize()
+    assert np.array_equal(Yv.cpu().numpy(), Y1)
+
+
+def test_edge_cases_and_errors(ksb):
+    p = (2, 2, 2, 2)
+    f = ksb.Factor(*p, ksgen.k4_uniform(*p, seed=1))
+    X = torch.zeros((0, 8), device=dev())
+    Y = torch.zeros((0, 8), device=dev())
+    ksb.matmul(f, X, Y)                                    # B = 0: no-op
+    X = torch.zeros((4, 8), device=dev())
+    with pytest.raises(ksb.KSError):                       # overlap
+        ksb.matmul(f, X, X)
+    g = ksb.Factor(1, 3, 3, 1, np.ones(9, np.float32))
+    with pytest.raises(ksb.KSError) as e:                  # not chainable
+        ksb.chain([f, g], torch.zeros((4, 3), device=dev()))
+    assert e.value.status == 3
+    with pytest.raises(ksb.KSError) as e:                  # TF32 needs b,c >= 16
+        f.set_math(ksb.MATH_TF32)
+    assert e.value.status == 4
+    f.set_kernel(ksb.KERNEL_STREAM)
+    h = ksb.Factor(1, 3, 3, 1, np.ones(9, np.float32)).set_kernel(ksb.KERNEL_STREAM)
+    with pytest.raises(ksb.KSError) as e:                  # forced family cannot run b=3
+        ksb.matmul(h, torch.zeros((4, 3), device=dev()))
+    assert e.value.status == 4
+    with pytest.raises(ksb.KSError):
+        ksb.Factor(0, 1, 1, 1, np.ones(1, np.float32))
+
+
+def test_plan_table(ksb):
+    f = ksb.Factor(2, 2, 2, 8, np.ones(64, np.float32))
+    assert f.plan(8192, "bsf") == "stream"
+    g = ksb.Factor(1, 3, 5, 2, np.ones(30, np.float32))
+    assert g.plan(8, "bsl") == "generic"

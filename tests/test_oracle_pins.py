@@ -342,3 +342,17 @@ def test_inputs_are_seeded_and_distributed():
     for pats in (configs.VIT_UP, configs.VIT_DOWN, configs.GPT2_UP, configs.GPT2_DOWN,
                  configs.dyadic_patterns(configs.FFT_L)):
         assert configs.chainable(pats)
+
+
+def test_round_tf32_rna():
+    """TF32 keeps 10 mantissa bits: representable values are fixed points, the
+    rounding error is <= 2^-11 relative, ties go away from zero."""
+    x = np.array([1.0, -3.5, 1 + 2 ** -10, 2.0 ** -20], np.float32)
+    assert np.array_equal(O.round_tf32_rna(x), x)
+    assert O.round_tf32_rna(np.float32(1 + 2 ** -11)) == np.float32(1 + 2 ** -10)     # tie away
+    assert O.round_tf32_rna(np.float32(-(1 + 2 ** -11))) == np.float32(-(1 + 2 ** -10))
+    assert O.round_tf32_rna(np.float32(1 + 2 ** -12)) == np.float32(1.0)
+    r = ksgen.x_normal(1, 100000, seed=3)[0]
+    t = O.round_tf32_rna(r)
+    assert np.all(np.abs(t.astype(np.float64) - r) <= 2.0 ** -11 * np.abs(r))
+    assert np.all((t.view(np.uint32) & np.uint32(0x1FFF)) == 0)
