@@ -189,47 +189,35 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(dev)
     flush = torch.empty(2 * props.L2_cache_size, dtype=torch.uint8, device=dev)
 
-    def step(evs=None):
-        """The chain, K_L first, each factor one fused launch."""
-        src = X
-        for t, l in enumerate(range(L - 1, -1, -1)):
-            n_out = dims[t + 1]
-            if l == 0:
-                dst = Y
-            else:
-                dst = bufs[t % 2].view(-1)[: B * n_out].view(shape(n_out))
-            if evs is not None:
-                evs[t][0].record(stream)
-            ksb.matmul(facs[l], src, dst, layout=lay, B=B)
-            if evs is not None:
-                evs[t][1].record(stream)
-            src = dst
+    def step():
+        """One pass of the hot path: the whole chain through the C ABI (ks_chain_ex)."""
+        ksb.chain(facs, X, Y, layout=lay)
 
-    # warm-up
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
 
     K = args.steps
     ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    ev_k = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
-            for _ in range(K)]
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    ksb.trace_enable(True)          # library-side CUDA events around every launch
     l0 = ksb.launch_count()
     t0 = time.time()
     for s in range(K):
         flush.fill_(s & 0xFF)                 # evict L2 between timed steps (not timed)
         ev_step[s][0].record(stream)
-        step(ev_k[s])
+        step()
         ev_step[s][1].record(stream)
     torch.cuda.synchronize()
     t1 = time.time()
     launches = ksb.launch_count() - l0
+    k_ms, k_fam, k_bytes = ksb.trace_read()
+    ksb.trace_enable(False)
     if world > 1:
         dist.barrier()
     time.sleep(0.1)
@@ -238,16 +226,12 @@ def run_ours(args):
 
     step_ms = [a.elapsed_time(b) for a, b in ev_step]
     tot_ms = sum(step_ms)
-    k_ms = [[a.elapsed_time(b) for a, b in row] for row in ev_k]
-    # dominant kernel: the factor family; all factors here run one family per plan
     plans = [facs[l].plan(B, lay) for l in range(L - 1, -1, -1)]
-    per_factor_bytes = [model_bytes(pats[l], B) for l in range(L - 1, -1, -1)]
     fam_time, fam_bytes, fam_n = {}, {}, {}
-    for s in range(K):
-        for t in range(L):
-            fam_time[plans[t]] = fam_time.get(plans[t], 0.0) + k_ms[s][t]
-            fam_bytes[plans[t]] = fam_bytes.get(plans[t], 0) + per_factor_bytes[t]
-            fam_n[plans[t]] = fam_n.get(plans[t], 0) + 1
+    for ms_, f_, b_ in zip(k_ms, k_fam, k_bytes):
+        fam_time[f_] = fam_time.get(f_, 0.0) + float(ms_)
+        fam_bytes[f_] = fam_bytes.get(f_, 0.0) + float(b_)
+        fam_n[f_] = fam_n.get(f_, 0) + 1
     dom = max(fam_time, key=fam_time.get)
 
     tot_t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
@@ -281,22 +265,10 @@ def run_ours(args):
                "unit": "GB/s", "h2d_bytes_per_step": int(Xh.numel() * 4),
                "d2h_bytes_per_step": int(Yh.numel() * 4), "api": "ks_chain_host", "steps": ke}
         # the e2e result must equal the device-resident one
-        if world == 1:
-            step()
-            torch.cuda.synchronize()
-            if not torch.equal(Yh, Y.cpu()):
-                raise RuntimeError("e2e result differs from device-resident result")
-
-    # chain API device-resident timing (same launches as `step`, via ks_chain_ex)
-    kc = min(K, 50)
-    evc = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kc)]
-    for s in range(kc):
-        flush.fill_(s & 0xFF)
-        evc[s][0].record(stream)
-        ksb.chain(facs, X, Y, layout=lay)
-        evc[s][1].record(stream)
-    torch.cuda.synchronize()
-    chain_api_ms = statistics.median(a.elapsed_time(b) for a, b in evc)
+        step()
+        torch.cuda.synchronize()
+        if not torch.equal(Yh, Y.cpu()):
+            raise RuntimeError("e2e result differs from device-resident result")
 
     if rank != 0:
         if world > 1:
@@ -328,7 +300,7 @@ def run_ours(args):
                      "share_of_step": round(fam_time[dom] / tot_ms, 4)},
         "gpu_launches": int(launches),
         "launches_per_step": launches / K,
-        "chain_api_ms_per_step": round(chain_api_ms, 5),
+        "kernel_ms_per_step": round(sum(fam_time.values()) / K, 5),
         "clocks": clocks,
         "e2e": e2e,
         "plans": plans,
@@ -345,18 +317,20 @@ def run_ours(args):
 
 
 def cpu_baseline(pats, K4s, X_host, B, budget_s=15.0):
-    """The oracle as it stands, on this host's cores, on a bounded row sample."""
+    """The oracle as it stands, on this host's cores, on a bounded row sample
+    (rows doubled until one timed run takes >= budget/3 seconds)."""
     import oracle
     import numpy as np
     threads = oracle.default_threads()
-    t = time.time()
-    oracle.chain(pats, K4s, X_host, rows=[0], threads=threads)
-    t1 = max(time.time() - t, 1e-3)
-    R = int(max(1, min(B, budget_s / t1)))
-    rows = np.arange(R)
-    t = time.time()
-    oracle.chain(pats, K4s, X_host, rows=rows, threads=threads)
-    dt = time.time() - t
+    oracle.chain(pats, K4s, X_host, rows=[0], threads=threads)      # warm (page-in, build)
+    R = 1
+    while True:
+        t = time.time()
+        oracle.chain(pats, K4s, X_host, rows=np.arange(R), threads=threads)
+        dt = time.time() - t
+        if dt >= budget_s / 3 or R >= B or dt * 2.2 > budget_s:
+            break
+        R = min(B, R * 2)
     byts = sum(model_bytes(p, R) for p in pats)
     return {"value": round(byts / dt / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{R} of {B} batch rows of the workload, FP64 naive dense triple loop (oracle/ks_oracle.c)",

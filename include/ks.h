@@ -153,6 +153,19 @@ ks_status_t ks_chain_host(const ks_handle_t* handles, int L, const float* X_host
  * (a*d*b*c floats).  count must equal the variant's element count.         */
 ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst_host, int64_t count);
 
+/* ---------------------------------------------------------------------------
+ * Launch tracing (profiling aid, off by default).  While enabled, every
+ * kernel launch the library makes is bracketed by a pair of CUDA events
+ * recorded on the launch stream, together with its kernel family and its
+ * algorithmic bytes 4*(B*N + a*b*c*d + B*M) (the paper's byte model, read X +
+ * nnz(K) + write Y).  ks_trace_enable(1) clears the buffer.
+ * ks_trace_read synchronises on the recorded events and copies up to `max`
+ * records (oldest first) into the caller's host arrays (any may be NULL),
+ * stores the number available in *count, then clears the buffer.           */
+ks_status_t ks_trace_enable(int on);
+ks_status_t ks_trace_read(int64_t max, int64_t* count, float* ms, int* family,
+                          double* model_bytes);
+
 /* Diagnostics. */
 ks_status_t ks_last_error(void);                /* per host thread           */
 const char* ks_last_error_message(void);        /* per host thread, static   */

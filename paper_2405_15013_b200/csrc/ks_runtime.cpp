@@ -18,6 +18,28 @@ thread_local char t_msg[512] = "ok";
 
 std::atomic<uint64_t> g_launches{0};
 
+// ---- launch tracing -----------------------------------------------------------
+struct TraceRec {
+    cudaEvent_t start, stop;
+    int family;
+    double bytes;
+};
+std::mutex g_trace_mu;
+std::atomic<bool> g_trace_on{false};
+std::vector<TraceRec> g_trace;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t trace_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
 ks_status_t fail(ks_status_t s, const char* fmt, ...) {
     t_status = s;
     va_list ap;
@@ -118,8 +140,22 @@ ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, i
         return fail(KS_ERR_UNSUPPORTED, "forced kernel %d cannot run pattern (%lld,%lld,%lld,%lld) "
                     "B=%lld layout=%d", (int)h.forced, (long long)h.a, (long long)h.b,
                     (long long)h.c, (long long)h.d, (long long)B, layout);
+    TraceRec rec{nullptr, nullptr, (int)k, 0.0};
+    const bool tracing = g_trace_on.load(std::memory_order_relaxed);
+    if (tracing) {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        rec.start = trace_event();
+        rec.stop = trace_event();
+        rec.bytes = 4.0 * ((double)B * (double)h.N + (double)h.nnz + (double)B * (double)h.M);
+        cudaEventRecord(rec.start, s);
+    }
     cudaError_t e = launch(k, h, call);
     if (e == cudaSuccess) e = cudaGetLastError();
+    if (tracing) {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        cudaEventRecord(rec.stop, s);
+        g_trace.push_back(rec);
+    }
     if (e != cudaSuccess) return fail_cuda(e, "kernel launch");
     return KS_OK;
 }
@@ -366,6 +402,40 @@ ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst, int64_t count
     cudaError_t e = cudaMemcpy(dst, src, sizeof(float) * (size_t)count, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail_cuda(e, "ks_read_packed");
     return ok();
+}
+
+ks_status_t ks_trace_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    for (auto& r : g_trace) {
+        g_event_pool.push_back(r.start);
+        g_event_pool.push_back(r.stop);
+    }
+    g_trace.clear();
+    g_trace_on.store(on != 0);
+    return ok();
+}
+
+ks_status_t ks_trace_read(int64_t max, int64_t* count, float* ms, int* family, double* bytes) {
+    if (max < 0) return fail(KS_ERR_INVALID_ARG, "max must be >= 0");
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    if (count) *count = (int64_t)g_trace.size();
+    ks_status_t st = KS_OK;
+    for (size_t t = 0; t < g_trace.size(); ++t) {
+        TraceRec& r = g_trace[t];
+        if ((int64_t)t < max) {
+            float v = 0.f;
+            cudaError_t e = cudaEventSynchronize(r.stop);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&v, r.start, r.stop);
+            if (e != cudaSuccess && st == KS_OK) st = fail_cuda(e, "ks_trace_read");
+            if (ms) ms[t] = v;
+            if (family) family[t] = r.family;
+            if (bytes) bytes[t] = r.bytes;
+        }
+        g_event_pool.push_back(r.start);
+        g_event_pool.push_back(r.stop);
+    }
+    g_trace.clear();
+    return st == KS_OK ? ok() : st;
 }
 
 ks_status_t ks_last_error(void) { return t_status; }

@@ -27,6 +27,7 @@ STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_C
 # Every symbol include/ks.h declares (tests check the .so exports them all).
 EXPORTS = ["ks_pack_weights", "ks_free", "ks_get_pattern", "ks_set_math", "ks_set_kernel",
            "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_chain_host", "ks_read_packed",
+           "ks_trace_enable", "ks_trace_read",
            "ks_last_error", "ks_last_error_message", "ks_status_string",
            "ks_kernel_launch_count", "ks_abi_version"]
 
@@ -72,6 +73,10 @@ def load_library(path: str = LIB_PATH):
     lib.ks_chain_host.restype = st
     lib.ks_read_packed.argtypes = [vp, ctypes.c_int, fp, i64]
     lib.ks_read_packed.restype = st
+    lib.ks_trace_enable.argtypes = [ctypes.c_int]
+    lib.ks_trace_enable.restype = st
+    lib.ks_trace_read.argtypes = [i64, ctypes.POINTER(i64), vp, vp, vp]
+    lib.ks_trace_read.restype = st
     lib.ks_last_error.argtypes = []
     lib.ks_last_error.restype = st
     lib.ks_last_error_message.argtypes = []
@@ -110,6 +115,24 @@ def launch_count() -> int:
     return int(load_library().ks_kernel_launch_count())
 
 
+def trace_enable(on: bool = True):
+    """Start (clears) / stop the library's per-launch event tracing."""
+    _check(load_library().ks_trace_enable(1 if on else 0))
+
+
+def trace_read(max_records: int = 1 << 20):
+    """(ms, family_name, model_bytes) per traced launch, oldest first; clears."""
+    lib = load_library()
+    cnt = ctypes.c_int64(0)
+    ms = np.zeros(max_records, np.float32)
+    fam = np.zeros(max_records, np.int32)
+    byt = np.zeros(max_records, np.float64)
+    _check(lib.ks_trace_read(max_records, ctypes.byref(cnt), ctypes.c_void_p(ms.ctypes.data),
+                             ctypes.c_void_p(fam.ctypes.data), ctypes.c_void_p(byt.ctypes.data)))
+    n = min(int(cnt.value), max_records)
+    return ms[:n], [KERNEL_NAMES[int(f)] for f in fam[:n]], byt[:n]
+
+
 class Factor:
     """One packed KS factor (opaque handle of ks_pack_weights)."""
 
@@ -120,6 +143,9 @@ class Factor:
         self.N = a * c * d
         self.nnz = a * b * c * d
         self._keep = None
+        if min(self.pattern) < 1:      # let the library report KS_ERR_PATTERN
+            h = lib.ks_pack_weights(a, b, c, d, None)
+            _check(lib.ks_last_error())
         if isinstance(K, np.ndarray):
             arr = np.ascontiguousarray(K, dtype=np.float32).reshape(-1)
             if arr.size != self.nnz:

@@ -247,3 +247,64 @@ def test_plan_table(ksb):
     assert f.plan(8192, "bsf") == "stream"
     g = ksb.Factor(1, 3, 5, 2, np.ones(30, np.float32))
     assert g.plan(8, "bsl") == "generic"
+
+
+# ---------------------------------------------------------- FFMA kernel ----
+GEMMLIKE = [(1, 48, 48, 1), (1, 64, 64, 2), (2, 96, 96, 4), (1, 128, 128, 3), (3, 64, 64, 16),
+            (1, 48, 48, 64), (6, 64, 64, 1), (1, 768, 192, 2), (6, 64, 256, 1), (64, 64, 64, 1),
+            (1, 64, 256, 16), (1, 256, 64, 16), (2, 32, 16, 4), (1, 24, 8, 5), (2, 192, 48, 2)]
+
+
+@pytest.mark.parametrize("p", GEMMLIKE)
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+def test_ffma_matches_oracle_and_generic(ksb, p, layout):
+    """Register-tiled kernel: same FMA order as the generic kernel (bit-equal)
+    and within the FP32 contract of the oracle; ragged batch tails."""
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_uniform(*p, seed=1000 + p[1])
+    X = ksgen.x_normal(300, N, seed=0)
+    f = ksb.Factor(*p, K4)
+    assert f.plan(300, layout) == "ffma"
+    f.set_kernel(ksb.KERNEL_FFMA)
+    Yf = run(ksb, f, X, layout)
+    f.set_kernel(ksb.KERNEL_GENERIC)
+    Yg = run(ksb, f, X, layout)
+    assert np.array_equal(Yf, Yg)
+    rows = np.arange(300) if M * N <= 1 << 22 else np.array([0, 1, 63, 64, 127, 128, 255, 256, 299])
+    Yref, env = O.matmul(p, K4, X, rows=rows, want_env=True)
+    check_fp32(Yf[rows], Yref, env, p[2])
+    if layout == "bsf":
+        f.set_kernel(ksb.KERNEL_FFMA)
+        for B in (1, 7):
+            assert np.array_equal(run(ksb, f, X[:B], layout), Yg[:B])
+
+
+@pytest.mark.parametrize("p", [(1, 128, 128, 64), (16, 48, 48, 4), (1, 96, 96, 1), (4, 64, 64, 16)])
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+def test_sweep_full_size_sampled_rows(ksb, p, layout):
+    """configs[2] at B = 25088 in bench's launch configuration (auto plan):
+    sampled rows against the oracle, computed one by one."""
+    B = configs.SWEEP_BATCH
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_uniform(*p, seed=1000)
+    X = ksgen.x_normal(B, N, seed=0)
+    f = ksb.Factor(*p, K4)
+    Yg = run(ksb, f, X, layout)
+    rows = np.array([0, 1, 2, 127, 128, 12543, 25086, 25087] + list(np.random.default_rng(2).integers(0, B, 4)))
+    Yref, env = O.matmul(p, K4, X, rows=rows, want_env=True)
+    check_fp32(Yg[rows], Yref, env, p[2])
+
+
+@pytest.mark.parametrize("name", ["VIT_UP", "GPT2_DOWN"])
+def test_model_chain_full_size_sampled_rows(ksb, name):
+    pats = getattr(configs, name)
+    B = configs.VIT_BATCH if name.startswith("VIT") else configs.GPT2_BATCH
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    N = configs.chain_dims(pats)[0]
+    X = ksgen.x_normal(B, N, seed=0)
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    Y = ksb.chain(fs, to_dev(X))
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, B // 2, B - 1])
+    Yref = O.chain(pats, K4s, X, rows=rows)
+    assert O.normwise_error(Y.cpu().numpy()[rows], Yref) <= FP32_TOL
