@@ -399,6 +399,13 @@ def round_tf32_rna(x) -> np.ndarray:
     return ((b + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
 
 
+def truncate_tf32(x) -> np.ndarray:
+    """TF32 value of float32 bits read by a tensor core that ignores the 13
+    low mantissa bits (round toward zero).  Finite inputs only."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    return (b & np.uint32(0xFFFFE000)).view(np.float32)
+
+
 def envelope_delta(c: int, u_in: float, u: float = 2.0 ** -24) -> float:
     """Per-hop relative factor delta = 2 u_in + u_in^2 + gamma_{2c}
     (SURVEY §8c O-6): standard order-independent summation bound with slack."""

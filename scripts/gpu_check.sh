@@ -19,6 +19,7 @@ if [[ $STAGES == *bench* ]]; then
 fi
 if [[ $STAGES == *sweep* ]]; then
   timeout 900 python bench_sweep.py fp32 > gpurun_out/sweep_fp32.json 2> gpurun_out/sweep.err
+  timeout 900 python bench_sweep.py tf32 > gpurun_out/sweep_tf32.json 2> gpurun_out/sweep_tf32.err
 fi
 if [[ $STAGES == *ncu* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \

@@ -356,3 +356,15 @@ def test_round_tf32_rna():
     t = O.round_tf32_rna(r)
     assert np.all(np.abs(t.astype(np.float64) - r) <= 2.0 ** -11 * np.abs(r))
     assert np.all((t.view(np.uint32) & np.uint32(0x1FFF)) == 0)
+
+
+def test_truncate_tf32():
+    """Truncation toward zero to 10 mantissa bits: |t| <= |x|, error < 2^-10 relative."""
+    x = np.array([1.0, -3.5, 1 + 2 ** -10], np.float32)
+    assert np.array_equal(O.truncate_tf32(x), x)
+    assert O.truncate_tf32(np.float32(1 + 2 ** -11 + 2 ** -12)) == np.float32(1.0)
+    assert O.truncate_tf32(np.float32(-(1 + 2 ** -11))) == np.float32(-1.0)
+    r = ksgen.x_normal(1, 100000, seed=4)[0]
+    t = O.truncate_tf32(r)
+    assert np.all(np.abs(t) <= np.abs(r))
+    assert np.all(np.abs(t.astype(np.float64) - r) < 2.0 ** -10 * np.abs(r))
