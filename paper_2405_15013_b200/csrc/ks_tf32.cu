@@ -2,34 +2,41 @@
 // for the GEMM-like patterns where each (i, j) block is a genuine dense
 // contraction (b, c >= 16; north star).  Not in the paper, whose kernel is
 // CUDA-core only: on B200 the FP32 FFMA path is ALU-bound
-// for b, c >= 48 (arithmetic intensity bc/(2(b+c)) > the FFMA ridge), so the
-// tensor cores turn these factors HBM-bound again.
+// for b, c >= 48 (arithmetic intensity bc/(2(b+c)) above the FFMA ridge), so
+// the tensor cores turn these factors HBM-bound again.
 //
-// One CTA owns the output tile Y[n0:n0+128, row_{i,j}[k0:k0+BN]]
-// (output-stationary, Alg. 3; written exactly once).
+// Work unit ("tile") = output block Y[n0:n0+128, row_{i,j}[k0:k0+BN]]
+// (output-stationary, Alg. 3; each element written once).
 //   UMMA view:  D[m][n] = sum_k A[m][k] B[n][k],  M = 128 batch rows,
 //               N = BN outputs (k index of the KS block), K = l (c).
-//   A = X[:, col_{i,j}]  -- BSL: MN-major (batch contiguous), BSF d=1: K-major
-//   B = K[row_{i,j}, col_{i,j}] from k_tf32 (pre-rounded RNA, [q][k][l], K-major)
-// Warp roles (160 threads):
-//   warps 0-3  producers: cp.async 16-byte chunks of the X and K tiles straight
-//              into the canonical no-swizzle UMMA smem layouts (core matrices
-//              of 8 rows x 16 B), STAGES-deep ring, mbarrier full/empty;
-//              then the epilogue: tcgen05.ld (32x32b) TMEM -> registers ->
-//              coalesced global stores in the caller's layout.
-//   warp 4     TMEM allocator + single-thread MMA issuer (tcgen05.mma,
-//              tcgen05.commit -> empty[stage] / accumulator-ready barrier).
-// X is fed as raw FP32 bits: the tensor core uses its TF32 part (truncation of
-// the 13 low mantissa bits); K is rounded to nearest at pack time.  FP32
-// accumulation.  Contract: normwise error <= 5e-3 (north star), DESIGN.md.
+//   A = X[n0:n0+128, col_{i,j}], B = K[row_{i,j}, col_{i,j}] (k_tf32,
+//   pre-rounded RNA at pack time, [q][k][l]); both K-major in shared memory
+//   in the canonical no-swizzle layout (8-row x 16-byte core matrices).
+//   (tcgen05 ignores the "MN-major" bit for kind::tf32 -- measured, see
+//   scripts/probe_umma.cu -- so batch-contiguous BSL tiles are transposed on
+//   the way in.)
+// Persistent CTAs (grid <= 2 per SM), tiles round-robin; warp roles
+// (288 threads):
+//   warps 0-3  producers: X and K chunks (128 x 32 l, BN x 32 l) into a
+//              STAGES-deep smem ring (mbarrier full/empty).  K and the
+//              ld-contiguous BSF X tile go by cp.async 16 B; BSL X is read
+//              as coalesced 4-byte columns and written transposed (STS.128).
+//   warp 4     TMEM allocator + single-thread MMA issuer (double-buffered
+//              accumulator: 2 x BN TMEM columns).
+//   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> coalesced global
+//              stores in the caller's layout, overlapping the next tile's MMAs.
+// X is fed as raw FP32 bits (the tensor core reads the TF32 part: truncation
+// of the 13 low mantissa bits); FP32 accumulation.  Contract: normwise error
+// <= 5e-3 (north star); DESIGN.md derives the per-element envelope.
 #include "ks_internal.h"
 
 namespace {
 
-constexpr int BM = 128;       // batch rows per CTA = UMMA M
+constexpr int BM = 128;       // batch rows per tile = UMMA M
 constexpr int BKC = 32;       // l per pipeline stage (4 UMMA k-steps of 8)
-constexpr int NPROD = 128;    // producer / epilogue threads
-constexpr int NTHREADS = NPROD + 32;
+constexpr int NPROD = 128;    // producer threads (warps 0-3)
+constexpr int NEPI = 128;     // epilogue threads (warps 5-8)
+constexpr int NTHREADS = NPROD + 32 + NEPI;
 
 // ---- PTX wrappers ----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -68,10 +75,12 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
 
-// Shared-memory matrix descriptor, no swizzle (canonical "interleave" layout):
-// start address, leading-dimension byte offset, stride-dimension byte offset,
-// version 1 (sm_100), layout type 0.
+// Shared-memory matrix descriptor, no swizzle: start, LBO, SBO, version 1.
 __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3FFF);
@@ -81,10 +90,9 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint3
     return d;
 }
 
-// Instruction descriptor: D f32, A/B tf32, A major (0 K, 1 MN), B K-major, N, M = 128.
-__host__ __device__ constexpr uint32_t make_idesc(int a_mn_major, int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn_major << 15) |
-           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// Instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128.
+__host__ __device__ constexpr uint32_t make_idesc(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
@@ -120,44 +128,54 @@ struct Tf32Cfg {
     static constexpr int A_BYTES = BM * BKC * 4;          // 16 KB
     static constexpr int B_BYTES = BN * BKC * 4;          // BN * 128 B
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (STAGE <= 32 * 1024) ? 3 : 2;
-    static constexpr int BAR_BYTES = 128;
+    static constexpr int STAGES = BN <= 64 ? 4 : BN <= 128 ? 3 : 2;
+    static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = STAGES * STAGE + BAR_BYTES;
-    static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                   : 2 * BN <= 256 ? 256 : 512;
+    static constexpr int CTAS_PER_SM = TMEM_COLS <= 256 ? 2 : 1;
     static_assert(BN % 16 == 0 && BN <= 256, "UMMA N for M=128");
 };
 
-// Smem layouts (byte offsets inside a stage), no swizzle, 16-byte chunks:
-//  K-major tile (rows r, K index l in [0,32)):   (r/8)*1024 + (l/4)*128 + (r%8)*16 + (l%4)*4
-//      -> LBO (next 4-l chunk) = 128, SBO (next 8-row group) = 1024
-//  MN-major A tile (rows m, l):                   (m/4)*512 + (l/8)*128 + (l%8)*16 + (m%4)*4
-//      -> LBO (next 8-l group) = 128, SBO (next 4-row chunk) = 512
+struct TileCoord {
+    int i, j, k0;
+    int64_t n0;
+    int64_t q;
+};
+
+__device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, int d, int BN) {
+    TileCoord t;
+    const int kc = (int)(tile % nkc);
+    tile /= nkc;
+    t.n0 = (tile % nnb) * BM;
+    t.q = tile / nnb;
+    t.i = (int)(t.q / d);
+    t.j = (int)(t.q % d);
+    t.k0 = kc * BN;
+    return t;
+}
+
+// K-major smem tile (rows r, K index l in [0,32)):  (r/8)*1024 + (l/4)*128 + (r%8)*16 + (l%4)*4
+//   -> LBO (next 4-l chunk) = 128 B, SBO (next 8-row group) = 1024 B.
 template <int LAYOUT, int BN>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<BN>::CTAS_PER_SM)
 ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, float* __restrict__ Y,
-               int64_t B, int a, int b, int c, int d) {
+               int64_t B, int a, int b, int c, int d, int64_t ntiles) {
     using C = Tf32Cfg<BN>;
     constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::STAGE);
-    // bars[0..S): full, bars[S..2S): empty, bars[2S]: accumulator ready, bars[2S+1] (low 32 bits): tmem base
+    // [0,S) full  [S,2S) empty  [2S,2S+2) acc_full  [2S+2,2S+4) acc_empty  [2S+4] tmem slot
     const uint32_t full0 = smem_u32(&bars[0]);
     const uint32_t empty0 = smem_u32(&bars[S]);
-    const uint32_t accb = smem_u32(&bars[2 * S]);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 1]);
+    const uint32_t accf0 = smem_u32(&bars[2 * S]);
+    const uint32_t acce0 = smem_u32(&bars[2 * S + 2]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4]);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int nkc = b / BN;
     const int64_t nnb = (B + BM - 1) / BM;
-    int64_t bid = blockIdx.x;
-    const int kc = (int)(bid % nkc);
-    bid /= nkc;
-    const int64_t nb = bid % nnb;
-    const int64_t q = bid / nnb;                 // q = i*d + j
-    const int i = (int)(q / d), j = (int)(q % d);
-    const int k0 = kc * BN;
-    const int64_t n0 = nb * BM;
     const int64_t N = (int64_t)a * c * d, M = (int64_t)a * b * d;
     const int nk = (c + BKC - 1) / BKC;
 
@@ -166,7 +184,10 @@ ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, floa
             mbar_init(full0 + 8 * s, NPROD);
             mbar_init(empty0 + 8 * s, 1);
         }
-        mbar_init(accb, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(accf0 + 8 * s, 1);
+            mbar_init(acce0 + 8 * s, NEPI);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) {
@@ -181,102 +202,137 @@ ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, floa
     const uint32_t smem0 = smem_u32(smem);
 
     if (warp < 4) {
-        // ===================== producers =====================
-        const float* xcol = nullptr;   // BSL: row s = i*c*d + l*d + j ; BSF: element (n, i*c*d + l)
-        const float* kt = Kt32 + ((int64_t)q * b + k0) * c;   // [k][l] rows of this tile
-        for (int t = 0; t < nk; ++t) {
-            const int st = t % S;
-            if (t >= S) mbar_wait(empty0 + 8 * st, ((t / S) - 1) & 1);
-            const uint32_t sa = smem0 + st * C::STAGE;
-            const uint32_t sb = sa + C::A_BYTES;
-            const int l0 = t * BKC;
-            // ---- A tile: 128 rows x 32 l = 1024 chunks of 16 B
+        // ============================ producers ============================
+        // flat chunk index g over this CTA's tiles: tile = blockIdx.x + (g / nk) * gridDim.x
+        const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+        const int64_t G = my_tiles * nk;
+        float v[BKC];                                    // BSL: next chunk's column, prefetched
+        auto load_bsl = [&](int64_t gg) {
+            const TileCoord tc = decode(blockIdx.x + (gg / nk) * gridDim.x, nkc, nnb, d, BN);
+            const int l0 = (int)(gg % nk) * BKC;
+            const int64_t n = tc.n0 + tid;
+            const bool nok = n < B;
+            const float* xr = X + ((int64_t)tc.i * c * d + tc.j) * B + (nok ? n : 0);
+            const int64_t ls = (int64_t)d * B;           // stride between consecutive l
 #pragma unroll
-            for (int r = 0; r < (BM * BKC / 4) / NPROD; ++r) {
-                const int idx = tid + r * NPROD;
+            for (int l = 0; l < BKC; ++l) v[l] = (nok && l0 + l < c) ? __ldcs(xr + (int64_t)(l0 + l) * ls) : 0.f;
+        };
+        if (LAYOUT == KS_LAYOUT_BSL && G > 0) load_bsl(0);
+        for (int64_t g = 0; g < G; ++g) {
+            const TileCoord tc = decode(blockIdx.x + (g / nk) * gridDim.x, nkc, nnb, d, BN);
+            const float* kt = Kt32 + (tc.q * b + tc.k0) * c;          // [k][l] rows of this tile
+            const int t = (int)(g % nk);
+            {
+                const int st = (int)(g % S);
+                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                const uint32_t sa = smem0 + st * C::STAGE;
+                const uint32_t sb = sa + C::A_BYTES;
+                const int l0 = t * BKC;
                 if (LAYOUT == KS_LAYOUT_BSL) {
-                    const int m4 = idx % (BM / 4), l = idx / (BM / 4);
-                    const int64_t n = n0 + 4 * m4;
-                    const bool ok = (l0 + l < c) && (n < B);
-                    const float* src = X + ((int64_t)i * c * d + (int64_t)(ok ? l0 + l : 0) * d + j) * B + (ok ? n : 0);
-                    cp_async16(sa + m4 * 512 + (l / 8) * 128 + (l % 8) * 16, src, ok ? 16u : 0u);
-                } else {
-                    const int l4 = idx % (BKC / 4), m = idx / (BKC / 4);
-                    const int64_t n = n0 + m;
-                    const bool ok = (l0 + 4 * l4 < c) && (n < B);
-                    const float* src = X + (ok ? n : 0) * N + (int64_t)i * c + (ok ? l0 + 4 * l4 : 0);
-                    cp_async16(sa + (m / 8) * 1024 + l4 * 128 + (m % 8) * 16, src, ok ? 16u : 0u);
-                }
-            }
-            // ---- B tile: BN rows x 32 l
+                    // thread = batch row: its 32 l values (column loads, coalesced across the
+                    // warp) go out as 8 K-major 16-B chunks; then prefetch the next chunk
 #pragma unroll
-            for (int r = 0; r < (BN * BKC / 4 + NPROD - 1) / NPROD; ++r) {
-                const int idx = tid + r * NPROD;
-                if (idx < BN * BKC / 4) {
-                    const int l4 = idx % (BKC / 4), kr = idx / (BKC / 4);
-                    const bool ok = (l0 + 4 * l4 < c);
-                    const float* src = kt + (int64_t)kr * c + (ok ? l0 + 4 * l4 : 0);
-                    cp_async16(sb + (kr / 8) * 1024 + l4 * 128 + (kr % 8) * 16, src, ok ? 16u : 0u);
+                    for (int l4 = 0; l4 < BKC / 4; ++l4)
+                        sts128(sa + (tid / 8) * 1024 + l4 * 128 + (tid % 8) * 16, v[4 * l4], v[4 * l4 + 1],
+                               v[4 * l4 + 2], v[4 * l4 + 3]);
+                    if (g + 1 < G) load_bsl(g + 1);
+                } else {
+                    // BSF, d = 1: row n, l contiguous: 16-B chunks straight into place
+#pragma unroll
+                    for (int r = 0; r < (BM * BKC / 4) / NPROD; ++r) {
+                        const int idx = tid + r * NPROD;
+                        const int l4 = idx % (BKC / 4), m = idx / (BKC / 4);
+                        const int64_t n = tc.n0 + m;
+                        const bool ok = (l0 + 4 * l4 < c) && (n < B);
+                        const float* src = X + (ok ? n : 0) * N + (int64_t)tc.i * c + (ok ? l0 + 4 * l4 : 0);
+                        cp_async16(sa + (m / 8) * 1024 + l4 * 128 + (m % 8) * 16, src, ok ? 16u : 0u);
+                    }
                 }
-            }
-            cp_async_commit();
-            if (t >= S - 1) {
-                cp_async_wait<S - 1>();
-                fence_proxy_async();
-                mbar_arrive(full0 + 8 * ((t - (S - 1)) % S));
+#pragma unroll
+                for (int r = 0; r < (BN * BKC / 4 + NPROD - 1) / NPROD; ++r) {
+                    const int idx = tid + r * NPROD;
+                    if (idx < BN * BKC / 4) {
+                        const int l4 = idx % (BKC / 4), kr = idx / (BKC / 4);
+                        const bool ok = (l0 + 4 * l4 < c);
+                        const float* src = kt + (int64_t)kr * c + (ok ? l0 + 4 * l4 : 0);
+                        cp_async16(sb + (kr / 8) * 1024 + l4 * 128 + (kr % 8) * 16, src, ok ? 16u : 0u);
+                    }
+                }
+                cp_async_commit();
+                // retire chunk g-(S-1): its cp.async have landed (wait_group) and this
+                // thread's generic-proxy writes are made visible to the async proxy
+                if (g >= S - 1) {
+                    cp_async_wait<S - 1>();
+                    fence_proxy_async();
+                    mbar_arrive(full0 + 8 * (int)((g - (S - 1)) % S));
+                }
             }
         }
         cp_async_wait<0>();
         fence_proxy_async();
-        for (int u = (nk > S - 1 ? nk - (S - 1) : 0); u < nk; ++u) mbar_arrive(full0 + 8 * (u % S));
-
-        // ===================== epilogue =====================
-        mbar_wait(accb, 0);
-        tc_fence_after();
-        const int row = warp * 32 + (tid & 31);          // TMEM lane = batch row in tile
-        const int64_t n = n0 + row;
-        const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-        for (int col = 0; col < BN; col += 16) {
-            float v[16];
-            tmem_ld16(tbase + col, v);
-            if (n < B) {
-                if (LAYOUT == KS_LAYOUT_BSL) {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int64_t r = (int64_t)i * b * d + (int64_t)(k0 + col + e) * d + j;
-                        __stcs(Y + r * B + n, v[e]);
-                    }
-                } else {
-                    float* yp = Y + n * M + (int64_t)i * b + k0 + col;
-#pragma unroll
-                    for (int e = 0; e < 16; e += 4)
-                        __stcs(reinterpret_cast<float4*>(yp + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
-                }
-            }
-        }
+        for (int64_t u = (G > S - 1 ? G - (S - 1) : 0); u < G; ++u) mbar_arrive(full0 + 8 * (int)(u % S));
     } else if (warp == 4) {
-        // ===================== MMA issuer =====================
+        // ============================ MMA issuer ============================
         if ((tid & 31) == 0) {
-            constexpr uint32_t idesc = make_idesc(LAYOUT == KS_LAYOUT_BSL ? 1 : 0, BN);
-            for (int t = 0; t < nk; ++t) {
-                const int st = t % S;
-                mbar_wait(full0 + 8 * st, (t / S) & 1);
+            constexpr uint32_t idesc = make_idesc(BN);
+            int64_t g = 0;
+            int64_t it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int ab = (int)(it & 1);
+                if (it >= 2) mbar_wait(acce0 + 8 * ab, (uint32_t)(((it / 2) - 1) & 1));
                 tc_fence_after();
-                const uint32_t sa = smem0 + st * C::STAGE;
-                const uint32_t sb = sa + C::A_BYTES;
-                const int ksteps = min(BKC / 8, (c - t * BKC) / 8);
-                for (int s = 0; s < ksteps; ++s) {
-                    const uint64_t ad = (LAYOUT == KS_LAYOUT_BSL) ? make_desc(sa + s * 128, 128, 512)
-                                                                  : make_desc(sa + s * 256, 128, 1024);
-                    const uint64_t bd = make_desc(sb + s * 256, 128, 1024);
-                    mma_tf32(tmem, ad, bd, idesc, (t > 0 || s > 0) ? 1u : 0u);
+                const uint32_t dtm = tmem + (uint32_t)(ab * BN);
+                for (int t = 0; t < nk; ++t, ++g) {
+                    const int st = (int)(g % S);
+                    mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+                    tc_fence_after();
+                    const uint32_t sa = smem0 + st * C::STAGE;
+                    const uint32_t sb = sa + C::A_BYTES;
+                    const int ksteps = min(BKC / 8, (c - t * BKC) / 8);
+                    for (int s = 0; s < ksteps; ++s) {
+                        mma_tf32(dtm, make_desc(sa + s * 256, 128, 1024), make_desc(sb + s * 256, 128, 1024),
+                                 idesc, (t > 0 || s > 0) ? 1u : 0u);
+                    }
+                    mma_commit(empty0 + 8 * st);
                 }
-                mma_commit(empty0 + 8 * st);
+                mma_commit(accf0 + 8 * ab);
             }
-            mma_commit(accb);
         }
         __syncwarp();
+    } else {
+        // ============================ epilogue ============================
+        const int lq = warp & 3;                          // TMEM lane quarter this warp may access
+        const int row = lq * 32 + (tid & 31);
+        int64_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const TileCoord tc = decode(tile, nkc, nnb, d, BN);
+            const int ab = (int)(it & 1);
+            mbar_wait(accf0 + 8 * ab, (uint32_t)((it / 2) & 1));
+            tc_fence_after();
+            const int64_t n = tc.n0 + row;
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * BN);
+#pragma unroll 1
+            for (int col = 0; col < BN; col += 16) {
+                float v[16];
+                tmem_ld16(tbase + col, v);
+                if (n < B) {
+                    if (LAYOUT == KS_LAYOUT_BSL) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const int64_t r = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j;
+                            __stcs(Y + r * B + n, v[e]);
+                        }
+                    } else {
+                        float* yp = Y + n * M + (int64_t)tc.i * b + tc.k0 + col;
+#pragma unroll
+                        for (int e = 0; e < 16; e += 4)
+                            __stcs(reinterpret_cast<float4*>(yp + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(acce0 + 8 * ab);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -304,10 +360,11 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
         if (e != cudaSuccess) return e;
         attr[h.device & 63] = true;
     }
-    const int64_t blocks = (h.b / BN) * ((call.B + BM - 1) / BM) * (h.a * h.d);
-    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    kern<<<(unsigned)blocks, NTHREADS, C::SMEM, call.stream>>>(call.X, h.k_tf32, call.Y, call.B, (int)h.a,
-                                                                (int)h.b, (int)h.c, (int)h.d);
+    const int64_t ntiles = (h.b / BN) * ((call.B + BM - 1) / BM) * (h.a * h.d);
+    const int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS_PER_SM;
+    const int64_t grid = ntiles < slots ? ntiles : slots;
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(call.X, h.k_tf32, call.Y, call.B, (int)h.a,
+                                                              (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
     return cudaGetLastError();
 }
@@ -343,9 +400,8 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (h.b < 16 || h.c < 16 || h.c % 8 != 0 || pick_bn(h.b) == 0) return false;
     if (h.a * h.d > (int64_t(1) << 30)) return false;
     const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
-    if (al & 15) return false;
-    if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0;
-    return h.d == 1;      // BSF with d > 1: FP32 kernels (TF32 gather not built yet)
+    if (call.layout == KS_LAYOUT_BSL) return (al & 3) == 0;
+    return h.d == 1 && (al & 15) == 0;   // BSF d > 1: FP32 kernels (TF32 gather not built yet)
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
