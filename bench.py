@@ -47,7 +47,8 @@ def parse_args(argv=None):
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch override")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also run the configs[2] sweep vs bmm+permute")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[2] sweep vs bmm+permute")
+    ap.add_argument("--no-verify", action="store_true", help="skip the oracle check of sampled rows")
     return ap.parse_args(argv)
 
 
@@ -270,11 +271,31 @@ def run_ours(args):
         if not torch.equal(Yh, Y.cpu()):
             raise RuntimeError("e2e result differs from device-resident result")
 
+    # verification (outside the timed region): sampled rows of every rank's Y,
+    # gathered to all ranks over NCCL, checked on rank 0 against the oracle
+    vrows = np.array(sorted({0, 1, B // 2, B - 1}))
+    Yc = Y.cpu().numpy()
+    samp = torch.from_numpy(np.ascontiguousarray(Yc[vrows] if lay == "bsf" else Yc[:, vrows].T)).to(dev)
+    parts = [samp]
+    if world > 1:
+        parts = [torch.empty_like(samp) for _ in range(world)]
+        dist.all_gather(parts, samp)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return None
+    verify = None
+    if not args.no_verify:
+        import oracle
+        errs = []
+        for r, part in enumerate(parts):
+            Xr = X_host if r == rank else ksgen.x_normal(B, dims[0], seed=r)
+            ref = oracle.chain(pats, K4s, Xr, rows=vrows)
+            errs.append(oracle.normwise_error(part.cpu().numpy(), ref))
+        verify = {"rows_per_rank": len(vrows), "ranks": world, "max_normwise_err": max(errs),
+                  "tolerance": 1e-5, "ok": bool(max(errs) <= 1e-5)}
 
     peaks, src = measured_peaks()
     peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
@@ -305,11 +326,18 @@ def run_ours(args):
         "e2e": e2e,
         "plans": plans,
     }
+    line["verify"] = verify
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(pats, K4s, X_host, B, budget_s=15.0)
-    if args.sweep:
+    if not args.no_sweep and world == 1:
+        # second half of the metric: configs[2] median speedup vs bmm+permute
         from bench_sweep import run_sweep
-        line["sweep"] = run_sweep(dev)
+        sw = {}
+        for math in ("fp32", "tf32"):
+            r = run_sweep(dev, reps=5, math=math)
+            r.pop("rows")
+            sw[math] = r
+        line["sweep"] = sw
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
