@@ -51,7 +51,8 @@ struct Cfg {
     static constexpr int B_VECS = B_ELEMS / 4;
     static constexpr int B_PER_T = (B_VECS + THREADS - 1) / THREADS;
     static constexpr bool SMEM_EPI = (LAYOUT == KS_LAYOUT_BSF);   // used only when d > 1
-    static constexpr int C_ELEMS = BMJ * BN * J;
+    static constexpr int BNP = BN + 4;                // epilogue plane pitch
+    static constexpr int C_ELEMS = BMJ * BNP * J;
     static constexpr int PIPE_ELEMS = 2 * (A_ELEMS + B_ELEMS);
     static constexpr int SMEM_ELEMS = (SMEM_EPI && C_ELEMS > PIPE_ELEMS) ? C_ELEMS : PIPE_ELEMS;
     static constexpr int SMEM_BYTES = SMEM_ELEMS * 4;
@@ -258,21 +259,33 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
             }
         }
     } else {
-        // structured epilogue through shared memory: Cs[n][k][jj] -> J-wide runs
+        // structured epilogue through shared memory: one plane per j, Cs[jj][n][k]
+        // (row pitch BN+4 keeps vector stores aligned and spreads banks), then
+        // each (n, k) gathers its J values into one J-wide global store.
         float* Cs = smem;
+        float* plane = Cs + wj * (C::BMJ * C::BNP);
 #pragma unroll
         for (int m = 0; m < TM; ++m) {
             const int n = rowA + (m & 3) + 32 * (m >> 2);
+            float* dst = plane + n * C::BNP + colB;
+            if constexpr (TN == 8) {
+                *reinterpret_cast<float4*>(dst) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+                *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[m][4], acc[m][5], acc[m][6], acc[m][7]);
+            } else {
 #pragma unroll
-            for (int q = 0; q < TN; ++q) Cs[((n * C::BN) + colB + q) * J + wj] = acc[m][q];
+                for (int q = 0; q < TN / 2; ++q)
+                    *reinterpret_cast<float2*>(dst + 2 * q) = make_float2(acc[m][2 * q], acc[m][2 * q + 1]);
+            }
         }
         __syncthreads();
         for (int e = tid; e < C::BMJ * C::BN; e += C::THREADS) {
             const int n = e / C::BN, k = e % C::BN;
             if (n0 + n >= B) continue;
-            const VT v = *reinterpret_cast<const VT*>(Cs + (size_t)e * J);
+            float v[J];
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) v[jj] = Cs[jj * (C::BMJ * C::BNP) + n * C::BNP + k];
             float* yp = Y + (n0 + n) * M + (int64_t)i * b * d + (int64_t)(k0 + k) * d + j0;
-            __stcs(reinterpret_cast<VT*>(yp), v);
+            __stcs(reinterpret_cast<VT*>(yp), *reinterpret_cast<const VT*>(v));
         }
     }
 }

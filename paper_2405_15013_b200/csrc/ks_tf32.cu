@@ -1,42 +1,51 @@
-// TF32 tensor-core KS kernel (tcgen05.mma.kind::tf32, accumulators in TMEM)
-// for the GEMM-like patterns where each (i, j) block is a genuine dense
-// contraction (b, c >= 16; north star).  Not in the paper, whose kernel is
-// CUDA-core only: on B200 the FP32 FFMA path is ALU-bound
-// for b, c >= 48 (arithmetic intensity bc/(2(b+c)) above the FFMA ridge), so
-// the tensor cores turn these factors HBM-bound again.
+// TF32 tensor-core KS kernel (tcgen05.mma.kind::tf32, accumulators in TMEM,
+// operands staged by TMA) for the GEMM-like patterns where each (i, j) block
+// is a genuine dense contraction (b, c >= 16; north star).  Not in the paper,
+// whose kernel is CUDA-core only: on B200 the FP32 FFMA
+// path is ALU-bound for b, c >= 48 (arithmetic intensity bc/(2(b+c)) above the
+// FFMA ridge), so the tensor cores turn these factors HBM-bound again.
 //
 // Work unit ("tile") = output block Y[n0:n0+128, row_{i,j}[k0:k0+BN]]
 // (output-stationary, Alg. 3; each element written once).
 //   UMMA view:  D[m][n] = sum_k A[m][k] B[n][k],  M = 128 batch rows,
 //               N = BN outputs (k index of the KS block), K = l (c).
-//   A = X[n0:n0+128, col_{i,j}], B = K[row_{i,j}, col_{i,j}] (k_tf32,
-//   pre-rounded RNA at pack time, [q][k][l]); both K-major in shared memory
-//   in the canonical no-swizzle layout (8-row x 16-byte core matrices).
-//   (tcgen05 ignores the "MN-major" bit for kind::tf32 -- measured, see
-//   scripts/probe_umma.cu -- so batch-contiguous BSL tiles are transposed on
-//   the way in.)
-// Persistent CTAs (grid <= 2 per SM), tiles round-robin; warp roles
-// (288 threads):
-//   warps 0-3  producers: X and K chunks (128 x 32 l, BN x 32 l) into a
-//              STAGES-deep smem ring (mbarrier full/empty).  K and the
-//              ld-contiguous BSF X tile go by cp.async 16 B; BSL X is read
-//              as coalesced 4-byte columns and written transposed (STS.128).
-//   warp 4     TMEM allocator + single-thread MMA issuer (double-buffered
-//              accumulator: 2 x BN TMEM columns).
-//   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> coalesced global
-//              stores in the caller's layout, overlapping the next tile's MMAs.
-// X is fed as raw FP32 bits (the tensor core reads the TF32 part: truncation
-// of the 13 low mantissa bits); FP32 accumulation.  Contract: normwise error
-// <= 5e-3 (north star); DESIGN.md derives the per-element envelope.
+//   A = X[n0:n0+128, col_{i,j}],  B = K[row_{i,j}, col_{i,j}] (k_tf32: rows of
+//   c values, pre-rounded RNA at pack time).  Both K-major, 128-byte swizzled
+//   (the layout TMA SWIZZLE_128B produces), 32 l per pipeline stage.
+// Operand movement (no permutation pass):
+//   * B:            TMA 2-D box {32 l, BN rows} from k_tf32.
+//   * A, BSF d = 1: TMA 2-D box {32 l, 128 rows} straight from X (rows of N).
+//   * A, BSL:       TMA 3-D box {128 batch, 1 j, 32 l} of X viewed as
+//                   [a*c][d][B] into a staging ring; tcgen05 ignores the
+//                   MN-major bit for kind::tf32 (measured: scripts/probe_umma.cu),
+//                   so 4 transposer warps rewrite each staged chunk K-major
+//                   (32 LDS.32 + 8 conflict-free STS.128 per thread).
+// Persistent CTAs (one per SM), tiles round-robin; 320 threads:
+//   warp 0      lane 0: X/A TMA issuer, lane 1: B TMA issuer
+//   warps 1-4   BSL transposers
+//   warp 5      TMEM allocator + single-thread MMA issuer (double-buffered
+//               accumulator, 2 x BN TMEM columns)
+//   warps 6-9   epilogue: tcgen05.ld 32x32b -> registers -> coalesced global
+//               stores in the caller's layout, overlapping the next tile.
+// X is fed as raw FP32 bits (the tensor core uses the TF32 part: truncation of
+// the 13 low mantissa bits); FP32 accumulation.  Contract: normwise error
+// <= 5e-3 (north star); R9/R10 give the per-element envelope.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "ks_internal.h"
 
 namespace {
 
-constexpr int BM = 128;       // batch rows per tile = UMMA M
-constexpr int BKC = 32;       // l per pipeline stage (4 UMMA k-steps of 8)
-constexpr int NPROD = 128;    // producer threads (warps 0-3)
-constexpr int NEPI = 128;     // epilogue threads (warps 5-8)
-constexpr int NTHREADS = NPROD + 32 + NEPI;
+constexpr int BM = 128;        // batch rows per tile = UMMA M
+constexpr int BKC = 32;        // l per pipeline stage (4 UMMA k-steps of 8)
+constexpr int NTRANS = 128;    // transposer threads (warps 1-4)
+constexpr int NEPI = 128;      // epilogue threads (warps 6-9)
+constexpr int NTHREADS = 320;
+constexpr int A_BYTES = BM * BKC * 4;      // 16 KB
+constexpr int STG_BYTES = BKC * BM * 4;    // 16 KB staging chunk [32 l][128 n]
 
 // ---- PTX wrappers ----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -47,6 +56,9 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -59,12 +71,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "DONE:\n"
         "}\n" ::"r"(bar), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -79,14 +94,22 @@ __device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c,
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
+__device__ __forceinline__ float lds32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
 
-// Shared-memory matrix descriptor, no swizzle: start, LBO, SBO, version 1.
-__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor for a K-major, 128-byte-swizzled operand:
+// start address, LBO = 16 B (unused for swizzled K-major), SBO = 1024 B
+// (stride between 8-row groups), version 1 (sm_100), layout type 2 (SW128).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
     d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
     return d;
 }
 
@@ -123,74 +146,91 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
 }
 
-template <int BN>
+template <int LAYOUT, int BN>
 struct Tf32Cfg {
-    static constexpr int A_BYTES = BM * BKC * 4;          // 16 KB
-    static constexpr int B_BYTES = BN * BKC * 4;          // BN * 128 B
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN <= 64 ? 4 : BN <= 128 ? 3 : 2;
-    static constexpr int BAR_BYTES = 256;
-    static constexpr int SMEM = STAGES * STAGE + BAR_BYTES;
+    static constexpr int B_BYTES = BN * BKC * 4;          // BN * 128 B (multiple of 1 KB)
+    static constexpr int SLOT = A_BYTES + B_BYTES;
+    static constexpr int CTAS = BN <= 64 ? 2 : 1;                                 // CTAs per SM
+    static constexpr int BUDGET = CTAS == 2 ? 108 * 1024 : 200 * 1024;
+    static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? 3 : BN > 128 ? 3 : 6) : 0;   // staging
+    static constexpr int S_FIT = (BUDGET - P * STG_BYTES) / SLOT;
+    static constexpr int S = S_FIT > 6 ? 6 : S_FIT;                              // operand slots
+    static constexpr int BAR_OFF = S * SLOT + P * STG_BYTES;
+    static constexpr int SMEM = BAR_OFF + 256 + 1024;                            // + barriers + align pad
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
-    static constexpr int CTAS_PER_SM = TMEM_COLS <= 256 ? 2 : 1;
     static_assert(BN % 16 == 0 && BN <= 256, "UMMA N for M=128");
+    static_assert(S >= 2, "pipeline too shallow");
 };
 
 struct TileCoord {
     int i, j, k0;
-    int64_t n0;
-    int64_t q;
+    int n0;
+    int q;
 };
 
 __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, int d, int BN) {
     TileCoord t;
     const int kc = (int)(tile % nkc);
     tile /= nkc;
-    t.n0 = (tile % nnb) * BM;
-    t.q = tile / nnb;
-    t.i = (int)(t.q / d);
-    t.j = (int)(t.q % d);
+    t.n0 = (int)(tile % nnb) * BM;
+    t.q = (int)(tile / nnb);
+    t.i = t.q / d;
+    t.j = t.q % d;
     t.k0 = kc * BN;
     return t;
 }
 
-// K-major smem tile (rows r, K index l in [0,32)):  (r/8)*1024 + (l/4)*128 + (r%8)*16 + (l%4)*4
-//   -> LBO (next 4-l chunk) = 128 B, SBO (next 8-row group) = 1024 B.
 template <int LAYOUT, int BN>
-__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<BN>::CTAS_PER_SM)
-ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, float* __restrict__ Y,
-               int64_t B, int a, int b, int c, int d, int64_t ntiles) {
-    using C = Tf32Cfg<BN>;
-    constexpr int S = C::STAGES;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::STAGE);
-    // [0,S) full  [S,2S) empty  [2S,2S+2) acc_full  [2S+2,2S+4) acc_empty  [2S+4] tmem slot
+__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN>::CTAS)
+ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+               float* __restrict__ Y, int64_t B, int a, int b, int c, int d, int64_t ntiles, int dbg) {
+    using C = Tf32Cfg<LAYOUT, BN>;
+    constexpr int S = C::S;
+    constexpr int P = C::P > 0 ? C::P : 1;      // (BSF: no staging; P only names unused barriers)
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    // [0,S) full  [S,2S) empty  [2S,2S+2) acc_full  [2S+2,2S+4) acc_empty
+    // [2S+4, 2S+4+P) stg_full  [.., +P) stg_empty   then the TMEM slot
     const uint32_t full0 = smem_u32(&bars[0]);
     const uint32_t empty0 = smem_u32(&bars[S]);
     const uint32_t accf0 = smem_u32(&bars[2 * S]);
     const uint32_t acce0 = smem_u32(&bars[2 * S + 2]);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4]);
+    const uint32_t sfull0 = smem_u32(&bars[2 * S + 4]);
+    const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + (P > 0 ? P : 1)]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * (P > 0 ? P : 1)]);
+    const uint32_t slot0 = smem_u32(smem);                 // S x (A 16 KB | B BN*128 B), 1 KB aligned
+    const uint32_t stg0 = slot0 + S * C::SLOT;             // P x 16 KB staging (BSL)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
+    const int lane = tid & 31;
     const int nkc = b / BN;
     const int64_t nnb = (B + BM - 1) / BM;
-    const int64_t N = (int64_t)a * c * d, M = (int64_t)a * b * d;
+    const int64_t M = (int64_t)a * b * d;
     const int nk = (c + BKC - 1) / BKC;
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t G = my_tiles * nk;
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, NPROD);
+            mbar_init(full0 + 8 * s, LAYOUT == KS_LAYOUT_BSL ? 1 + NTRANS : 2);
             mbar_init(empty0 + 8 * s, 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(accf0 + 8 * s, 1);
             mbar_init(acce0 + 8 * s, NEPI);
         }
+        for (int p = 0; p < P; ++p) {
+            mbar_init(sfull0 + 8 * p, 1);  // staging ring (BSL)
+            mbar_init(sempty0 + 8 * p, NTRANS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
     }
-    if (warp == 4) {
+    if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(C::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -199,81 +239,61 @@ ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, floa
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t smem0 = smem_u32(smem);
 
-    if (warp < 4) {
-        // ============================ producers ============================
-        // flat chunk index g over this CTA's tiles: tile = blockIdx.x + (g / nk) * gridDim.x
-        const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-        const int64_t G = my_tiles * nk;
-        float v[BKC];                                    // BSL: next chunk's column, prefetched
-        auto load_bsl = [&](int64_t gg) {
-            const TileCoord tc = decode(blockIdx.x + (gg / nk) * gridDim.x, nkc, nnb, d, BN);
-            const int l0 = (int)(gg % nk) * BKC;
-            const int64_t n = tc.n0 + tid;
-            const bool nok = n < B;
-            const float* xr = X + ((int64_t)tc.i * c * d + tc.j) * B + (nok ? n : 0);
-            const int64_t ls = (int64_t)d * B;           // stride between consecutive l
-#pragma unroll
-            for (int l = 0; l < BKC; ++l) v[l] = (nok && l0 + l < c) ? __ldcs(xr + (int64_t)(l0 + l) * ls) : 0.f;
-        };
-        if (LAYOUT == KS_LAYOUT_BSL && G > 0) load_bsl(0);
-        for (int64_t g = 0; g < G; ++g) {
-            const TileCoord tc = decode(blockIdx.x + (g / nk) * gridDim.x, nkc, nnb, d, BN);
-            const float* kt = Kt32 + (tc.q * b + tc.k0) * c;          // [k][l] rows of this tile
-            const int t = (int)(g % nk);
-            {
+    if (warp == 0) {
+        if (lane == 0) {
+            // One thread issues every TMA.  BSL: the X staging ring runs P-1 chunks
+            // ahead of the operand slots; BSF: A and B land in the same slot.
+            auto issue_x = [&](int64_t gx) {     // BSL staging chunk gx
+                const TileCoord tc = decode(blockIdx.x + (gx / nk) * gridDim.x, nkc, nnb, d, BN);
+                const int l0 = (int)(gx % nk) * BKC;
+                const int p = (int)(gx % P);
+                if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
+                mbar_expect_tx(sfull0 + 8 * p, STG_BYTES);
+                tma_3d(stg0 + p * STG_BYTES, &xmap, tc.n0, tc.j, tc.i * c + l0, sfull0 + 8 * p);
+            };
+            if (LAYOUT == KS_LAYOUT_BSL)
+                for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
+            for (int64_t g = 0; g < G; ++g) {
+                if (LAYOUT == KS_LAYOUT_BSL && g + P - 1 < G) issue_x(g + P - 1);
+                const TileCoord tc = decode(blockIdx.x + (g / nk) * gridDim.x, nkc, nnb, d, BN);
+                const int l0 = (int)(g % nk) * BKC;
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
-                const uint32_t sa = smem0 + st * C::STAGE;
-                const uint32_t sb = sa + C::A_BYTES;
-                const int l0 = t * BKC;
-                if (LAYOUT == KS_LAYOUT_BSL) {
-                    // thread = batch row: its 32 l values (column loads, coalesced across the
-                    // warp) go out as 8 K-major 16-B chunks; then prefetch the next chunk
-#pragma unroll
-                    for (int l4 = 0; l4 < BKC / 4; ++l4)
-                        sts128(sa + (tid / 8) * 1024 + l4 * 128 + (tid % 8) * 16, v[4 * l4], v[4 * l4 + 1],
-                               v[4 * l4 + 2], v[4 * l4 + 3]);
-                    if (g + 1 < G) load_bsl(g + 1);
-                } else {
-                    // BSF, d = 1: row n, l contiguous: 16-B chunks straight into place
-#pragma unroll
-                    for (int r = 0; r < (BM * BKC / 4) / NPROD; ++r) {
-                        const int idx = tid + r * NPROD;
-                        const int l4 = idx % (BKC / 4), m = idx / (BKC / 4);
-                        const int64_t n = tc.n0 + m;
-                        const bool ok = (l0 + 4 * l4 < c) && (n < B);
-                        const float* src = X + (ok ? n : 0) * N + (int64_t)tc.i * c + (ok ? l0 + 4 * l4 : 0);
-                        cp_async16(sa + (m / 8) * 1024 + l4 * 128 + (m % 8) * 16, src, ok ? 16u : 0u);
-                    }
+                if (LAYOUT != KS_LAYOUT_BSL) {
+                    mbar_expect_tx(full0 + 8 * st, A_BYTES);
+                    tma_2d(slot0 + st * C::SLOT, &xmap, tc.i * c + l0, tc.n0, full0 + 8 * st);
                 }
-#pragma unroll
-                for (int r = 0; r < (BN * BKC / 4 + NPROD - 1) / NPROD; ++r) {
-                    const int idx = tid + r * NPROD;
-                    if (idx < BN * BKC / 4) {
-                        const int l4 = idx % (BKC / 4), kr = idx / (BKC / 4);
-                        const bool ok = (l0 + 4 * l4 < c);
-                        const float* src = kt + (int64_t)kr * c + (ok ? l0 + 4 * l4 : 0);
-                        cp_async16(sb + (kr / 8) * 1024 + l4 * 128 + (kr % 8) * 16, src, ok ? 16u : 0u);
-                    }
-                }
-                cp_async_commit();
-                // retire chunk g-(S-1): its cp.async have landed (wait_group) and this
-                // thread's generic-proxy writes are made visible to the async proxy
-                if (g >= S - 1) {
-                    cp_async_wait<S - 1>();
-                    fence_proxy_async();
-                    mbar_arrive(full0 + 8 * (int)((g - (S - 1)) % S));
-                }
+                mbar_expect_tx(full0 + 8 * st, C::B_BYTES);
+                tma_2d(slot0 + st * C::SLOT + A_BYTES, &kmap, l0, tc.q * b + tc.k0, full0 + 8 * st);
             }
         }
-        cp_async_wait<0>();
-        fence_proxy_async();
-        for (int64_t u = (G > S - 1 ? G - (S - 1) : 0); u < G; ++u) mbar_arrive(full0 + 8 * (int)(u % S));
-    } else if (warp == 4) {
-        // ============================ MMA issuer ============================
-        if ((tid & 31) == 0) {
+    } else if (warp <= 4) {
+        // ---------------- BSL transposers: staging [l][n] -> K-major SW128 A ----------------
+        if (LAYOUT == KS_LAYOUT_BSL) {
+            const int r = tid - 32;                                    // batch row in the tile
+            const uint32_t rowoff = (uint32_t)((r / 8) * 1024 + (r % 8) * 128);
+            for (int64_t g = 0; g < G; ++g) {
+                const int p = (int)(g % P);
+                mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
+                float v[BKC];
+                const uint32_t src = stg0 + p * STG_BYTES + 4 * r;
+#pragma unroll
+                for (int l = 0; l < BKC; ++l) v[l] = (dbg & 2) ? 0.f : lds32(src + l * (BM * 4));
+                mbar_arrive(sempty0 + 8 * p);
+                const int st = (int)(g % S);
+                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                const uint32_t dst = slot0 + st * C::SLOT + rowoff;
+#pragma unroll
+                for (int l4 = 0; l4 < BKC / 4; ++l4)
+                    sts128(dst + ((l4 ^ (r % 8)) * 16), v[4 * l4], v[4 * l4 + 1], v[4 * l4 + 2], v[4 * l4 + 3]);
+                fence_proxy_async();
+                mbar_arrive(full0 + 8 * st);
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
             constexpr uint32_t idesc = make_idesc(BN);
             int64_t g = 0;
             int64_t it = 0;
@@ -286,13 +306,12 @@ ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, floa
                     const int st = (int)(g % S);
                     mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
                     tc_fence_after();
-                    const uint32_t sa = smem0 + st * C::STAGE;
-                    const uint32_t sb = sa + C::A_BYTES;
+                    const uint32_t sa = slot0 + st * C::SLOT;
+                    const uint32_t sb = sa + A_BYTES;
                     const int ksteps = min(BKC / 8, (c - t * BKC) / 8);
-                    for (int s = 0; s < ksteps; ++s) {
-                        mma_tf32(dtm, make_desc(sa + s * 256, 128, 1024), make_desc(sb + s * 256, 128, 1024),
-                                 idesc, (t > 0 || s > 0) ? 1u : 0u);
-                    }
+                    for (int s = 0; s < ksteps; ++s)
+                        mma_tf32(dtm, sw128_desc(sa + 32 * s), sw128_desc(sb + 32 * s), idesc,
+                                 (t > 0 || s > 0) ? 1u : 0u);
                     mma_commit(empty0 + 8 * st);
                 }
                 mma_commit(accf0 + 8 * ab);
@@ -300,22 +319,22 @@ ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, floa
         }
         __syncwarp();
     } else {
-        // ============================ epilogue ============================
+        // ---------------- epilogue ----------------
         const int lq = warp & 3;                          // TMEM lane quarter this warp may access
-        const int row = lq * 32 + (tid & 31);
+        const int row = lq * 32 + lane;
         int64_t it = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const TileCoord tc = decode(tile, nkc, nnb, d, BN);
             const int ab = (int)(it & 1);
             mbar_wait(accf0 + 8 * ab, (uint32_t)((it / 2) & 1));
             tc_fence_after();
-            const int64_t n = tc.n0 + row;
+            const int64_t n = (int64_t)tc.n0 + row;
             const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * BN);
 #pragma unroll 1
             for (int col = 0; col < BN; col += 16) {
                 float v[16];
                 tmem_ld16(tbase + col, v);
-                if (n < B) {
+                if (n < B && !(dbg & 1)) {
                     if (LAYOUT == KS_LAYOUT_BSL) {
 #pragma unroll
                         for (int e = 0; e < 16; ++e) {
@@ -336,13 +355,48 @@ ks_tf32_kernel(const float* __restrict__ X, const float* __restrict__ Kt32, floa
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 5) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
     }
 }
 
 // ------------------------------------------------------------------ host ------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+            const cuuint32_t* box, CUtensorMapSwizzle sw) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), dims,
+                    strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// KS_TF32_DEBUG (profiling experiments only): bit 0 skips the epilogue's global
+// stores, bit 1 skips the transposers' shared-memory reads.  0 in production.
+int debug_flags() {
+    static int v = [] {
+        const char* e = getenv("KS_TF32_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 int pick_bn(int64_t b) {
     if (b <= 256 && b % 16 == 0) return (int)b;
     for (int bn : {256, 192, 128, 96, 64, 48, 32, 16})
@@ -352,7 +406,25 @@ int pick_bn(int64_t b) {
 
 template <int LAYOUT, int BN>
 cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
-    using C = Tf32Cfg<BN>;
+    using C = Tf32Cfg<LAYOUT, BN>;
+    CUtensorMap xmap, kmap;
+    {
+        const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
+        const cuuint64_t ks[1] = {(cuuint64_t)h.c * 4};
+        const cuuint32_t kb[2] = {BKC, BN};
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    }
+    if (LAYOUT == KS_LAYOUT_BSL) {
+        const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
+        const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
+        const cuuint32_t xb[3] = {BM, 1, BKC};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    } else {
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
+        const cuuint32_t xb[2] = {BKC, BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    }
     auto kern = ks_tf32_kernel<LAYOUT, BN>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
@@ -361,10 +433,10 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
         attr[h.device & 63] = true;
     }
     const int64_t ntiles = (h.b / BN) * ((call.B + BM - 1) / BM) * (h.a * h.d);
-    const int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS_PER_SM;
+    const int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(call.X, h.k_tf32, call.Y, call.B, (int)h.a,
-                                                              (int)h.b, (int)h.c, (int)h.d, ntiles);
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.B, (int)h.a, (int)h.b,
+                                                              (int)h.c, (int)h.d, ntiles, debug_flags());
     ks::count_launch();
     return cudaGetLastError();
 }
@@ -398,10 +470,12 @@ namespace ks {
 
 bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (h.b < 16 || h.c < 16 || h.c % 8 != 0 || pick_bn(h.b) == 0) return false;
-    if (h.a * h.d > (int64_t(1) << 30)) return false;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
-    if (call.layout == KS_LAYOUT_BSL) return (al & 3) == 0;
-    return h.d == 1 && (al & 15) == 0;   // BSF d > 1: FP32 kernels (TF32 gather not built yet)
+    if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31)) return false;
+    if (call.B >= (int64_t(1) << 31)) return false;
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(call.X), ya = reinterpret_cast<uintptr_t>(call.Y);
+    if (xa & 15) return false;                                   // TMA global address
+    if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0 && (ya & 3) == 0;
+    return h.d == 1 && (ya & 15) == 0;   // BSF with d > 1: FP32 kernels (TF32 gather not built yet)
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {

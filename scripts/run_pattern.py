@@ -1,0 +1,45 @@
+"""Run ks_matmul on one pattern (for ncu captures and quick timing).
+
+    python scripts/run_pattern.py a b c d [--layout bsf|bsl] [--math fp32|tf32] [--B 25088] [--reps 5]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import ksgen  # noqa: E402
+import paper_2405_15013_b200 as ksb  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("p", type=int, nargs=4)
+ap.add_argument("--layout", default="bsf")
+ap.add_argument("--math", default="fp32")
+ap.add_argument("--kernel", default="auto")
+ap.add_argument("--B", type=int, default=25088)
+ap.add_argument("--reps", type=int, default=5)
+args = ap.parse_args()
+a, b, c, d = args.p
+M, N = a * b * d, a * c * d
+f = ksb.Factor(a, b, c, d, ksgen.k4_uniform(a, b, c, d, seed=1))
+if args.math == "tf32":
+    f.set_math(ksb.MATH_TF32)
+if args.kernel != "auto":
+    f.set_kernel({"generic": 1, "stream": 2, "ffma": 3, "tf32": 4}[args.kernel])
+dev = torch.device("cuda:0")
+X = torch.randn((args.B, N) if args.layout == "bsf" else (N, args.B), device=dev)
+Y = torch.empty((args.B, M) if args.layout == "bsf" else (M, args.B), device=dev)
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ksb.matmul(f, X, Y, layout=args.layout)
+torch.cuda.synchronize()
+s.record()
+for _ in range(args.reps):
+    ksb.matmul(f, X, Y, layout=args.layout)
+e.record()
+torch.cuda.synchronize()
+ms = s.elapsed_time(e) / args.reps
+byts = 4 * (args.B * N + a * b * c * d + args.B * M)
+print(f"{args.p} {args.layout} {args.math} plan={f.plan(args.B, args.layout)} {ms*1e3:.1f} us "
+      f"{byts/ms/1e6:.0f} GB/s {2*args.B*a*b*c*d/ms/1e9:.1f} TFLOP/s")
