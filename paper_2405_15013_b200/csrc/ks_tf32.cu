@@ -280,6 +280,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 const uint32_t src = stg0 + p * STG_BYTES + 4 * r;
 #pragma unroll
                 for (int l = 0; l < BKC; ++l) v[l] = (dbg & 2) ? 0.f : lds32(src + l * (BM * 4));
+                fence_proxy_async();      // generic reads before the TMA (async proxy) refill
                 mbar_arrive(sempty0 + 8 * p);
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
@@ -361,6 +362,234 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     }
 }
 
+// ==========================================================================
+// BSF with d % 4 == 0: J = 4 consecutive j per tile.  In BSF the 4 values
+// X[n, i*c*d + l*d + j0 .. j0+3] are one 16-byte vector, so a TMA 3-D box
+// {4 j, 16 l, 128 n} of X viewed as [B][a*c][d] gathers the d-strided columns
+// of 4 KS blocks at once with full 16-byte vectors (SURVEY §7 hard part 1).
+// Transposer warps split the staged [n][l][j] chunk into four K-major
+// 64-byte-swizzled A tiles (one per j); the MMA warp runs 4 accumulators
+// (4 x BN <= 256 TMEM columns, double-buffered); the epilogue writes the 4 j
+// of each (n, k) as one float4.
+// ==========================================================================
+constexpr int BKJ = 16;                       // l per stage (2 UMMA k-steps)
+constexpr int JJ = 4;
+constexpr int AJ_BYTES = BM * BKJ * 4;        // 8 KB per j
+constexpr int STGJ_ROW = (BKJ + 1) * JJ * 4;  // 272 B: box {4 j, 17 l, 128 n}, 1 l of padding
+constexpr int STGJ_BYTES = BM * STGJ_ROW;      // 34 KB staging chunk [128 n][17 l][4 j]
+
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;            // 8 rows x 64 B
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;                     // SWIZZLE_64B
+    return d;
+}
+
+template <int BN>
+struct Tf32JCfg {
+    static constexpr int B_BYTES = BN * BKJ * 4;          // per j, BN * 64 B
+    static constexpr int SLOT = JJ * (AJ_BYTES + B_BYTES);
+    static constexpr int P = 2;
+    static constexpr int S_FIT = (200 * 1024 - P * STGJ_BYTES) / SLOT;
+    static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
+    static constexpr int BAR_OFF = S * SLOT + P * STGJ_BYTES;
+    static constexpr int SMEM = BAR_OFF + 256 + 1024;
+    static constexpr int TMEM_COLS = 2 * JJ * BN <= 256 ? 256 : 512;
+    static_assert(JJ * BN <= 256 && BN % 16 == 0, "4 accumulators, double-buffered");
+    static_assert(S >= 2, "pipeline too shallow");
+};
+
+struct TileJ {
+    int i, j0, k0, n0;
+};
+
+__device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_t nnb, int BN) {
+    TileJ t;
+    t.k0 = (int)(tile % nkc) * BN;
+    tile /= nkc;
+    t.j0 = (int)(tile % njg) * JJ;              // j-groups of one (i, n-block) run back to back
+    tile /= njg;
+    t.n0 = (int)(tile % nnb) * BM;
+    t.i = (int)(tile / nnb);
+    return t;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                    float* __restrict__ Y, int64_t B, int a, int b, int c, int d, int64_t ntiles) {
+    using C = Tf32JCfg<BN>;
+    constexpr int S = C::S;
+    constexpr int P = C::P;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    const uint32_t full0 = smem_u32(&bars[0]);
+    const uint32_t empty0 = smem_u32(&bars[S]);
+    const uint32_t accf0 = smem_u32(&bars[2 * S]);
+    const uint32_t acce0 = smem_u32(&bars[2 * S + 2]);
+    const uint32_t sfull0 = smem_u32(&bars[2 * S + 4]);
+    const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + P]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * P]);
+    const uint32_t slot0 = smem_u32(smem);        // S x [4 A tiles (8 KB) | 4 B tiles (BN*64 B)]
+    const uint32_t stg0 = slot0 + S * C::SLOT;    // P x 32 KB staging
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int nkc = b / BN;
+    const int njg = d / JJ;
+    const int64_t nnb = (B + BM - 1) / BM;
+    const int64_t M = (int64_t)a * b * d;
+    const int nk = c / BKJ;                       // c % 16 == 0
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t G = my_tiles * nk;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1 + NTRANS);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(accf0 + 8 * s, 1);
+            mbar_init(acce0 + 8 * s, NEPI);
+        }
+        for (int p = 0; p < P; ++p) {
+            mbar_init(sfull0 + 8 * p, 1);
+            mbar_init(sempty0 + 8 * p, NTRANS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            auto issue_x = [&](int64_t gx) {
+                const TileJ tc = decode_j(blockIdx.x + (gx / nk) * gridDim.x, nkc, njg, nnb, BN);
+                const int l0 = (int)(gx % nk) * BKJ;
+                const int p = (int)(gx % P);
+                if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
+                mbar_expect_tx(sfull0 + 8 * p, STGJ_BYTES);
+                tma_3d(stg0 + p * STGJ_BYTES, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
+            };
+            for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
+            for (int64_t g = 0; g < G; ++g) {
+                if (g + P - 1 < G) issue_x(g + P - 1);
+                const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN);
+                const int l0 = (int)(g % nk) * BKJ;
+                const int st = (int)(g % S);
+                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                mbar_expect_tx(full0 + 8 * st, JJ * C::B_BYTES);
+                const uint32_t sb = slot0 + st * C::SLOT + JJ * AJ_BYTES;
+                for (int jj = 0; jj < JJ; ++jj)
+                    tma_2d(sb + jj * C::B_BYTES, &kmap, l0, ((tc.i * d + tc.j0 + jj) * b) + tc.k0, full0 + 8 * st);
+            }
+        }
+    } else if (warp <= 4) {
+        // staging [n][l][j] (256 B per row n) -> 4 K-major SW64 A tiles
+        const int r = tid - 32;
+        const uint32_t rowoff = (uint32_t)((r / 8) * 512 + (r % 8) * 64);
+        const int sw = (r % 8) / 2;
+        for (int64_t g = 0; g < G; ++g) {
+            const int p = (int)(g % P);
+            mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
+            float v[BKJ][JJ];
+            // rows are 17 l long (the box carries one extra l as padding), so the 8
+            // rows of a shared-memory phase fall on 8 different 16-byte bank groups
+            const uint32_t src = stg0 + p * STGJ_BYTES + r * STGJ_ROW;
+#pragma unroll
+            for (int l = 0; l < BKJ; ++l)
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[l][0]), "=f"(v[l][1]), "=f"(v[l][2]), "=f"(v[l][3]) : "r"(src + l * 16));
+            fence_proxy_async();          // generic reads before the TMA (async proxy) refill
+            mbar_arrive(sempty0 + 8 * p);
+            const int st = (int)(g % S);
+            if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+            const uint32_t sa = slot0 + st * C::SLOT + rowoff;
+#pragma unroll
+            for (int jj = 0; jj < JJ; ++jj)
+#pragma unroll
+                for (int ch = 0; ch < BKJ / 4; ++ch)
+                    sts128(sa + jj * AJ_BYTES + ((ch ^ sw) * 16), v[4 * ch][jj], v[4 * ch + 1][jj],
+                           v[4 * ch + 2][jj], v[4 * ch + 3][jj]);
+            fence_proxy_async();
+            mbar_arrive(full0 + 8 * st);
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(BN);
+            int64_t g = 0, it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int ab = (int)(it & 1);
+                if (it >= 2) mbar_wait(acce0 + 8 * ab, (uint32_t)(((it / 2) - 1) & 1));
+                tc_fence_after();
+                for (int t = 0; t < nk; ++t, ++g) {
+                    const int st = (int)(g % S);
+                    mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+                    tc_fence_after();
+                    const uint32_t sa = slot0 + st * C::SLOT;
+                    const uint32_t sb = sa + JJ * AJ_BYTES;
+#pragma unroll
+                    for (int jj = 0; jj < JJ; ++jj)
+#pragma unroll
+                        for (int s = 0; s < BKJ / 8; ++s)
+                            mma_tf32(tmem + (uint32_t)((ab * JJ + jj) * BN), sw64_desc(sa + jj * AJ_BYTES + 32 * s),
+                                     sw64_desc(sb + jj * C::B_BYTES + 32 * s), idesc, (t > 0 || s > 0) ? 1u : 0u);
+                    mma_commit(empty0 + 8 * st);
+                }
+                mma_commit(accf0 + 8 * ab);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int lq = warp & 3;
+        const int row = lq * 32 + lane;
+        int64_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const TileJ tc = decode_j(tile, nkc, njg, nnb, BN);
+            const int ab = (int)(it & 1);
+            mbar_wait(accf0 + 8 * ab, (uint32_t)((it / 2) & 1));
+            tc_fence_after();
+            const int64_t n = (int64_t)tc.n0 + row;
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * JJ * BN);
+#pragma unroll 1
+            for (int col = 0; col < BN; col += 16) {
+                float v[JJ][16];
+#pragma unroll
+                for (int jj = 0; jj < JJ; ++jj) tmem_ld16(tbase + jj * BN + col, v[jj]);
+                if (n < B) {
+                    float* yp = Y + n * M + (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        __stcs(reinterpret_cast<float4*>(yp + (int64_t)e * d),
+                               make_float4(v[0][e], v[1][e], v[2][e], v[3][e]));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(acce0 + 8 * ab);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+    }
+}
+
 // ------------------------------------------------------------------ host ------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -389,6 +618,16 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 
 // KS_TF32_DEBUG (profiling experiments only): bit 0 skips the epilogue's global
 // stores, bit 1 skips the transposers' shared-memory reads.  0 in production.
+// KS_TF32_MAXGRID (tests): cap the persistent grid so small problems exercise
+// several tiles per CTA.  0 / unset in production.
+int max_grid() {
+    static int v = [] {
+        const char* e = getenv("KS_TF32_MAXGRID");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 int debug_flags() {
     static int v = [] {
         const char* e = getenv("KS_TF32_DEBUG");
@@ -433,13 +672,55 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
         attr[h.device & 63] = true;
     }
     const int64_t ntiles = (h.b / BN) * ((call.B + BM - 1) / BM) * (h.a * h.d);
-    const int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
+    int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
+    if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.B, (int)h.a, (int)h.b,
                                                               (int)h.c, (int)h.d, ntiles, debug_flags());
     ks::count_launch();
     return cudaGetLastError();
 }
+
+int pick_bn_j(int64_t b) {
+    for (int bn : {64, 48, 32, 16})
+        if (b % bn == 0) return bn;
+    return 0;
+}
+
+template <int BN>
+cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
+    using C = Tf32JCfg<BN>;
+    CUtensorMap xmap, kmap;
+    {
+        const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
+        const cuuint64_t ks[1] = {(cuuint64_t)h.c * 4};
+        const cuuint32_t kb[2] = {BKJ, BN};
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
+        const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
+        const cuuint32_t xb[3] = {JJ, BKJ + 1, BM};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_tf32_bsfj_kernel<BN>;
+    static bool attr[64] = {false};
+    if (!attr[h.device & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr[h.device & 63] = true;
+    }
+    const int64_t ntiles = (h.b / BN) * (h.d / JJ) * ((call.B + BM - 1) / BM) * h.a;
+    int64_t slots = (int64_t)ks::num_sms(h.device);
+    if (max_grid() > 0) slots = max_grid();
+    const int64_t grid = ntiles < slots ? ntiles : slots;
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.B, (int)h.a, (int)h.b,
+                                                              (int)h.c, (int)h.d, ntiles);
+    ks::count_launch();
+    return cudaGetLastError();
+}
+
+bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % BKJ == 0 && pick_bn_j(h.b) != 0; }
 
 template <int LAYOUT>
 cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
@@ -475,12 +756,20 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     const uintptr_t xa = reinterpret_cast<uintptr_t>(call.X), ya = reinterpret_cast<uintptr_t>(call.Y);
     if (xa & 15) return false;                                   // TMA global address
     if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0 && (ya & 3) == 0;
-    return h.d == 1 && (ya & 15) == 0;   // BSF with d > 1: FP32 kernels (TF32 gather not built yet)
+    if (ya & 15) return false;
+    return h.d == 1 || bsfj_ok(h);      // BSF: d = 1 direct; d % 4 == 0 four-j gather
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
-    return call.layout == KS_LAYOUT_BSL ? launch_layout<KS_LAYOUT_BSL>(h, call)
-                                        : launch_layout<KS_LAYOUT_BSF>(h, call);
+    if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL>(h, call);
+    if (h.d == 1) return launch_layout<KS_LAYOUT_BSF>(h, call);
+    switch (pick_bn_j(h.b)) {
+        case 64: return launch_bsfj<64>(h, call);
+        case 48: return launch_bsfj<48>(h, call);
+        case 32: return launch_bsfj<32>(h, call);
+        case 16: return launch_bsfj<16>(h, call);
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace ks

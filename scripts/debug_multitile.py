@@ -1,0 +1,36 @@
+"""Compare the TF32 kernel against the oracle with a capped persistent grid
+(KS_TF32_MAXGRID set by the caller) so each CTA runs several tiles."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import ksgen  # noqa: E402
+import oracle as O  # noqa: E402
+import paper_2405_15013_b200 as ksb  # noqa: E402
+
+worst = 0.0
+for p, lay, B in [((1, 64, 64, 4), "bsf", 1024), ((1, 64, 64, 4), "bsl", 1024), ((1, 64, 64, 1), "bsf", 1024),
+                  ((2, 48, 48, 8), "bsf", 512), ((1, 128, 128, 8), "bsf", 512), ((2, 96, 96, 1), "bsl", 772),
+                  ((1, 256, 64, 16), "bsf", 300)]:
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_uniform(*p, seed=3)
+    X = ksgen.x_normal(B, N, seed=4)
+    f = ksb.Factor(*p, K4).set_math(ksb.MATH_TF32)
+    Xd = torch.from_numpy(X if lay == "bsf" else ksgen.to_bsl(X)).cuda()
+    Y = ksb.matmul(f, Xd, layout=lay)
+    torch.cuda.synchronize()
+    Yh = Y.cpu().numpy() if lay == "bsf" else Y.cpu().numpy().T
+    ref = O.matmul(p, K4, X)
+    err_rows = np.abs(Yh - ref).max(axis=1) / np.abs(ref).max()
+    bad = np.nonzero(err_rows > 5e-3)[0]
+    print(p, lay, B, "maxgrid", os.environ.get("KS_TF32_MAXGRID"), "err", O.normwise_error(Yh, ref),
+          "bad rows", len(bad), bad[:10], "bad blocks(128)", sorted(set((bad // 128).tolist()))[:20])
+    worst = max(worst, O.normwise_error(Yh, ref))
+    if len(bad):
+        r = bad[0]
+        badc = np.nonzero(np.abs(Yh[r] - ref[r]) > 5e-3 * np.abs(ref).max())[0]
+        print("   row", r, "bad cols", len(badc), badc[:20])
+sys.exit(0 if worst <= 5e-3 else 1)

@@ -44,7 +44,10 @@ def run(ksb, f, X_bsf, layout):
 CASES = [((1, 48, 48, 1), "bsf"), ((1, 64, 64, 1), "bsf"), ((2, 128, 128, 1), "bsf"), ((1, 768, 192, 2), "bsl"),
          ((6, 64, 64, 1), "bsf"), ((6, 64, 256, 1), "bsf"), ((64, 64, 64, 1), "bsf"), ((1, 256, 64, 16), "bsl"),
          ((1, 48, 48, 64), "bsl"), ((3, 96, 96, 4), "bsl"), ((1, 128, 128, 3), "bsl"), ((2, 16, 24, 3), "bsl"),
-         ((1, 16, 16, 1), "bsf"), ((1, 320, 40, 2), "bsl"), ((2, 96, 96, 1), "bsl"), ((6, 64, 64, 1), "bsl")]
+         ((1, 16, 16, 1), "bsf"), ((1, 320, 40, 2), "bsl"), ((2, 96, 96, 1), "bsl"), ((6, 64, 64, 1), "bsl"),
+         # BSF, d % 4 == 0: four-j TMA gather
+         ((1, 64, 64, 4), "bsf"), ((2, 48, 48, 16), "bsf"), ((1, 128, 128, 8), "bsf"), ((3, 96, 96, 4), "bsf"),
+         ((1, 64, 256, 16), "bsf"), ((1, 256, 64, 16), "bsf"), ((2, 16, 32, 12), "bsf")]
 
 
 @pytest.mark.parametrize("p,layout", CASES)
@@ -102,15 +105,32 @@ def test_tf32_model_chains_bsl(ksb, name):
     assert err <= TF32_TOL, err
 
 
-@pytest.mark.parametrize("p", [(1, 128, 128, 64), (4, 64, 64, 16), (1, 96, 96, 1)])
-def test_tf32_sweep_full_size_sampled_rows(ksb, p):
-    """configs[2] at B = 25088, TF32, BSL (the layout the TF32 path serves)."""
+@pytest.mark.parametrize("p,layout", [((1, 128, 128, 64), "bsl"), ((4, 64, 64, 16), "bsl"), ((1, 96, 96, 1), "bsl"),
+                                      ((1, 128, 128, 64), "bsf"), ((4, 64, 64, 16), "bsf"), ((1, 96, 96, 1), "bsf")])
+def test_tf32_sweep_full_size_sampled_rows(ksb, p, layout):
+    """configs[2] at B = 25088, TF32, both layouts, in bench's launch configuration."""
     B = configs.SWEEP_BATCH
     M, N, _ = O.dims(p)
     K4 = ksgen.k4_uniform(*p, seed=1000)
     X = ksgen.x_normal(B, N, seed=0)
     f = ksb.Factor(*p, K4).set_math(ksb.MATH_TF32)
-    Yg = run(ksb, f, X, "bsl")
+    assert f.plan(B, layout) == "tf32"
+    Yg = run(ksb, f, X, layout)
     rows = np.array([0, 1, 127, 128, 12543, 25087] + list(np.random.default_rng(3).integers(0, B, 4)))
     Yref = O.matmul(p, K4, X, rows=rows)
     assert O.normwise_error(Yg[rows], Yref) <= TF32_TOL
+
+
+@pytest.mark.parametrize("grid", [1, 2, 3])
+def test_tf32_many_tiles_per_cta(grid):
+    """Persistent kernels with a capped grid (KS_TF32_MAXGRID) so every CTA runs
+    several tiles: exercises the mbarrier ring / TMEM double-buffer wrap-around
+    (a missing proxy fence once showed up only here)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KS_TF32_MAXGRID=str(grid))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "debug_multitile.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
