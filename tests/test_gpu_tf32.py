@@ -131,6 +131,6 @@ def test_tf32_many_tiles_per_cta(grid):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, KS_TF32_MAXGRID=str(grid))
-    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "debug_multitile.py")], env=env,
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "multitile_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
