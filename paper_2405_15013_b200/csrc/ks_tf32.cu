@@ -150,9 +150,12 @@ template <int LAYOUT, int BN>
 struct Tf32Cfg {
     static constexpr int B_BYTES = BN * BKC * 4;          // BN * 128 B (multiple of 1 KB)
     static constexpr int SLOT = A_BYTES + B_BYTES;
-    static constexpr int CTAS = BN <= 64 ? 2 : 1;                                 // CTAs per SM
-    static constexpr int BUDGET = CTAS == 2 ? 108 * 1024 : 200 * 1024;
-    static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? 3 : BN > 128 ? 3 : 6) : 0;   // staging
+    // Two co-resident CTAs per SM (TMEM 2 x 2*BN <= 512 columns, ~110 KB smem each)
+    // measured ~1.4x faster than one deep-pipelined CTA: more independent
+    // tiles in flight hide TMA latency better than a deeper ring.
+    static constexpr int CTAS = BN <= 128 ? 2 : 1;                                // CTAs per SM
+    static constexpr int BUDGET = CTAS == 2 ? 110 * 1024 : 200 * 1024;
+    static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 ? 3 : 2) : 3) : 0;   // staging
     static constexpr int S_FIT = (BUDGET - P * STG_BYTES) / SLOT;
     static constexpr int S = S_FIT > 6 ? 6 : S_FIT;                              // operand slots
     static constexpr int BAR_OFF = S * SLOT + P * STG_BYTES;
@@ -636,9 +639,12 @@ int debug_flags() {
     return v;
 }
 
+// Output-tile width: the whole block when b <= 128 (two CTAs per SM fit), else
+// the largest divisor <= 128 (b/BN tiles share one X tile through L2: the tile
+// order runs the k-chunks of a tile back to back).
 int pick_bn(int64_t b) {
-    if (b <= 256 && b % 16 == 0) return (int)b;
-    for (int bn : {256, 192, 128, 96, 64, 48, 32, 16})
+    if (b <= 128 && b % 16 == 0) return (int)b;
+    for (int bn : {128, 112, 96, 80, 64, 48, 32, 16})
         if (b % bn == 0) return bn;
     return 0;
 }
