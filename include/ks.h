@@ -63,7 +63,8 @@ typedef enum {
     KS_KERNEL_GENERIC = 1,  /* one thread per output element, any pattern   */
     KS_KERNEL_STREAM = 2,   /* vectorised streaming kernel, b,c in {1,2,4}  */
     KS_KERNEL_FFMA = 3,     /* register-tiled FP32 kernel, larger b,c       */
-    KS_KERNEL_TF32 = 4      /* tcgen05 TF32 tensor-core kernel              */
+    KS_KERNEL_TF32 = 4,     /* tcgen05 TF32 tensor-core kernel              */
+    KS_KERNEL_FUSED_CHAIN = 5  /* whole chain in one launch (trace records only) */
 } ks_kernel_t;
 
 typedef enum {
@@ -135,6 +136,19 @@ ks_status_t ks_chain(const ks_handle_t* handles, int L, const float* X, float* Y
 /* Same as ks_chain with an explicit layout for X, Y and the intermediates. */
 ks_status_t ks_chain_ex(const ks_handle_t* handles, int L, const float* X, float* Y,
                         int64_t B, ks_layout_t layout, ks_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Chain fusion policy (process-wide, default on).  When on, ks_chain /
+ * ks_chain_ex / ks_chain_host run an eligible chain -- BSF, 2 <= L <= 32,
+ * every factor square with b = c in {2, 4} (e.g. the FFT / square dyadic
+ * butterfly) and FP32 math -- as ONE kernel that keeps R batch rows
+ * in shared memory across all factors: X is read and Y
+ * written once instead of one HBM round trip per factor.  The result is
+ * bit-identical to the per-factor launches.  Off: one launch per factor.
+ * ks_chain_fusion_eligible reports whether a call would fuse (1) or not (0).
+ * ------------------------------------------------------------------------- */
+ks_status_t ks_set_chain_fusion(int enable);
+int ks_chain_fusion_eligible(const ks_handle_t* handles, int L, int64_t B, ks_layout_t layout);
 
 /* ---------------------------------------------------------------------------
  * ks_chain_host -- end-to-end form of ks_chain_ex for HOST buffers: X_host and

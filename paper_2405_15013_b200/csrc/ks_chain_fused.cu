@@ -1,0 +1,234 @@
+// Fused multi-factor chain kernel: applies every factor of
+// a square small-block chain (b_l = c_l = BB in {2, 4}, all dimensions equal,
+// e.g. the FFT / square dyadic butterfly, Table 3)
+// to R batch rows held in shared memory, so X is read once and Y written once
+// instead of one HBM round trip per factor.
+//
+// Why it is legal in place: with b = c the output rows row_{i,j} (Alg. 2 line 3,
+// PAPER.md:356) and input columns col_{i,j} (line 4) of a block are the same
+// index set {i*b*d + l*d + j}, and the blocks partition [0, N),
+// so each (i, j) block of each row is read and rewritten by exactly one thread.
+//
+// Arithmetic per output: l ascending, one FP32 FMA chain starting from 0 -- the
+// exact operation sequence of the per-factor kernels, so the fused chain is
+// bit-identical to L separate ks_matmul launches (tested).
+//
+// Passes: consecutive square-dyadic factors whose d doubles (the DIT order of
+// the chain application, K_L first) are grouped up to 3 per shared-memory pass
+// ("radix-8"): a thread loads the 8 values {base + m*d0}, applies the 2-3
+// factors in registers and writes them back, cutting shared-memory traffic 3x.
+// Other factor sequences run one factor per pass.
+#include "ks_internal.h"
+
+#include <vector>
+
+namespace {
+
+constexpr int MAXF = 32;
+constexpr int THREADS = 256;
+
+struct FusedFactor {
+    const float* k;   // canonical K4 of the factor
+    int a, d;
+};
+
+struct FusedParams {
+    FusedFactor f[MAXF];   // application order (K_L first)
+    int pass_len[MAXF];    // number of factors in each pass (1..3), passes in order
+    int npass;
+    int N;                 // row length (all dims equal)
+};
+
+// One radix-2^T pass over all rows of the tile, T consecutive dyadic factors
+// (b = c = 2) with d, 2d, 4d.
+template <int T>
+__device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const FusedFactor* F) {
+    constexpr int E = 1 << T;
+    const int d0 = F[0].d;
+    const int nitem = N / E;                      // (super-block of the last factor, j) pairs
+    for (int it = threadIdx.x; it < nitem; it += THREADS) {
+        const int j = it % d0;
+        const int blk = it / d0;                  // super-block of size E*d0
+        const int base = blk * (E * d0) + j;
+        // weights: for factor t, pair p (bit t of m = 0), K4[i][k][l][jt]
+        float kw[T][E / 2][4];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int dt = d0 << t;
+#pragma unroll
+            for (int p = 0; p < E / 2; ++p) {
+                // p enumerates m with bit t cleared
+                const int lo = p & ((1 << t) - 1);
+                const int m = ((p >> t) << (t + 1)) | lo;
+                const int s = base + m * d0;
+                const int i = s / (2 * dt);
+                const int jt = s % dt;
+                const float* kp = F[t].k + ((int64_t)(i * 2) * 2) * dt + jt;   // K4[i][0][0][jt]
+                kw[t][p][0] = __ldg(kp);              // k=0,l=0
+                kw[t][p][1] = __ldg(kp + dt);         // k=0,l=1
+                kw[t][p][2] = __ldg(kp + 2 * dt);     // k=1,l=0
+                kw[t][p][3] = __ldg(kp + 3 * dt);     // k=1,l=1
+            }
+        }
+        for (int r = 0; r < rows; ++r) {
+            float* row = sm + (size_t)r * N + base;
+            float v[E];
+            if (d0 == 1) {                         // E consecutive floats: vector shared loads
+#pragma unroll
+                for (int m = 0; m < E; m += 4) {
+                    const float4 q = *reinterpret_cast<const float4*>(row + m);
+                    v[m] = q.x; v[m + 1] = q.y; v[m + 2] = q.z; v[m + 3] = q.w;
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = row[m * d0];
+            }
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+#pragma unroll
+                for (int p = 0; p < E / 2; ++p) {
+                    const int lo = p & ((1 << t) - 1);
+                    const int m0 = ((p >> t) << (t + 1)) | lo;
+                    const int m1 = m0 | (1 << t);
+                    const float x0 = v[m0], x1 = v[m1];
+                    v[m0] = fmaf(x1, kw[t][p][1], fmaf(x0, kw[t][p][0], 0.f));
+                    v[m1] = fmaf(x1, kw[t][p][3], fmaf(x0, kw[t][p][2], 0.f));
+                }
+            }
+            if (d0 == 1) {
+#pragma unroll
+                for (int m = 0; m < E; m += 4)
+                    *reinterpret_cast<float4*>(row + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
+            } else {
+#pragma unroll
+                for (int m = 0; m < E; ++m) row[m * d0] = v[m];
+            }
+        }
+    }
+}
+
+// One factor with b = c = BB (any a, d) per pass.
+template <int BB>
+__device__ __forceinline__ void block_pass(float* sm, int rows, int N, const FusedFactor& F) {
+    const int d = F.d;
+    const int nblk = F.a * d;
+    for (int blk = threadIdx.x; blk < nblk; blk += THREADS) {
+        const int i = blk / d, j = blk % d;
+        float kr[BB][BB];
+#pragma unroll
+        for (int k = 0; k < BB; ++k)
+#pragma unroll
+            for (int l = 0; l < BB; ++l) kr[k][l] = __ldg(F.k + ((int64_t)(i * BB + k) * BB + l) * d + j);
+        const int base = i * BB * d + j;
+        for (int r = 0; r < rows; ++r) {
+            float* row = sm + (size_t)r * N + base;
+            float x[BB];
+#pragma unroll
+            for (int l = 0; l < BB; ++l) x[l] = row[l * d];
+#pragma unroll
+            for (int k = 0; k < BB; ++k) {
+                float acc = 0.f;
+#pragma unroll
+                for (int l = 0; l < BB; ++l) acc = fmaf(x[l], kr[k][l], acc);
+                row[k * d] = acc;
+            }
+        }
+    }
+}
+
+template <int BB>
+__global__ void __launch_bounds__(THREADS, 2)
+ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, int64_t B, const __grid_constant__ FusedParams P,
+                      int R) {
+    extern __shared__ float4 sm4[];
+    float* sm = reinterpret_cast<float*>(sm4);
+    const int N = P.N;
+    for (int64_t row0 = (int64_t)blockIdx.x * R; row0 < B; row0 += (int64_t)gridDim.x * R) {
+        const int rows = (int)((B - row0) < R ? (B - row0) : R);
+        const int nv = rows * N / 4;
+        const float4* src = reinterpret_cast<const float4*>(X + row0 * N);
+        for (int e = threadIdx.x; e < nv; e += THREADS) sm4[e] = __ldcs(src + e);
+        __syncthreads();
+        int f = 0;
+        for (int ps = 0; ps < P.npass; ++ps) {
+            const int len = P.pass_len[ps];
+            if (BB == 2 && len == 3) dyadic_pass<3>(sm, rows, N, &P.f[f]);
+            else if (BB == 2 && len == 2) dyadic_pass<2>(sm, rows, N, &P.f[f]);
+            else block_pass<BB>(sm, rows, N, P.f[f]);
+            f += len;
+            __syncthreads();
+        }
+        float4* dst = reinterpret_cast<float4*>(Y + row0 * N);
+        for (int e = threadIdx.x; e < nv; e += THREADS) __stcs(dst + e, sm4[e]);
+        __syncthreads();
+    }
+}
+
+constexpr int SMEM_BUDGET = 100 * 1024;      // two CTAs per SM: one loads/stores while the other computes
+
+}  // namespace
+
+namespace ks {
+
+// Eligibility: BSF, L <= 32, every factor square with b = c = BB in {2, 4},
+// all dimensions equal to N, N % 4 == 0, at least one row fits in shared
+// memory, 16-byte aligned X and Y.
+bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call) {
+    if (call.layout != KS_LAYOUT_BSF || L < 2 || L > MAXF) return false;
+    const int64_t bb = hs[0]->b;
+    if (bb != 2 && bb != 4) return false;
+    const int64_t N = hs[0]->N;
+    for (int l = 0; l < L; ++l) {
+        if (hs[l]->b != bb || hs[l]->c != bb || hs[l]->N != N || hs[l]->M != N) return false;
+    }
+    if (N % 4 != 0 || N * 4 > SMEM_BUDGET || N > (int64_t(1) << 24)) return false;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
+    return (al & 15) == 0;
+}
+
+cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call) {
+    FusedParams P{};
+    const int64_t N = hs[0]->N;
+    P.N = (int)N;
+    // application order: K_L first (handles[L-1])
+    for (int t = 0; t < L; ++t) {
+        const ks_handle_s& h = *hs[L - 1 - t];
+        P.f[t] = FusedFactor{h.k_canon, (int)h.a, (int)h.d};
+    }
+    // group dyadic runs (b = c = 2, d doubling, a halving) into passes of <= 3
+    int t = 0;
+    P.npass = 0;
+    const bool dyadic = hs[0]->b == 2;
+    while (t < L) {
+        int len = 1;
+        if (dyadic) {
+            while (len < 3 && t + len < L && P.f[t + len].d == 2 * P.f[t + len - 1].d &&
+                   2 * P.f[t + len].a == P.f[t + len - 1].a)
+                ++len;
+        }
+        P.pass_len[P.npass++] = len;
+        t += len;
+    }
+    int64_t R = SMEM_BUDGET / (N * 4);
+    if (R > 16) R = 16;
+    const int64_t sms = num_sms(hs[0]->device);
+    // enough row groups to fill the machine
+    while (R > 1 && (call.B + R - 1) / R < sms) R /= 2;
+    const size_t smem = (size_t)R * N * 4;
+    int64_t groups = (call.B + R - 1) / R;
+    const int64_t grid = groups < sms ? groups : sms;
+    cudaError_t e;
+    if (hs[0]->b == 2) {
+        e = cudaFuncSetAttribute(ks_chain_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        ks_chain_fused_kernel<2><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.B, P, (int)R);
+    } else {
+        e = cudaFuncSetAttribute(ks_chain_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        ks_chain_fused_kernel<4><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.B, P, (int)R);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace ks

@@ -49,6 +49,10 @@ cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call);
 bool tf32_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);
 
+// Fused multi-factor chain (ks_chain_fused.cu): one launch for a whole chain.
+bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call);
+cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call);
+
 int num_sms(int device);
 
 }  // namespace ks

@@ -182,10 +182,47 @@ ks_status_t validate_chain(const ks_handle_t* hs, int L, int64_t B, int layout) 
     return KS_OK;
 }
 
+std::atomic<bool> g_fusion{true};
+
+bool fusion_ok(const ks_handle_t* hs, int L, const KsCall& call) {
+    if (!g_fusion.load(std::memory_order_relaxed) || L < 2) return false;
+    for (int l = 0; l < L; ++l)
+        if (hs[l]->forced != KS_KERNEL_AUTO || hs[l]->math != KS_MATH_FP32) return false;
+    return ks::fused_chain_supports(hs, L, call);
+}
+
+// Whole chain in one launch (validated arguments, fusion_ok true).
+ks_status_t run_fused(const ks_handle_t* hs, int L, const KsCall& call) {
+    TraceRec rec{nullptr, nullptr, (int)KS_KERNEL_FUSED_CHAIN, 0.0};
+    const bool tracing = g_trace_on.load(std::memory_order_relaxed);
+    if (tracing) {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        rec.start = trace_event();
+        rec.stop = trace_event();
+        double nnz = 0;
+        for (int l = 0; l < L; ++l) nnz += (double)hs[l]->nnz;
+        rec.bytes = 4.0 * ((double)call.B * (double)hs[L - 1]->N + nnz + (double)call.B * (double)hs[0]->M);
+        cudaEventRecord(rec.start, call.stream);
+    }
+    cudaError_t e = ks::fused_chain_launch(hs, L, call);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (tracing) {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        cudaEventRecord(rec.stop, call.stream);
+        g_trace.push_back(rec);
+    }
+    if (e != cudaSuccess) return fail_cuda(e, "fused chain launch");
+    return KS_OK;
+}
+
 // Chain on device buffers; X, Y validated by the caller.
 ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
                       int layout, cudaStream_t s) {
     if (L == 1) return run_one(*hs[0], X, Y, B, layout, s);
+    {
+        KsCall call{X, Y, B, layout, s};
+        if (fusion_ok(hs, L, call)) return run_fused(hs, L, call);
+    }
     int64_t maxdim = 0;
     for (int l = 1; l < L; ++l) maxdim = hs[l]->M > maxdim ? hs[l]->M : maxdim;
     cudaMemPool_t pool;
@@ -358,6 +395,20 @@ ks_status_t ks_chain_ex(const ks_handle_t* hs, int L, const float* X, float* Y, 
     if (overlap(X, B * hs[L - 1]->N * 4, Y, B * hs[0]->M * 4)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
     s = run_chain(hs, L, X, Y, B, (int)layout, static_cast<cudaStream_t>(stream));
     return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_set_chain_fusion(int enable) {
+    g_fusion.store(enable != 0);
+    return ok();
+}
+
+int ks_chain_fusion_eligible(const ks_handle_t* hs, int L, int64_t B, ks_layout_t layout) {
+    if (validate_chain(hs, L, B, (int)layout) != KS_OK) return 0;
+    // plans assume 256-byte aligned (allocator) pointers
+    KsCall call{reinterpret_cast<const float*>(uintptr_t(256)), reinterpret_cast<float*>(uintptr_t(256)), B,
+                (int)layout, nullptr};
+    ok();
+    return fusion_ok(hs, L, call) ? 1 : 0;
 }
 
 ks_status_t ks_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,

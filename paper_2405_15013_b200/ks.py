@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libks.so")
 BSF, BSL = 0, 1
 MATH_FP32, MATH_TF32 = 0, 1
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STREAM, KERNEL_FFMA, KERNEL_TF32 = range(5)
-KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32"}
+KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32", 5: "fused_chain"}
 
 STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_CHAIN_SHAPE",
           4: "KS_ERR_UNSUPPORTED", 5: "KS_ERR_DEVICE", 6: "KS_ERR_ALIGNMENT", 7: "KS_ERR_OOM",
@@ -26,7 +26,8 @@ STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_C
 
 # Every symbol include/ks.h declares (tests check the .so exports them all).
 EXPORTS = ["ks_pack_weights", "ks_free", "ks_get_pattern", "ks_set_math", "ks_set_kernel",
-           "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_chain_host", "ks_read_packed",
+           "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_set_chain_fusion",
+           "ks_chain_fusion_eligible", "ks_chain_host", "ks_read_packed",
            "ks_trace_enable", "ks_trace_read",
            "ks_last_error", "ks_last_error_message", "ks_status_string",
            "ks_kernel_launch_count", "ks_abi_version"]
@@ -69,6 +70,10 @@ def load_library(path: str = LIB_PATH):
     lib.ks_chain.restype = st
     lib.ks_chain_ex.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, ctypes.c_int, vp]
     lib.ks_chain_ex.restype = st
+    lib.ks_set_chain_fusion.argtypes = [ctypes.c_int]
+    lib.ks_set_chain_fusion.restype = st
+    lib.ks_chain_fusion_eligible.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int]
+    lib.ks_chain_fusion_eligible.restype = ctypes.c_int
     lib.ks_chain_host.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, ctypes.c_int, vp]
     lib.ks_chain_host.restype = st
     lib.ks_read_packed.argtypes = [vp, ctypes.c_int, fp, i64]
@@ -239,6 +244,15 @@ def chain(factors, X, Y=None, layout="bsf", stream=None):
     _check(_lib.ks_chain_ex(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"),
                             int(B), lay, _stream_ptr(stream)))
     return Y
+
+
+def set_chain_fusion(enable: bool):
+    """Process-wide chain fusion policy (ks_set_chain_fusion); default on."""
+    _check(load_library().ks_set_chain_fusion(1 if enable else 0))
+
+
+def chain_fusion_eligible(factors, B: int, layout="bsf") -> bool:
+    return bool(load_library().ks_chain_fusion_eligible(_handles(factors), len(factors), int(B), _layout(layout)))
 
 
 def chain_host(factors, X_host, Y_host, layout="bsf", stream=None):

@@ -1,0 +1,116 @@
+"""Fused multi-factor chain kernel (NEXT-1): same result as the per-factor
+launches, bit for bit (identical FMA order), and the oracle contract."""
+import numpy as np
+import pytest
+
+import ksgen
+from ksgen import configs
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ksb():
+    import paper_2405_15013_b200 as ksb
+    ksb.load_library()
+    yield ksb
+    ksb.set_chain_fusion(True)
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda:0")
+
+
+def both(ksb, fs, X):
+    ksb.set_chain_fusion(True)
+    n0 = ksb.launch_count()
+    Yf = ksb.chain(fs, to_dev(X))
+    torch.cuda.synchronize()
+    fused_launches = ksb.launch_count() - n0
+    ksb.set_chain_fusion(False)
+    Yu = ksb.chain(fs, to_dev(X))
+    torch.cuda.synchronize()
+    ksb.set_chain_fusion(True)
+    return Yf.cpu().numpy(), Yu.cpu().numpy(), fused_launches
+
+
+CHAINS = {
+    "dyadic3": configs.dyadic_patterns(3),
+    "dyadic7": configs.dyadic_patterns(7),
+    "dyadic12": configs.dyadic_patterns(12),
+    "kaleidoscope6": configs.dyadic_patterns(6) + list(reversed(configs.dyadic_patterns(6))),
+    "radix4_butterfly": [(1, 4, 4, 16), (4, 4, 4, 4), (16, 4, 4, 1)],
+    "square_mixed": [(2, 2, 2, 4), (8, 2, 2, 1), (4, 2, 2, 2), (1, 2, 2, 8)],
+}
+
+
+@pytest.mark.parametrize("name", sorted(CHAINS))
+@pytest.mark.parametrize("B", [1, 7, 300])
+def test_fused_equals_per_factor_bitwise(ksb, name, B):
+    pats = CHAINS[name]
+    N = configs.chain_dims(pats)[0]
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    assert ksb.chain_fusion_eligible(fs, B, "bsf")
+    X = ksgen.x_normal(B, N, seed=0)
+    Yf, Yu, nl = both(ksb, fs, X)
+    assert nl == 1
+    assert np.array_equal(Yf, Yu)
+    assert O.normwise_error(Yf, O.chain(pats, K4s, X)) <= 1e-5
+
+
+@pytest.mark.parametrize("L", [2, 5, 12])
+def test_fused_hadamard_exact(ksb, L):
+    pats, K4s = O.hadamard_factors(L)
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    X = ksgen.x_int(33, 2 ** L, seed=2002)
+    Yf, _, _ = both(ksb, fs, X)
+    assert np.array_equal(Yf.astype(np.float64), O.chain(pats, K4s, X))
+
+
+def test_fused_fft_full_size_sampled_rows(ksb):
+    """configs[1] (B = 8192) through the fused kernel, sampled rows vs the oracle."""
+    L, B = configs.FFT_L, configs.FFT_BATCH
+    pats = configs.dyadic_patterns(L)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    X = ksgen.x_normal(B, 2 ** L, seed=0)
+    Yf, Yu, nl = both(ksb, fs, X)
+    assert nl == 1 and np.array_equal(Yf, Yu)
+    rows = np.array([0, 5, 4095, 8191])
+    assert O.normwise_error(Yf[rows], O.chain(pats, K4s, X, rows=rows)) <= 1e-5
+
+
+def test_fusion_eligibility(ksb):
+    pats = configs.dyadic_patterns(4)
+    fs = [ksb.Factor(*p, ksgen.k4_uniform(*p, seed=1)) for p in pats]
+    assert ksb.chain_fusion_eligible(fs, 64, "bsf")
+    assert not ksb.chain_fusion_eligible(fs, 64, "bsl")          # BSF only
+    fs[0].set_kernel(ksb.KERNEL_GENERIC)                         # forced kernel -> per factor
+    assert not ksb.chain_fusion_eligible(fs, 64, "bsf")
+    fs[0].set_kernel(ksb.KERNEL_AUTO)
+    ksb.set_chain_fusion(False)
+    assert not ksb.chain_fusion_eligible(fs, 64, "bsf")
+    ksb.set_chain_fusion(True)
+    g = [ksb.Factor(*p, ksgen.k4_uniform(*p, seed=1)) for p in configs.VIT_UP]
+    assert not ksb.chain_fusion_eligible(g, 64, "bsf")           # not square small-block
+
+
+def test_fused_chain_host_and_trace(ksb):
+    pats = configs.dyadic_patterns(10)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    X = ksgen.x_normal(100, 1024, seed=0)
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh = torch.empty((100, 1024)).pin_memory()
+    ksb.trace_enable(True)
+    ksb.chain_host(fs, Xh, Yh)
+    torch.cuda.synchronize()
+    ms, fam, byts = ksb.trace_read()
+    ksb.trace_enable(False)
+    assert fam == ["fused_chain"]
+    assert byts[0] == 4 * (100 * 1024 * 2 + sum(np.prod(p) for p in pats))
+    Yf, Yu, _ = both(ksb, fs, X)
+    assert np.array_equal(Yh.numpy(), Yu)
