@@ -20,12 +20,12 @@
 // Other factor sequences run one factor per pass.
 #include "ks_internal.h"
 
-#include <vector>
+#include <cstdlib>
 
 namespace {
 
 constexpr int MAXF = 32;
-constexpr int THREADS = 256;
+constexpr int THREADS = 512;
 
 struct FusedFactor {
     const float* k;   // canonical K4 of the factor
@@ -52,17 +52,38 @@ __device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const Fu
         const int base = blk * (E * d0) + j;
         // weights: for factor t, pair p (bit t of m = 0), K4[i][k][l][jt]
         float kw[T][E / 2][4];
+        if (d0 == 1) {
+            // the item's weights of factor t are one 2^(T+1)-float run starting at
+            // blk * 2^(T+1): vector loads; offset of (pair p, k, l) inside the run is
+            // (p >> t) * 4 * 2^t + (2k + l) * 2^t + (p mod 2^t)
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                float kk[2 * E];
+                const float4* src = reinterpret_cast<const float4*>(F[t].k + (int64_t)blk * (2 * E));
+#pragma unroll
+                for (int q = 0; q < E / 2; ++q) {
+                    const float4 w = __ldg(src + q);
+                    kk[4 * q] = w.x; kk[4 * q + 1] = w.y; kk[4 * q + 2] = w.z; kk[4 * q + 3] = w.w;
+                }
+#pragma unroll
+                for (int p = 0; p < E / 2; ++p)
+#pragma unroll
+                    for (int kl = 0; kl < 4; ++kl)
+                        kw[t][p][kl] = kk[(p >> t) * 4 * (1 << t) + kl * (1 << t) + (p & ((1 << t) - 1))];
+            }
+        } else
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             const int dt = d0 << t;
 #pragma unroll
             for (int p = 0; p < E / 2; ++p) {
-                // p enumerates m with bit t cleared
+                // p enumerates m with bit t cleared; s = base + m*d0 = d0*(blk*E + m) + j
+                // with j < d0, so for factor t (d_t = d0 * 2^t, super-block 2*d_t):
+                //   i  = s / (2 d_t) = (blk*E + m) >> (t+1),  j_t = s % d_t = d0*(m mod 2^t) + j
                 const int lo = p & ((1 << t) - 1);
                 const int m = ((p >> t) << (t + 1)) | lo;
-                const int s = base + m * d0;
-                const int i = s / (2 * dt);
-                const int jt = s % dt;
+                const int i = (blk << (T - t - 1)) + (m >> (t + 1));
+                const int jt = d0 * (m & ((1 << t) - 1)) + j;
                 const float* kp = F[t].k + ((int64_t)(i * 2) * 2) * dt + jt;   // K4[i][0][0][jt]
                 kw[t][p][0] = __ldg(kp);              // k=0,l=0
                 kw[t][p][1] = __ldg(kp + dt);         // k=0,l=1
@@ -136,19 +157,58 @@ __device__ __forceinline__ void block_pass(float* sm, int rows, int N, const Fus
     }
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Row groups move by bulk asynchronous copies (TMA engine, cp.async.bulk): the
+// next group streams into the second buffer while this one is computed, and
+// the finished group drains to HBM in the background.
 template <int BB>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, 1)
 ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, int64_t B, const __grid_constant__ FusedParams P,
                       int R) {
-    extern __shared__ float4 sm4[];
-    float* sm = reinterpret_cast<float*>(sm4);
+    extern __shared__ __align__(128) float4 sm4[];
+    __shared__ __align__(8) uint64_t full[2];
     const int N = P.N;
-    for (int64_t row0 = (int64_t)blockIdx.x * R; row0 < B; row0 += (int64_t)gridDim.x * R) {
-        const int rows = (int)((B - row0) < R ? (B - row0) : R);
-        const int nv = rows * N / 4;
-        const float4* src = reinterpret_cast<const float4*>(X + row0 * N);
-        for (int e = threadIdx.x; e < nv; e += THREADS) sm4[e] = __ldcs(src + e);
-        __syncthreads();
+    float* buf[2] = {reinterpret_cast<float*>(sm4), reinterpret_cast<float*>(sm4) + (size_t)R * N};
+    const int64_t ngroups = (B + R - 1) / R;
+    const int64_t mine = ngroups > blockIdx.x ? (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto group_rows = [&](int64_t k) {
+        const int64_t row0 = ((int64_t)blockIdx.x + k * gridDim.x) * R;
+        return (int)((B - row0) < R ? (B - row0) : R);
+    };
+    auto issue_load = [&](int64_t k) {          // thread 0 only
+        const int64_t row0 = ((int64_t)blockIdx.x + k * gridDim.x) * R;
+        const uint32_t bytes = (uint32_t)group_rows(k) * (uint32_t)N * 4u;
+        const uint32_t bar = smem_u32(&full[k & 1]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(buf[k & 1])), "l"(X + row0 * N), "r"(bytes), "r"(bar) : "memory");
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (mine > 0) issue_load(0);
+    }
+    __syncthreads();
+    for (int64_t k = 0; k < mine; ++k) {
+        if (threadIdx.x == 0 && k + 1 < mine) {
+            // the other buffer's previous contents (group k-1) must have left for HBM
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            issue_load(k + 1);
+        }
+        {
+            const uint32_t bar = smem_u32(&full[k & 1]);
+            const uint32_t par = (uint32_t)((k >> 1) & 1);
+            asm volatile(
+                "{\n.reg .pred P1;\nLAB_WAIT:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}\n" ::"r"(bar), "r"(par) : "memory");
+        }
+        float* sm = buf[k & 1];
+        const int rows = group_rows(k);
         int f = 0;
         for (int ps = 0; ps < P.npass; ++ps) {
             const int len = P.pass_len[ps];
@@ -158,13 +218,21 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, int64_
             f += len;
             __syncthreads();
         }
-        float4* dst = reinterpret_cast<float4*>(Y + row0 * N);
-        for (int e = threadIdx.x; e < nv; e += THREADS) __stcs(dst + e, sm4[e]);
+        // generic writes/reads of this buffer before the async-proxy store (and the
+        // later refill of the buffer)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
+        if (threadIdx.x == 0) {
+            const int64_t row0 = ((int64_t)blockIdx.x + k * gridDim.x) * R;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(Y + row0 * N), "r"(smem_u32(sm)), "r"((uint32_t)rows * (uint32_t)N * 4u) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
     }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-constexpr int SMEM_BUDGET = 100 * 1024;      // two CTAs per SM: one loads/stores while the other computes
+constexpr int SMEM_BUDGET = 200 * 1024;      // two row-group buffers (double-buffered)
 
 }  // namespace
 
@@ -181,7 +249,7 @@ bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call) {
     for (int l = 0; l < L; ++l) {
         if (hs[l]->b != bb || hs[l]->c != bb || hs[l]->N != N || hs[l]->M != N) return false;
     }
-    if (N % 4 != 0 || N * 4 > SMEM_BUDGET || N > (int64_t(1) << 24)) return false;
+    if (N % 4 != 0 || 2 * N * 4 > SMEM_BUDGET || N > (int64_t(1) << 24)) return false;
     const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
     return (al & 15) == 0;
 }
@@ -199,24 +267,29 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
     int t = 0;
     P.npass = 0;
     const bool dyadic = hs[0]->b == 2;
+    static const int max_len = [] {           // KS_FUSED_RADIX (experiments): 2, 4 or 8
+        const char* e = getenv("KS_FUSED_RADIX");
+        const int r = e ? atoi(e) : 8;
+        return r >= 8 ? 3 : r >= 4 ? 2 : 1;
+    }();
     while (t < L) {
         int len = 1;
         if (dyadic) {
-            while (len < 3 && t + len < L && P.f[t + len].d == 2 * P.f[t + len - 1].d &&
+            while (len < max_len && t + len < L && P.f[t + len].d == 2 * P.f[t + len - 1].d &&
                    2 * P.f[t + len].a == P.f[t + len - 1].a)
                 ++len;
         }
         P.pass_len[P.npass++] = len;
         t += len;
     }
-    int64_t R = SMEM_BUDGET / (N * 4);
+    int64_t R = SMEM_BUDGET / (2 * N * 4);                      // rows per buffer
     if (R > 16) R = 16;
     const int64_t sms = num_sms(hs[0]->device);
     // enough row groups to fill the machine
     while (R > 1 && (call.B + R - 1) / R < sms) R /= 2;
-    const size_t smem = (size_t)R * N * 4;
+    const size_t smem = (size_t)2 * R * N * 4;
     int64_t groups = (call.B + R - 1) / R;
-    const int64_t grid = groups < sms ? groups : sms;
+    const int64_t grid = groups < sms ? groups : sms;             // persistent, one CTA per SM
     cudaError_t e;
     if (hs[0]->b == 2) {
         e = cudaFuncSetAttribute(ks_chain_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
