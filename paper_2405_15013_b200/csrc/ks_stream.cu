@@ -16,6 +16,8 @@
 //   weights are warp-uniform scalars, every row load/store is a fully
 //   coalesced V-wide vector along the batch.
 // Reduction order: l ascending with FP32 FMA, identical in both layouts.
+#include <cstdlib>
+
 #include "ks_internal.h"
 
 namespace {
@@ -137,9 +139,17 @@ __global__ void __launch_bounds__(256) ks_stream_bsl(
     }
 }
 
-template <int BB, int CC, int V>
-cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
-    constexpr int RT = (BB * CC <= 4) ? 8 : 4;
+// KS_STREAM_RT (experiments only): rows per thread for the BSF stream kernel.
+int stream_rt() {
+    static int v = [] {
+        const char* e = getenv("KS_STREAM_RT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int BB, int CC, int V, int RT>
+cudaError_t launch_bsf_rt(const ks_handle_s& h, const KsCall& call) {
     const int threads = 256;
     const int64_t P = h.a * (h.d / V);
     const int64_t items = P * ((call.B + RT - 1) / RT);
@@ -148,6 +158,18 @@ cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
         call.X, h.k_canon, call.Y, call.B, (int)h.a, (int)h.d);
     ks::count_launch();
     return cudaGetLastError();
+}
+
+template <int BB, int CC, int V>
+cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
+    if (BB * CC <= 4) {
+        const int rt = stream_rt();
+        if (rt == 2) return launch_bsf_rt<BB, CC, V, 2>(h, call);
+        if (rt == 4) return launch_bsf_rt<BB, CC, V, 4>(h, call);
+        if (rt == 16) return launch_bsf_rt<BB, CC, V, 16>(h, call);
+        return launch_bsf_rt<BB, CC, V, 8>(h, call);
+    }
+    return launch_bsf_rt<BB, CC, V, 4>(h, call);
 }
 
 template <int BB, int CC, int V>
