@@ -107,11 +107,72 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
             "rows": rows}
 
 
+def permutation_share(dev, reps: int = 7, patterns=None, math: str = "fp32"):
+    """SURVEY §8f NEXT-4 / App. E.3 on B200: the share of
+    bmm+permute time spent in the two permutations, (dt - dt~)/dt, where dt~
+    times the same batched GEMM on the pre-permuted pattern (ad, b, c, 1) whose
+    permutations are identities.  BSF, as Fig. 3."""
+    import numpy as np
+    import torch
+
+    import ksgen
+
+    pats = patterns or ksgen.grid.sweep_patterns()
+    B = ksgen.configs.SWEEP_BATCH
+    torch.backends.cuda.matmul.allow_tf32 = (math == "tf32")
+    props = torch.cuda.get_device_properties(dev)
+    flush = torch.empty(2 * props.L2_cache_size, dtype=torch.uint8, device=dev)
+    nmax = max(p[0] * p[2] * p[3] for p in pats)
+    X = torch.randn((B, nmax), device=dev)
+    rows = []
+    for (a, b, c, d) in pats:
+        Kb = torch.from_numpy(ksgen.k4_uniform(a, b, c, d, seed=1).transpose(0, 3, 1, 2)
+                              .reshape(a * d, b, c).copy()).to(dev)
+        Xp = X[:, : a * c * d].contiguous()
+        t_full = _time(lambda: bmm_bsf(Xp, Kb, a, b, c, d), flush, reps)
+        t_noperm = _time(lambda: bmm_bsf(Xp, Kb, a * d, b, c, 1), flush, reps)
+        share = max(0.0, min(1.0, (t_full - t_noperm) / t_full))
+        rows.append({"pattern": [a, b, c, d], "h": (b + c) / (b * c), "bmm_ms": round(t_full, 5),
+                     "bmm_no_perm_ms": round(t_noperm, 5), "perm_share": round(share, 4)})
+    torch.backends.cuda.matmul.allow_tf32 = False
+    by_h = {}
+    for r in rows:
+        by_h.setdefault(round(r["h"], 6), []).append(r["perm_share"])
+    return {"math": math, "batch": B, "patterns": len(rows),
+            "median_share_by_h": {str(k): round(float(np.median(v)), 4) for k, v in sorted(by_h.items())},
+            "max_share": max(r["perm_share"] for r in rows), "rows": rows}
+
+
+def speedup_regression(sweep):
+    """The paper's heuristic fit: log speedup = b0 + b1 log density
+    + b2 log h, least squares over the sweep, per layout and min-over-layouts."""
+    import numpy as np
+    out = {}
+    for key in ("bsf_speedup", "bsl_speedup", "min_speedup"):
+        A, y = [], []
+        for r in sweep["rows"]:
+            a, b, c, d = r["pattern"]
+            A.append([1.0, np.log(1.0 / (a * d)), np.log((b + c) / (b * c))])
+            y.append(np.log(r[key]))
+        A, y = np.array(A), np.array(y)
+        coef, *_ = np.linalg.lstsq(A, y, rcond=None)
+        pred = A @ coef
+        r2 = 1 - np.sum((y - pred) ** 2) / max(np.sum((y - y.mean()) ** 2), 1e-30)
+        out[key] = {"b0": round(float(coef[0]), 4), "b_log_density": round(float(coef[1]), 4),
+                    "b_log_h": round(float(coef[2]), 4), "r2": round(float(r2), 4)}
+    out["paper_fp32_a100"] = {"b0": 1.69, "b_log_density": -0.031, "b_log_h": 0.325, "adj_r2": 0.697}
+    return out
+
+
 if __name__ == "__main__":
     import json
     import sys
     import torch
     dev = torch.device("cuda:0")
-    math = sys.argv[1] if len(sys.argv) > 1 else "fp32"
-    out = run_sweep(dev, math=math)
+    mode = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+    if mode == "perm":
+        out = {"fp32": permutation_share(dev, math="fp32"), "tf32": permutation_share(dev, math="tf32")}
+    else:
+        out = run_sweep(dev, math=mode)
+        out["regression"] = speedup_regression(out)
     print(json.dumps(out))
