@@ -138,6 +138,19 @@ ks_status_t ks_chain_ex(const ks_handle_t* handles, int L, const float* X, float
                         int64_t B, ks_layout_t layout, ks_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * KSLinear bias (the "+bias" rows of Table 7, PAPER.md:1563;
+ * S:406-415): the same operations with Y += 1 * bias^T fused into the epilogue of
+ * the last factor applied (K_1), i.e. Y(n, r) = (X K_L^T ... K_1^T)(n, r) + bias[r].
+ *   bias : device, M(K_1) floats, 4-byte aligned (16-byte alignment keeps the
+ *          vector paths), or NULL for no bias (then identical to ks_matmul /
+ *          ks_chain_ex).  The bias is added after the FP32 reduction.
+ * ------------------------------------------------------------------------- */
+ks_status_t ks_matmul_bias(ks_handle_t h, const float* X, float* Y, const float* bias,
+                           int64_t B, ks_layout_t layout, ks_stream_t stream);
+ks_status_t ks_chain_bias(const ks_handle_t* handles, int L, const float* X, float* Y,
+                          const float* bias, int64_t B, ks_layout_t layout, ks_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * Chain fusion policy (process-wide, default on).  When on, ks_chain /
  * ks_chain_ex / ks_chain_host run an eligible chain -- BSF, 2 <= L <= 32,
  * every factor square with b = c in {2, 4} (e.g. the FFT / square dyadic

@@ -9,3 +9,4 @@ from .ks import (  # noqa: F401
     Factor, KSError, matmul, chain, chain_host, launch_count, load_library, LIB_PATH, EXPORTS,
     trace_enable, trace_read, set_chain_fusion, chain_fusion_eligible,
 )
+from .kslinear import KSLinear  # noqa: F401

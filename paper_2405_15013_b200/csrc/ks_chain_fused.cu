@@ -166,8 +166,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // the finished group drains to HBM in the background.
 template <int BB>
 __global__ void __launch_bounds__(THREADS, 1)
-ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, int64_t B, const __grid_constant__ FusedParams P,
-                      int R) {
+ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const float* __restrict__ bias, int64_t B,
+                      const __grid_constant__ FusedParams P, int R) {
     extern __shared__ __align__(128) float4 sm4[];
     __shared__ __align__(8) uint64_t full[2];
     const int N = P.N;
@@ -218,6 +218,15 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, int64_
             f += len;
             __syncthreads();
         }
+        if (bias) {                                 // KSLinear bias after the last factor (NEXT-2)
+            for (int e = threadIdx.x; e < rows * N / 4; e += THREADS) {
+                float4 q = reinterpret_cast<float4*>(sm)[e];
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + (e % (N / 4)));
+                q.x += bb.x; q.y += bb.y; q.z += bb.z; q.w += bb.w;
+                reinterpret_cast<float4*>(sm)[e] = q;
+            }
+            __syncthreads();
+        }
         // generic writes/reads of this buffer before the async-proxy store (and the
         // later refill of the buffer)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -251,7 +260,7 @@ bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call) {
     }
     if (N % 4 != 0 || 2 * N * 4 > SMEM_BUDGET || N > (int64_t(1) << 24)) return false;
     const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
-    return (al & 15) == 0;
+    return ((al | reinterpret_cast<uintptr_t>(call.bias)) & 15) == 0;
 }
 
 cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call) {
@@ -294,11 +303,13 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
     if (hs[0]->b == 2) {
         e = cudaFuncSetAttribute(ks_chain_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        ks_chain_fused_kernel<2><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.B, P, (int)R);
+        ks_chain_fused_kernel<2><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.bias, call.B, P,
+                                                                                 (int)R);
     } else {
         e = cudaFuncSetAttribute(ks_chain_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        ks_chain_fused_kernel<4><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.B, P, (int)R);
+        ks_chain_fused_kernel<4><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.bias, call.B, P,
+                                                                                 (int)R);
     }
     count_launch();
     return cudaGetLastError();

@@ -63,7 +63,7 @@ struct Cfg {
 template <int LAYOUT, int J, int WPJM, int WPJN, int TN>
 __global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN>::THREADS, 2)
 ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float* __restrict__ Y,
-               int64_t B, int a, int b, int c, int d) {
+               const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
     using C = Cfg<LAYOUT, J, WPJM, WPJN, TN>;
     using VT = typename VecJ<J>::T;
     extern __shared__ __align__(16) float smem[];
@@ -229,6 +229,14 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
 
     // ---- epilogue: each owned Y element written exactly once ------------------
     const int j = j0 + wj;
+    if (bias) {                                   // KSLinear bias (NEXT-2), per output row r
+#pragma unroll
+        for (int q = 0; q < TN; ++q) {
+            const float bq = __ldg(bias + (int64_t)i * b * d + (int64_t)(k0 + colB + q) * d + j);
+#pragma unroll
+            for (int m = 0; m < TM; ++m) acc[m][q] += bq;
+        }
+    }
     if (LAYOUT == KS_LAYOUT_BSL) {
         // Y[(i*b*d + k*d + j) * B + n], n contiguous
 #pragma unroll
@@ -324,7 +332,7 @@ cudaError_t launch_cfg(const ks_handle_s& h, const KsCall& call) {
     const int64_t blocks = nkc * nnb * (h.a * h.d / J);
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     kern<<<(unsigned)blocks, C::THREADS, C::SMEM_BYTES, call.stream>>>(
-        call.X, h.k_tile, call.Y, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d);
+        call.X, h.k_tile, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d);
     ks::count_launch();
     return cudaGetLastError();
 }

@@ -14,7 +14,7 @@ namespace {
 template <int LAYOUT>
 __global__ void __launch_bounds__(256) ks_generic_kernel(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
-    int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
+    const float* __restrict__ bias, int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
     const int64_t M = a * b * d, N = a * c * d;
     const int64_t total = B * M;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
             const float x = LAYOUT == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n];
             acc = fmaf(x, kp[l * d], acc);
         }
-        Y[e] = acc;
+        Y[e] = bias ? acc + bias[r] : acc;
     }
 }
 
@@ -53,10 +53,10 @@ cudaError_t generic_launch(const ks_handle_s& h, const KsCall& call) {
     if (blocks < 1) blocks = 1;
     if (call.layout == KS_LAYOUT_BSF)
         ks_generic_kernel<KS_LAYOUT_BSF><<<(unsigned)blocks, threads, 0, call.stream>>>(
-            call.X, h.k_canon, call.Y, call.B, h.a, h.b, h.c, h.d);
+            call.X, h.k_canon, call.Y, call.bias, call.B, h.a, h.b, h.c, h.d);
     else
         ks_generic_kernel<KS_LAYOUT_BSL><<<(unsigned)blocks, threads, 0, call.stream>>>(
-            call.X, h.k_canon, call.Y, call.B, h.a, h.b, h.c, h.d);
+            call.X, h.k_canon, call.Y, call.bias, call.B, h.a, h.b, h.c, h.d);
     count_launch();
     return cudaGetLastError();
 }

@@ -24,6 +24,7 @@ struct KsCall {
     int64_t B;
     int layout;           // ks_layout_t
     cudaStream_t stream;
+    const float* bias = nullptr;   // optional length-M vector added in the epilogue
 };
 
 namespace ks {

@@ -133,8 +133,8 @@ cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
 
 // One factor, arguments already validated.
 ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, int layout,
-                    cudaStream_t s) {
-    KsCall call{X, Y, B, layout, s};
+                    cudaStream_t s, const float* bias = nullptr) {
+    KsCall call{X, Y, B, layout, s, bias};
     ks_kernel_t k = choose(h, call);
     if (k == KS_KERNEL_AUTO)
         return fail(KS_ERR_UNSUPPORTED, "forced kernel %d cannot run pattern (%lld,%lld,%lld,%lld) "
@@ -217,10 +217,10 @@ ks_status_t run_fused(const ks_handle_t* hs, int L, const KsCall& call) {
 
 // Chain on device buffers; X, Y validated by the caller.
 ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
-                      int layout, cudaStream_t s) {
-    if (L == 1) return run_one(*hs[0], X, Y, B, layout, s);
+                      int layout, cudaStream_t s, const float* bias = nullptr) {
+    if (L == 1) return run_one(*hs[0], X, Y, B, layout, s, bias);
     {
-        KsCall call{X, Y, B, layout, s};
+        KsCall call{X, Y, B, layout, s, bias};
         if (fusion_ok(hs, L, call)) return run_fused(hs, L, call);
     }
     int64_t maxdim = 0;
@@ -242,7 +242,7 @@ ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, in
     const float* in = X;
     for (int l = L - 1; l >= 0 && st == KS_OK; --l) {
         float* out = (l == 0) ? Y : static_cast<float*>(buf[(L - 1 - l) % nbuf]);
-        st = run_one(*hs[l], in, out, B, layout, s);
+        st = run_one(*hs[l], in, out, B, layout, s, l == 0 ? bias : nullptr);   // bias after the last hop
         in = out;
     }
     for (int i = 0; i < nbuf; ++i) cudaFreeAsync(buf[i], s);
@@ -368,7 +368,13 @@ ks_status_t ks_plan(ks_handle_t h, int64_t B, ks_layout_t layout, ks_kernel_t* o
 
 ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B, ks_layout_t layout,
                       ks_stream_t stream) {
+    return ks_matmul_bias(h, X, Y, nullptr, B, layout, stream);
+}
+
+ks_status_t ks_matmul_bias(ks_handle_t h, const float* X, float* Y, const float* bias, int64_t B,
+                           ks_layout_t layout, ks_stream_t stream) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (reinterpret_cast<uintptr_t>(bias) & 3) return fail(KS_ERR_ALIGNMENT, "bias must be 4-byte aligned");
     if (B < 0) return fail(KS_ERR_INVALID_ARG, "B must be >= 0");
     if (layout != KS_LAYOUT_BSF && layout != KS_LAYOUT_BSL) return fail(KS_ERR_INVALID_ARG, "bad layout %d", (int)layout);
     ks_status_t s = check_device(h);
@@ -380,20 +386,26 @@ ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B, ks_lay
     int64_t xb, yb;
     if (!mul_ok(B, h->N * 4, &xb) || !mul_ok(B, h->M * 4, &yb)) return fail(KS_ERR_INVALID_ARG, "B too large");
     if (overlap(X, xb, Y, yb)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
-    s = run_one(*h, X, Y, B, layout, static_cast<cudaStream_t>(stream));
+    s = run_one(*h, X, Y, B, layout, static_cast<cudaStream_t>(stream), bias);
     return s == KS_OK ? ok() : s;
 }
 
 ks_status_t ks_chain_ex(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
                         ks_layout_t layout, ks_stream_t stream) {
+    return ks_chain_bias(hs, L, X, Y, nullptr, B, layout, stream);
+}
+
+ks_status_t ks_chain_bias(const ks_handle_t* hs, int L, const float* X, float* Y, const float* bias,
+                          int64_t B, ks_layout_t layout, ks_stream_t stream) {
     ks_status_t s = validate_chain(hs, L, B, (int)layout);
     if (s != KS_OK) return s;
+    if (reinterpret_cast<uintptr_t>(bias) & 3) return fail(KS_ERR_ALIGNMENT, "bias must be 4-byte aligned");
     if (B == 0) return ok();
     if (!X || !Y) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
     if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 3)
         return fail(KS_ERR_ALIGNMENT, "X and Y must be 4-byte aligned");
     if (overlap(X, B * hs[L - 1]->N * 4, Y, B * hs[0]->M * 4)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
-    s = run_chain(hs, L, X, Y, B, (int)layout, static_cast<cudaStream_t>(stream));
+    s = run_chain(hs, L, X, Y, B, (int)layout, static_cast<cudaStream_t>(stream), bias);
     return s == KS_OK ? ok() : s;
 }
 

@@ -16,8 +16,6 @@
 //   weights are warp-uniform scalars, every row load/store is a fully
 //   coalesced V-wide vector along the batch.
 // Reduction order: l ascending with FP32 FMA, identical in both layouts.
-#include <cstdlib>
-
 #include "ks_internal.h"
 
 namespace {
@@ -49,11 +47,20 @@ __device__ __forceinline__ float4 vfmas(float4 x, float k, float4 acc) {
 }
 __device__ __forceinline__ float vfmas(float x, float k, float acc) { return fmaf(x, k, acc); }
 
+__device__ __forceinline__ float vadd(float a, float b) { return a + b; }
+__device__ __forceinline__ float2 vadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float vadds(float a, float s) { return a + s; }
+__device__ __forceinline__ float2 vadds(float2 a, float s) { return make_float2(a.x + s, a.y + s); }
+__device__ __forceinline__ float4 vadds(float4 a, float s) { return make_float4(a.x + s, a.y + s, a.z + s, a.w + s); }
+
 // ---------------------------------------------------------------- BSF ------
 template <int BB, int CC, int V, int RT>
 __global__ void __launch_bounds__(256) ks_stream_bsf(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
-    int64_t B, int a, int d) {
+    const float* __restrict__ bias, int64_t B, int a, int d) {
     using T = typename Vec<V>::T;
     const int dv = d / V;
     const int64_t P = (int64_t)a * dv;                 // items per batch row
@@ -73,6 +80,11 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
         for (int l = 0; l < CC; ++l)
             kr[k][l] = __ldg(reinterpret_cast<const T*>(K4 + ((int64_t)(i * BB + k) * CC + l) * d + j));
 
+    T br[BB];                                          // bias of row_{i,j}[k], j..j+V
+#pragma unroll
+    for (int k = 0; k < BB; ++k)
+        br[k] = bias ? __ldg(reinterpret_cast<const T*>(bias + (int64_t)i * BB * d + k * d + j)) : vzero<V>();
+
     const int64_t n0 = chunk * RT;
     const float* xb = X + n0 * N + (int64_t)i * CC * d + j;
     float* yb = Y + n0 * M + (int64_t)i * BB * d + j;
@@ -90,6 +102,7 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
             T acc = vzero<V>();
 #pragma unroll
             for (int l = 0; l < CC; ++l) acc = vfma(xr[r][l], kr[k][l], acc);
+            if (bias) acc = vadd(acc, br[k]);
             __stcs(reinterpret_cast<T*>(yb + r * M + k * d), acc);
         }
     }
@@ -99,7 +112,7 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
 template <int BB, int CC, int V, int RT>
 __global__ void __launch_bounds__(256) ks_stream_bsl(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
-    int64_t B, int a, int d, int64_t nblocks) {
+    const float* __restrict__ bias, int64_t B, int a, int d, int64_t nblocks) {
     using T = typename Vec<V>::T;
     const int64_t NV = B / V;
     const int64_t q = blockIdx.x / nblocks;          // q = i*d + j
@@ -134,42 +147,25 @@ __global__ void __launch_bounds__(256) ks_stream_bsl(
             T acc = vzero<V>();
 #pragma unroll
             for (int l = 0; l < CC; ++l) acc = vfmas(xr[r][l], kr[k][l], acc);
+            if (bias) acc = vadds(acc, __ldg(bias + (int64_t)i * BB * d + k * d + j));
             __stcs(reinterpret_cast<T*>(yb + k * rowx) + nv, acc);
         }
     }
 }
 
-// KS_STREAM_RT (experiments only): rows per thread for the BSF stream kernel.
-int stream_rt() {
-    static int v = [] {
-        const char* e = getenv("KS_STREAM_RT");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
-template <int BB, int CC, int V, int RT>
-cudaError_t launch_bsf_rt(const ks_handle_s& h, const KsCall& call) {
+// Rows per thread (BSF): measured on the FFT chain, RT = 2, 4, 8 reach the same
+// ~90% of copy bandwidth per factor; 8 keeps the fewest threads in flight.
+template <int BB, int CC, int V>
+cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
+    constexpr int RT = (BB * CC <= 4) ? 8 : 4;
     const int threads = 256;
     const int64_t P = h.a * (h.d / V);
     const int64_t items = P * ((call.B + RT - 1) / RT);
     const int64_t blocks = (items + threads - 1) / threads;
     ks_stream_bsf<BB, CC, V, RT><<<(unsigned)blocks, threads, 0, call.stream>>>(
-        call.X, h.k_canon, call.Y, call.B, (int)h.a, (int)h.d);
+        call.X, h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d);
     ks::count_launch();
     return cudaGetLastError();
-}
-
-template <int BB, int CC, int V>
-cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
-    if (BB * CC <= 4) {
-        const int rt = stream_rt();
-        if (rt == 2) return launch_bsf_rt<BB, CC, V, 2>(h, call);
-        if (rt == 4) return launch_bsf_rt<BB, CC, V, 4>(h, call);
-        if (rt == 16) return launch_bsf_rt<BB, CC, V, 16>(h, call);
-        return launch_bsf_rt<BB, CC, V, 8>(h, call);
-    }
-    return launch_bsf_rt<BB, CC, V, 4>(h, call);
 }
 
 template <int BB, int CC, int V>
@@ -181,14 +177,15 @@ cudaError_t launch_bsl(const ks_handle_s& h, const KsCall& call) {
     const int64_t nblocks = (NV + (int64_t)threads * RT - 1) / ((int64_t)threads * RT);
     const int64_t blocks = h.a * h.d * nblocks;
     ks_stream_bsl<BB, CC, V, RT><<<(unsigned)blocks, threads, 0, call.stream>>>(
-        call.X, h.k_canon, call.Y, call.B, (int)h.a, (int)h.d, nblocks);
+        call.X, h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d, nblocks);
     ks::count_launch();
     return cudaGetLastError();
 }
 
 int pick_vec(const ks_handle_s& h, const KsCall& call) {
     const int64_t span = call.layout == KS_LAYOUT_BSF ? h.d : call.B;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
+    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y) |
+                         (call.layout == KS_LAYOUT_BSF ? reinterpret_cast<uintptr_t>(call.bias) : 0);
     if (span % 4 == 0 && (al & 15) == 0) return 4;
     if (span % 2 == 0 && (al & 7) == 0) return 2;
     return 1;

@@ -187,7 +187,8 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
 template <int LAYOUT, int BN>
 __global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-               float* __restrict__ Y, int64_t B, int a, int b, int c, int d, int64_t ntiles, int dbg) {
+               float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+               int64_t ntiles, int dbg) {
     using C = Tf32Cfg<LAYOUT, BN>;
     constexpr int S = C::S;
     constexpr int P = C::P > 0 ? C::P : 1;      // (BSF: no staging; P only names unused barriers)
@@ -338,6 +339,11 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             for (int col = 0; col < BN; col += 16) {
                 float v[16];
                 tmem_ld16(tbase + col, v);
+                if (bias) {                       // KSLinear bias (NEXT-2), per output row r
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        v[e] += __ldg(bias + (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j);
+                }
                 if (n < B && !(dbg & 1)) {
                     if (LAYOUT == KS_LAYOUT_BSL) {
 #pragma unroll
@@ -423,7 +429,8 @@ __device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_
 template <int BN>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                    float* __restrict__ Y, int64_t B, int a, int b, int c, int d, int64_t ntiles) {
+                    float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c,
+                    int d, int64_t ntiles) {
     using C = Tf32JCfg<BN>;
     constexpr int S = C::S;
     constexpr int P = C::P;
@@ -574,11 +581,17 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
                 for (int jj = 0; jj < JJ; ++jj) tmem_ld16(tbase + jj * BN + col, v[jj]);
                 if (n < B) {
-                    float* yp = Y + n * M + (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+                    const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+                    float* yp = Y + n * M + r0;
 #pragma unroll
-                    for (int e = 0; e < 16; ++e)
-                        __stcs(reinterpret_cast<float4*>(yp + (int64_t)e * d),
-                               make_float4(v[0][e], v[1][e], v[2][e], v[3][e]));
+                    for (int e = 0; e < 16; ++e) {
+                        float4 o = make_float4(v[0][e], v[1][e], v[2][e], v[3][e]);
+                        if (bias) {               // KSLinear bias (NEXT-2)
+                            const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + r0 + (int64_t)e * d));
+                            o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+                        }
+                        __stcs(reinterpret_cast<float4*>(yp + (int64_t)e * d), o);
+                    }
                 }
             }
             tc_fence_before();
@@ -681,8 +694,8 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.B, (int)h.a, (int)h.b,
-                                                              (int)h.c, (int)h.d, ntiles, debug_flags());
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.bias, call.B, (int)h.a,
+                                                              (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags());
     ks::count_launch();
     return cudaGetLastError();
 }
@@ -720,8 +733,8 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.B, (int)h.a, (int)h.b,
-                                                              (int)h.c, (int)h.d, ntiles);
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.bias, call.B, (int)h.a,
+                                                              (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
     return cudaGetLastError();
 }
@@ -763,7 +776,8 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (xa & 15) return false;                                   // TMA global address
     if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0 && (ya & 3) == 0;
     if (ya & 15) return false;
-    return h.d == 1 || bsfj_ok(h);      // BSF: d = 1 direct; d % 4 == 0 four-j gather
+    // BSF: d = 1 direct; d % 4 == 0 four-j gather (its bias loads are 16-byte vectors)
+    return h.d == 1 || (bsfj_ok(h) && (reinterpret_cast<uintptr_t>(call.bias) & 15) == 0);
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {

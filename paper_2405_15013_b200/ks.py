@@ -26,7 +26,8 @@ STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_C
 
 # Every symbol include/ks.h declares (tests check the .so exports them all).
 EXPORTS = ["ks_pack_weights", "ks_free", "ks_get_pattern", "ks_set_math", "ks_set_kernel",
-           "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_set_chain_fusion",
+           "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_matmul_bias", "ks_chain_bias",
+           "ks_set_chain_fusion",
            "ks_chain_fusion_eligible", "ks_chain_host", "ks_read_packed",
            "ks_trace_enable", "ks_trace_read",
            "ks_last_error", "ks_last_error_message", "ks_status_string",
@@ -70,6 +71,10 @@ def load_library(path: str = LIB_PATH):
     lib.ks_chain.restype = st
     lib.ks_chain_ex.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, ctypes.c_int, vp]
     lib.ks_chain_ex.restype = st
+    lib.ks_matmul_bias.argtypes = [vp, fp, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_matmul_bias.restype = st
+    lib.ks_chain_bias.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_chain_bias.restype = st
     lib.ks_set_chain_fusion.argtypes = [ctypes.c_int]
     lib.ks_set_chain_fusion.restype = st
     lib.ks_chain_fusion_eligible.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int]
@@ -216,15 +221,20 @@ def _dev_ptr(t, what):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None):
-    """Y = X K^T through ks_matmul.  X: CUDA float32, (B, N) for BSF or (N, B) for BSL."""
+def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None, bias=None):
+    """Y = X K^T (+ bias) through ks_matmul / ks_matmul_bias.  X: CUDA float32,
+    (B, N) for BSF or (N, B) for BSL; bias: CUDA float32 (M,) or None."""
     import torch
     lay = _layout(layout)
     if B is None:
         B = X.shape[0] if lay == BSF else X.shape[1]
     if Y is None:
         Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=torch.float32)
-    _check(_lib.ks_matmul(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), int(B), lay, _stream_ptr(stream)))
+    if bias is None:
+        _check(_lib.ks_matmul(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), int(B), lay, _stream_ptr(stream)))
+    else:
+        _check(_lib.ks_matmul_bias(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), _dev_ptr(bias, "bias"), int(B),
+                                   lay, _stream_ptr(stream)))
     return Y
 
 
@@ -233,16 +243,21 @@ def _handles(factors):
     return arr
 
 
-def chain(factors, X, Y=None, layout="bsf", stream=None):
-    """Y = X K_L^T ... K_1^T through ks_chain_ex; factors in paper order K_1..K_L."""
+def chain(factors, X, Y=None, layout="bsf", stream=None, bias=None):
+    """Y = X K_L^T ... K_1^T (+ bias) through ks_chain_ex / ks_chain_bias; factors
+    in paper order K_1..K_L."""
     import torch
     lay = _layout(layout)
     B = X.shape[0] if lay == BSF else X.shape[1]
     M = factors[0].M
     if Y is None:
         Y = torch.empty((B, M) if lay == BSF else (M, B), device=X.device, dtype=torch.float32)
-    _check(_lib.ks_chain_ex(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"),
-                            int(B), lay, _stream_ptr(stream)))
+    if bias is None:
+        _check(_lib.ks_chain_ex(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"),
+                                int(B), lay, _stream_ptr(stream)))
+    else:
+        _check(_lib.ks_chain_bias(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"),
+                                  _dev_ptr(bias, "bias"), int(B), lay, _stream_ptr(stream)))
     return Y
 
 
