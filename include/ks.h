@@ -57,6 +57,14 @@ typedef enum { KS_LAYOUT_BSF = 0, KS_LAYOUT_BSL = 1 } ks_layout_t;
  * pack time; X: per kernel), products accumulated in FP32. */
 typedef enum { KS_MATH_FP32 = 0, KS_MATH_TF32 = 1 } ks_math_t;
 
+/* Storage / operand type of a handle and of the X, Y, bias it is used with.
+ * F32 handles follow ks_math_t.  BF16 / F16 handles (the
+ * paper's FP16 study PAPER.md:1597-1696) multiply on tcgen05 tensor cores
+ * (kind::f16) with FP32 accumulation and round the output to nearest-even;
+ * patterns the tensor-core kernel cannot take run a generic half kernel with
+ * FP32 accumulation.                                                         */
+typedef enum { KS_DTYPE_F32 = 0, KS_DTYPE_BF16 = 1, KS_DTYPE_F16 = 2 } ks_dtype_t;
+
 /* Kernel families; KS_KERNEL_AUTO lets the plan table choose (default).    */
 typedef enum {
     KS_KERNEL_AUTO = 0,
@@ -93,6 +101,14 @@ typedef enum {
  * device current at call time.  Returns NULL on error (see ks_last_error).
  * ------------------------------------------------------------------------- */
 ks_handle_t ks_pack_weights(int64_t a, int64_t b, int64_t c, int64_t d, const float* K);
+
+/* Same with an explicit element type: K holds a*b*c*d values of `dtype`
+ * (host or device).  A handle's dtype is fixed; use it with ks_matmul_any /
+ * ks_chain_any (ks_matmul / ks_chain / ks_chain_ex / ks_*_bias accept only
+ * F32 handles and return KS_ERR_INVALID_ARG otherwise).                     */
+ks_handle_t ks_pack_weights_ex(int64_t a, int64_t b, int64_t c, int64_t d, const void* K,
+                               ks_dtype_t dtype);
+ks_status_t ks_get_dtype(ks_handle_t h, ks_dtype_t* out);
 
 /* Release a handle (NULL is ignored).  Synchronises the handle's device. */
 void ks_free(ks_handle_t h);
@@ -150,6 +166,14 @@ ks_status_t ks_matmul_bias(ks_handle_t h, const float* X, float* Y, const float*
 ks_status_t ks_chain_bias(const ks_handle_t* handles, int L, const float* X, float* Y,
                           const float* bias, int64_t B, ks_layout_t layout, ks_stream_t stream);
 
+/* Type-generic forms: X, Y, bias (may be NULL) are device arrays of the
+ * handles' dtype (all handles of a chain must share it; intermediates use it
+ * too).  Semantics otherwise as ks_matmul_bias / ks_chain_bias.             */
+ks_status_t ks_matmul_any(ks_handle_t h, const void* X, void* Y, const void* bias, int64_t B,
+                          ks_layout_t layout, ks_stream_t stream);
+ks_status_t ks_chain_any(const ks_handle_t* handles, int L, const void* X, void* Y,
+                         const void* bias, int64_t B, ks_layout_t layout, ks_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * Chain fusion policy (process-wide, default on).  When on, ks_chain /
  * ks_chain_ex / ks_chain_host run an eligible chain -- BSF, 2 <= L <= 32,
@@ -177,7 +201,9 @@ ks_status_t ks_chain_host(const ks_handle_t* handles, int L, const float* X_host
 /* Copy one packed variant of K back to host (tests check the index maps
  * bit-exactly).  variant 0: canonical a*b*c*d;  1: tile-contiguous K^T,
  * [i*d+j][l][k] (a*d*c*b floats);  2: TF32-rounded tiles [i*d+j][k][l]
- * (a*d*b*c floats).  count must equal the variant's element count.         */
+ * (a*d*b*c floats).  count must equal the variant's element count.  Half
+ * handles copy elements of their dtype (2 bytes each): variant 0 canonical,
+ * 2 tensor-core tiles [i*d+j][k][l] (unrounded); variant 1 does not exist.  */
 ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst_host, int64_t count);
 
 /* ---------------------------------------------------------------------------

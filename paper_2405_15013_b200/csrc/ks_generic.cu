@@ -7,6 +7,9 @@
 // (Alg. 2 line 4), l ascending, FP32 FMA:
 //     Y(n, r) = sum_l X(n, i*c*d + l*d + j) * K4[i][k][l][j].
 // Every output is written exactly once (row sets partition [0,M)).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "ks_internal.h"
 
 namespace {
@@ -38,9 +41,67 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
     }
 }
 
+// Half-precision generic kernel: same reduction order, FP32 accumulation,
+// output rounded to nearest-even (half handles whose pattern the tensor-core
+// kernel cannot take).
+template <typename T, int LAYOUT>
+__global__ void __launch_bounds__(256) ks_generic_half_kernel(
+    const T* __restrict__ X, const T* __restrict__ K4, T* __restrict__ Y, const T* __restrict__ bias,
+    int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
+    const int64_t M = a * b * d, N = a * c * d;
+    const int64_t total = B * M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t n, r;
+        if (LAYOUT == KS_LAYOUT_BSF) { n = e / M; r = e - n * M; }
+        else                         { r = e / B; n = e - r * B; }
+        const int64_t i = r / (b * d);
+        const int64_t rem = r - i * b * d;
+        const int64_t k = rem / d;
+        const int64_t j = rem - k * d;
+        const int64_t s0 = i * c * d + j;
+        const T* kp = K4 + ((i * b + k) * c) * d + j;
+        float acc = 0.f;
+        for (int64_t l = 0; l < c; ++l) {
+            const int64_t s = s0 + l * d;
+            const float x = (float)(LAYOUT == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n]);
+            acc = fmaf(x, (float)kp[l * d], acc);
+        }
+        if (bias) acc += (float)bias[r];
+        Y[e] = T(acc);
+    }
+}
+
+template <typename T>
+cudaError_t launch_generic_half(const ks_handle_s& h, const KsCall& call) {
+    const int threads = 256;
+    const int64_t total = call.B * h.M;
+    int64_t blocks = (total + threads - 1) / threads;
+    const int64_t cap = (int64_t)ks::num_sms(h.device) * 8 * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const T* X = reinterpret_cast<const T*>(call.X);
+    T* Y = reinterpret_cast<T*>(call.Y);
+    const T* K = reinterpret_cast<const T*>(h.k_canon);
+    const T* bias = reinterpret_cast<const T*>(call.bias);
+    if (call.layout == KS_LAYOUT_BSF)
+        ks_generic_half_kernel<T, KS_LAYOUT_BSF><<<(unsigned)blocks, threads, 0, call.stream>>>(
+            X, K, Y, bias, call.B, h.a, h.b, h.c, h.d);
+    else
+        ks_generic_half_kernel<T, KS_LAYOUT_BSL><<<(unsigned)blocks, threads, 0, call.stream>>>(
+            X, K, Y, bias, call.B, h.a, h.b, h.c, h.d);
+    ks::count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 namespace ks {
+
+cudaError_t generic_half_launch(const ks_handle_s& h, const KsCall& call) {
+    return h.dtype == KS_DTYPE_BF16 ? launch_generic_half<__nv_bfloat16>(h, call)
+                                    : launch_generic_half<__half>(h, call);
+}
 
 bool generic_supports(const ks_handle_s&, const KsCall&) { return true; }
 

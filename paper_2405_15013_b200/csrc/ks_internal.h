@@ -16,6 +16,9 @@ struct ks_handle_s {
     float* k_tf32;        // [i*d+j][k][l]  TF32-rounded, K-major B operand
     ks_math_t math;
     ks_kernel_t forced;
+    int dtype = KS_DTYPE_F32;   // element type of K, X, Y (half handles: k_canon / k_tf32
+                                // hold half values, k_tile is unused)
+    int esize() const { return dtype == KS_DTYPE_F32 ? 4 : 2; }
 };
 
 struct KsCall {
@@ -49,6 +52,12 @@ cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call);
 
 bool tf32_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);
+
+// half precision handles (NEXT-3): tcgen05 kind::f16 kernel and a generic one
+bool half_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t half_launch(const ks_handle_s& h, const KsCall& call);
+cudaError_t generic_half_launch(const ks_handle_s& h, const KsCall& call);
+cudaError_t pack_half(const ks_handle_s& h, cudaStream_t s);
 
 // Fused multi-factor chain (ks_chain_fused.cu): one launch for a whole chain.
 bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call);

@@ -35,9 +35,36 @@ __global__ void pack_kernel(const float* __restrict__ k4, float* __restrict__ ti
     }
 }
 
+// Half handles: a pure permutation of the 16-bit values into [i*d+j][k][l]
+// (the tensor-core weight tiles); no rounding.
+__global__ void pack_half_kernel(const uint16_t* __restrict__ k4, uint16_t* __restrict__ mma, int64_t a,
+                                 int64_t b, int64_t c, int64_t d) {
+    const int64_t nnz = a * b * c * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e % d;
+        int64_t t = e / d;
+        const int64_t l = t % c;
+        t /= c;
+        const int64_t k = t % b;
+        const int64_t i = t / b;
+        mma[((i * d + j) * b + k) * c + l] = k4[e];
+    }
+}
+
 }  // namespace
 
 namespace ks {
+
+cudaError_t pack_half(const ks_handle_s& h, cudaStream_t s) {
+    const int threads = 256;
+    int64_t blocks = (h.nnz + threads - 1) / threads;
+    if (blocks > 65535 * 8) blocks = 65535 * 8;
+    pack_half_kernel<<<(unsigned)blocks, threads, 0, s>>>(reinterpret_cast<const uint16_t*>(h.k_canon),
+                                                          reinterpret_cast<uint16_t*>(h.k_tf32), h.a, h.b, h.c, h.d);
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t pack_tiles(const ks_handle_s& h, cudaStream_t s) {
     const int threads = 256;

@@ -106,6 +106,13 @@ bool overlap(const void* x, int64_t xbytes, const void* y, int64_t ybytes) {
 }
 
 ks_kernel_t choose(const ks_handle_s& h, const KsCall& call) {
+    if (h.dtype != KS_DTYPE_F32) {           // half handles: tensor cores, else generic
+        if (h.forced == KS_KERNEL_GENERIC) return KS_KERNEL_GENERIC;
+        const bool tc = ks::half_supports(h, call);
+        if (h.forced == KS_KERNEL_TF32) return tc ? KS_KERNEL_TF32 : KS_KERNEL_AUTO;
+        if (h.forced != KS_KERNEL_AUTO) return KS_KERNEL_AUTO;
+        return tc ? KS_KERNEL_TF32 : KS_KERNEL_GENERIC;
+    }
     if (h.forced != KS_KERNEL_AUTO) {
         switch (h.forced) {
             case KS_KERNEL_GENERIC: return ks::generic_supports(h, call) ? KS_KERNEL_GENERIC : KS_KERNEL_AUTO;
@@ -122,6 +129,11 @@ ks_kernel_t choose(const ks_handle_s& h, const KsCall& call) {
 }
 
 cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
+    if (h.dtype != KS_DTYPE_F32) {
+        if (k == KS_KERNEL_TF32) return ks::half_launch(h, call);
+        if (k == KS_KERNEL_GENERIC) return ks::generic_half_launch(h, call);
+        return cudaErrorInvalidValue;
+    }
     switch (k) {
         case KS_KERNEL_GENERIC: return ks::generic_launch(h, call);
         case KS_KERNEL_STREAM:  return ks::stream_launch(h, call);
@@ -146,7 +158,7 @@ ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, i
         std::lock_guard<std::mutex> lk(g_trace_mu);
         rec.start = trace_event();
         rec.stop = trace_event();
-        rec.bytes = 4.0 * ((double)B * (double)h.N + (double)h.nnz + (double)B * (double)h.M);
+        rec.bytes = h.esize() * ((double)B * (double)h.N + (double)h.nnz + (double)B * (double)h.M);
         cudaEventRecord(rec.start, s);
     }
     cudaError_t e = launch(k, h, call);
@@ -169,6 +181,7 @@ ks_status_t validate_chain(const ks_handle_t* hs, int L, int64_t B, int layout) 
         if (!hs[l]) return fail(KS_ERR_INVALID_ARG, "handles[%d] is NULL", l);
         ks_status_t s = check_device(hs[l]);
         if (s != KS_OK) return s;
+        if (hs[l]->dtype != hs[0]->dtype) return fail(KS_ERR_INVALID_ARG, "handles of a chain must share a dtype");
     }
     for (int l = 0; l + 1 < L; ++l)
         if (hs[l]->N != hs[l + 1]->M)
@@ -187,7 +200,8 @@ std::atomic<bool> g_fusion{true};
 bool fusion_ok(const ks_handle_t* hs, int L, const KsCall& call) {
     if (!g_fusion.load(std::memory_order_relaxed) || L < 2) return false;
     for (int l = 0; l < L; ++l)
-        if (hs[l]->forced != KS_KERNEL_AUTO || hs[l]->math != KS_MATH_FP32) return false;
+        if (hs[l]->forced != KS_KERNEL_AUTO || hs[l]->math != KS_MATH_FP32 || hs[l]->dtype != KS_DTYPE_F32)
+            return false;
     return ks::fused_chain_supports(hs, L, call);
 }
 
@@ -228,7 +242,7 @@ ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, in
     cudaMemPool_t pool;
     cudaError_t e = get_pool(hs[0]->device, &pool);
     if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
-    const size_t bytes = sizeof(float) * (size_t)(B * maxdim);
+    const size_t bytes = (size_t)hs[0]->esize() * (size_t)(B * maxdim);
     void* buf[2] = {nullptr, nullptr};
     const int nbuf = L >= 3 ? 2 : 1;
     for (int i = 0; i < nbuf; ++i) {
@@ -271,6 +285,14 @@ int num_sms(int device) {
 extern "C" {
 
 ks_handle_t ks_pack_weights(int64_t a, int64_t b, int64_t c, int64_t d, const float* K) {
+    return ks_pack_weights_ex(a, b, c, d, K, KS_DTYPE_F32);
+}
+
+ks_handle_t ks_pack_weights_ex(int64_t a, int64_t b, int64_t c, int64_t d, const void* K, ks_dtype_t dtype) {
+    if (dtype != KS_DTYPE_F32 && dtype != KS_DTYPE_BF16 && dtype != KS_DTYPE_F16) {
+        fail(KS_ERR_INVALID_ARG, "bad dtype %d", (int)dtype);
+        return nullptr;
+    }
     if (a < 1 || b < 1 || c < 1 || d < 1) {
         fail(KS_ERR_PATTERN, "pattern entries must be >= 1, got (%lld,%lld,%lld,%lld)",
              (long long)a, (long long)b, (long long)c, (long long)d);
@@ -299,16 +321,18 @@ ks_handle_t ks_pack_weights(int64_t a, int64_t b, int64_t c, int64_t d, const fl
     h->device = dev;
     h->math = KS_MATH_FP32;
     h->forced = KS_KERNEL_AUTO;
-    const size_t bytes = sizeof(float) * (size_t)nnz;
+    h->dtype = dtype;
+    const bool f32 = dtype == KS_DTYPE_F32;
+    const size_t bytes = (size_t)h->esize() * (size_t)nnz;
     if ((e = cudaMalloc(&h->k_canon, bytes)) != cudaSuccess ||
-        (e = cudaMalloc(&h->k_tile, bytes)) != cudaSuccess ||
+        (f32 && (e = cudaMalloc(&h->k_tile, bytes)) != cudaSuccess) ||
         (e = cudaMalloc(&h->k_tf32, bytes)) != cudaSuccess) {
         fail_cuda(e, "ks_pack_weights alloc");
         ks_free(h);
         return nullptr;
     }
     if ((e = cudaMemcpy(h->k_canon, K, bytes, cudaMemcpyDefault)) != cudaSuccess ||
-        (e = ks::pack_tiles(*h, 0)) != cudaSuccess ||
+        (e = f32 ? ks::pack_tiles(*h, 0) : ks::pack_half(*h, 0)) != cudaSuccess ||
         (e = cudaStreamSynchronize(0)) != cudaSuccess) {
         fail_cuda(e, "ks_pack_weights copy/pack");
         ks_free(h);
@@ -340,6 +364,8 @@ ks_status_t ks_get_pattern(ks_handle_t h, int64_t out[4]) {
 ks_status_t ks_set_math(ks_handle_t h, ks_math_t m) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
     if (m != KS_MATH_FP32 && m != KS_MATH_TF32) return fail(KS_ERR_INVALID_ARG, "bad math %d", (int)m);
+    if (m == KS_MATH_TF32 && h->dtype != KS_DTYPE_F32)
+        return fail(KS_ERR_UNSUPPORTED, "math applies to F32 handles (half handles use kind::f16)");
     if (m == KS_MATH_TF32 && (h->b < 16 || h->c < 16))
         return fail(KS_ERR_UNSUPPORTED, "TF32 needs b,c >= 16 (pattern has b=%lld c=%lld)",
                     (long long)h->b, (long long)h->c);
@@ -371,23 +397,32 @@ ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B, ks_lay
     return ks_matmul_bias(h, X, Y, nullptr, B, layout, stream);
 }
 
-ks_status_t ks_matmul_bias(ks_handle_t h, const float* X, float* Y, const float* bias, int64_t B,
-                           ks_layout_t layout, ks_stream_t stream) {
+ks_status_t ks_matmul_any(ks_handle_t h, const void* X, void* Y, const void* bias, int64_t B,
+                          ks_layout_t layout, ks_stream_t stream) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
-    if (reinterpret_cast<uintptr_t>(bias) & 3) return fail(KS_ERR_ALIGNMENT, "bias must be 4-byte aligned");
+    const uintptr_t amask = (uintptr_t)h->esize() - 1;
+    if (reinterpret_cast<uintptr_t>(bias) & amask) return fail(KS_ERR_ALIGNMENT, "bias must be element-aligned");
     if (B < 0) return fail(KS_ERR_INVALID_ARG, "B must be >= 0");
     if (layout != KS_LAYOUT_BSF && layout != KS_LAYOUT_BSL) return fail(KS_ERR_INVALID_ARG, "bad layout %d", (int)layout);
     ks_status_t s = check_device(h);
     if (s != KS_OK) return s;
     if (B == 0) return ok();
     if (!X || !Y) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
-    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 3)
-        return fail(KS_ERR_ALIGNMENT, "X and Y must be 4-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & amask)
+        return fail(KS_ERR_ALIGNMENT, "X and Y must be element-aligned");
     int64_t xb, yb;
-    if (!mul_ok(B, h->N * 4, &xb) || !mul_ok(B, h->M * 4, &yb)) return fail(KS_ERR_INVALID_ARG, "B too large");
+    if (!mul_ok(B, h->N * h->esize(), &xb) || !mul_ok(B, h->M * h->esize(), &yb))
+        return fail(KS_ERR_INVALID_ARG, "B too large");
     if (overlap(X, xb, Y, yb)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
-    s = run_one(*h, X, Y, B, layout, static_cast<cudaStream_t>(stream), bias);
+    s = run_one(*h, static_cast<const float*>(X), static_cast<float*>(Y), B, layout,
+                static_cast<cudaStream_t>(stream), static_cast<const float*>(bias));
     return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_matmul_bias(ks_handle_t h, const float* X, float* Y, const float* bias, int64_t B,
+                           ks_layout_t layout, ks_stream_t stream) {
+    if (h && h->dtype != KS_DTYPE_F32) return fail(KS_ERR_INVALID_ARG, "half handle: use ks_matmul_any");
+    return ks_matmul_any(h, X, Y, bias, B, layout, stream);
 }
 
 ks_status_t ks_chain_ex(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
@@ -395,18 +430,34 @@ ks_status_t ks_chain_ex(const ks_handle_t* hs, int L, const float* X, float* Y, 
     return ks_chain_bias(hs, L, X, Y, nullptr, B, layout, stream);
 }
 
-ks_status_t ks_chain_bias(const ks_handle_t* hs, int L, const float* X, float* Y, const float* bias,
-                          int64_t B, ks_layout_t layout, ks_stream_t stream) {
+ks_status_t ks_chain_any(const ks_handle_t* hs, int L, const void* X, void* Y, const void* bias,
+                         int64_t B, ks_layout_t layout, ks_stream_t stream) {
     ks_status_t s = validate_chain(hs, L, B, (int)layout);
     if (s != KS_OK) return s;
-    if (reinterpret_cast<uintptr_t>(bias) & 3) return fail(KS_ERR_ALIGNMENT, "bias must be 4-byte aligned");
+    const int es = hs[0]->esize();
+    const uintptr_t amask = (uintptr_t)es - 1;
+    if (reinterpret_cast<uintptr_t>(bias) & amask) return fail(KS_ERR_ALIGNMENT, "bias must be element-aligned");
     if (B == 0) return ok();
     if (!X || !Y) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
-    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 3)
-        return fail(KS_ERR_ALIGNMENT, "X and Y must be 4-byte aligned");
-    if (overlap(X, B * hs[L - 1]->N * 4, Y, B * hs[0]->M * 4)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
-    s = run_chain(hs, L, X, Y, B, (int)layout, static_cast<cudaStream_t>(stream), bias);
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & amask)
+        return fail(KS_ERR_ALIGNMENT, "X and Y must be element-aligned");
+    if (overlap(X, B * hs[L - 1]->N * es, Y, B * hs[0]->M * es)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
+    s = run_chain(hs, L, static_cast<const float*>(X), static_cast<float*>(Y), B, (int)layout,
+                  static_cast<cudaStream_t>(stream), static_cast<const float*>(bias));
     return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_chain_bias(const ks_handle_t* hs, int L, const float* X, float* Y, const float* bias,
+                          int64_t B, ks_layout_t layout, ks_stream_t stream) {
+    if (hs && L >= 1 && hs[0] && hs[0]->dtype != KS_DTYPE_F32)
+        return fail(KS_ERR_INVALID_ARG, "half handles: use ks_chain_any");
+    return ks_chain_any(hs, L, X, Y, bias, B, layout, stream);
+}
+
+ks_status_t ks_get_dtype(ks_handle_t h, ks_dtype_t* out) {
+    if (!h || !out) return fail(KS_ERR_INVALID_ARG, "NULL argument");
+    *out = (ks_dtype_t)h->dtype;
+    return ok();
 }
 
 ks_status_t ks_set_chain_fusion(int enable) {
@@ -438,8 +489,8 @@ ks_status_t ks_chain_host(const ks_handle_t* hs, int L, const float* Xh, float* 
     cudaMemPool_t pool;
     cudaError_t e = get_pool(hs[0]->device, &pool);
     if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
-    const size_t xbytes = sizeof(float) * (size_t)(B * hs[L - 1]->N);
-    const size_t ybytes = sizeof(float) * (size_t)(B * hs[0]->M);
+    const size_t xbytes = (size_t)hs[0]->esize() * (size_t)(B * hs[L - 1]->N);
+    const size_t ybytes = (size_t)hs[0]->esize() * (size_t)(B * hs[0]->M);
     void *dX = nullptr, *dY = nullptr;
     if ((e = cudaMallocFromPoolAsync(&dX, xbytes, pool, st)) != cudaSuccess) return fail_cuda(e, "staging X");
     if ((e = cudaMallocFromPoolAsync(&dY, ybytes, pool, st)) != cudaSuccess) {
@@ -462,7 +513,7 @@ ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst, int64_t count
     if (count != h->nnz) return fail(KS_ERR_INVALID_ARG, "count must be a*b*c*d = %lld", (long long)h->nnz);
     const float* src = variant == 0 ? h->k_canon : variant == 1 ? h->k_tile : variant == 2 ? h->k_tf32 : nullptr;
     if (!src) return fail(KS_ERR_INVALID_ARG, "variant must be 0, 1 or 2");
-    cudaError_t e = cudaMemcpy(dst, src, sizeof(float) * (size_t)count, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(dst, src, (size_t)h->esize() * (size_t)count, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail_cuda(e, "ks_read_packed");
     return ok();
 }

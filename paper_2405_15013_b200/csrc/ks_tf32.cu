@@ -33,6 +33,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 
 #include "ks_internal.h"
@@ -184,12 +187,53 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-template <int LAYOUT, int BN>
+// Element type T: float (kind::tf32, the TF32 path) or __nv_bfloat16 / __half
+// (kind::f16, the half-precision path, NEXT-3).  A 128-byte operand row holds
+// BK = 128 / sizeof(T) elements; one MMA consumes 32 bytes of K (KSTEP elements).
+template <typename T> struct ElemTraits;
+template <> struct ElemTraits<float> {
+    static constexpr uint32_t fmt = 2;  // TF32
+    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    __device__ static float to_f(float v) { return v; }
+    __device__ static float from_f(float v) { return v; }
+};
+template <> struct ElemTraits<__nv_bfloat16> {
+    static constexpr uint32_t fmt = 1;  // BF16
+    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    __device__ static float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+    __device__ static __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+};
+template <> struct ElemTraits<__half> {
+    static constexpr uint32_t fmt = 0;  // F16
+    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    __device__ static float to_f(__half v) { return __half2float(v); }
+    __device__ static __half from_f(float v) { return __float2half_rn(v); }
+};
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+template <typename T>
+__host__ __device__ constexpr uint32_t make_idesc_t(int n) {
+    return (1u << 4) | (ElemTraits<T>::fmt << 7) | (ElemTraits<T>::fmt << 10) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(BM >> 4) << 24);
+}
+
+template <int LAYOUT, int BN, typename T = float>
 __global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-               float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+               T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
                int64_t ntiles, int dbg) {
     using C = Tf32Cfg<LAYOUT, BN>;
+    constexpr int BKC = 128 / (int)sizeof(T);        // K elements per stage (one 128-byte row)
+    constexpr int KSTEP = 32 / (int)sizeof(T);       // K elements per MMA
     constexpr int S = C::S;
     constexpr int P = C::P > 0 ? C::P : 1;      // (BSF: no staging; P only names unused barriers)
     extern __shared__ uint8_t smem_raw[];
@@ -280,18 +324,31 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             for (int64_t g = 0; g < G; ++g) {
                 const int p = (int)(g % P);
                 mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
-                float v[BKC];
-                const uint32_t src = stg0 + p * STG_BYTES + 4 * r;
+                // column r of the staged [BKC l][128 n] chunk, as 32-bit words
+                uint32_t w[32];
+                const uint32_t src = stg0 + p * STG_BYTES + (uint32_t)sizeof(T) * r;
+                if constexpr (sizeof(T) == 4) {
 #pragma unroll
-                for (int l = 0; l < BKC; ++l) v[l] = (dbg & 2) ? 0.f : lds32(src + l * (BM * 4));
+                    for (int l = 0; l < 32; ++l)
+                        w[l] = (dbg & 2) ? 0u : __float_as_uint(lds32(src + l * (BM * 4)));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {       // pack l = 2q, 2q+1 (little endian)
+                        uint16_t lo, hi;
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(lo) : "r"(src + (2 * q) * (BM * 2)));
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hi) : "r"(src + (2 * q + 1) * (BM * 2)));
+                        w[q] = (uint32_t)lo | ((uint32_t)hi << 16);
+                    }
+                }
                 fence_proxy_async();      // generic reads before the TMA (async proxy) refill
                 mbar_arrive(sempty0 + 8 * p);
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
                 const uint32_t dst = slot0 + st * C::SLOT + rowoff;
 #pragma unroll
-                for (int l4 = 0; l4 < BKC / 4; ++l4)
-                    sts128(dst + ((l4 ^ (r % 8)) * 16), v[4 * l4], v[4 * l4 + 1], v[4 * l4 + 2], v[4 * l4 + 3]);
+                for (int ch = 0; ch < 8; ++ch)
+                    sts128(dst + ((ch ^ (r % 8)) * 16), __uint_as_float(w[4 * ch]), __uint_as_float(w[4 * ch + 1]),
+                           __uint_as_float(w[4 * ch + 2]), __uint_as_float(w[4 * ch + 3]));
                 fence_proxy_async();
                 mbar_arrive(full0 + 8 * st);
             }
@@ -299,7 +356,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     } else if (warp == 5) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(BN);
+            constexpr uint32_t idesc = make_idesc_t<T>(BN);
             int64_t g = 0;
             int64_t it = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -313,10 +370,15 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     tc_fence_after();
                     const uint32_t sa = slot0 + st * C::SLOT;
                     const uint32_t sb = sa + A_BYTES;
-                    const int ksteps = min(BKC / 8, (c - t * BKC) / 8);
-                    for (int s = 0; s < ksteps; ++s)
-                        mma_tf32(dtm, sw128_desc(sa + 32 * s), sw128_desc(sb + 32 * s), idesc,
-                                 (t > 0 || s > 0) ? 1u : 0u);
+                    const int ksteps = min(BKC / KSTEP, (c - t * BKC) / KSTEP);
+                    for (int s = 0; s < ksteps; ++s) {
+                        if constexpr (sizeof(T) == 4)
+                            mma_tf32(dtm, sw128_desc(sa + 32 * s), sw128_desc(sb + 32 * s), idesc,
+                                     (t > 0 || s > 0) ? 1u : 0u);
+                        else
+                            mma_f16(dtm, sw128_desc(sa + 32 * s), sw128_desc(sb + 32 * s), idesc,
+                                    (t > 0 || s > 0) ? 1u : 0u);
+                    }
                     mma_commit(empty0 + 8 * st);
                 }
                 mma_commit(accf0 + 8 * ab);
@@ -342,20 +404,33 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 if (bias) {                       // KSLinear bias (NEXT-2), per output row r
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
-                        v[e] += __ldg(bias + (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j);
+                        v[e] += ElemTraits<T>::to_f(bias[(int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j]);
                 }
                 if (n < B && !(dbg & 1)) {
                     if (LAYOUT == KS_LAYOUT_BSL) {
 #pragma unroll
                         for (int e = 0; e < 16; ++e) {
                             const int64_t r = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j;
-                            __stcs(Y + r * B + n, v[e]);
+                            if constexpr (sizeof(T) == 4) __stcs(Y + r * B + n, v[e]);
+                            else Y[r * B + n] = ElemTraits<T>::from_f(v[e]);
                         }
                     } else {
-                        float* yp = Y + n * M + (int64_t)tc.i * b + tc.k0 + col;
+                        T* yp = Y + n * M + (int64_t)tc.i * b + tc.k0 + col;
+                        if constexpr (sizeof(T) == 4) {
 #pragma unroll
-                        for (int e = 0; e < 16; e += 4)
-                            __stcs(reinterpret_cast<float4*>(yp + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+                            for (int e = 0; e < 16; e += 4)
+                                __stcs(reinterpret_cast<float4*>(yp + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+                        } else {
+                            uint32_t pk[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const T lo = ElemTraits<T>::from_f(v[2 * e]), hi = ElemTraits<T>::from_f(v[2 * e + 1]);
+                                pk[e] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
+                                        ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
+                            }
+                            __stcs(reinterpret_cast<uint4*>(yp), make_uint4(pk[0], pk[1], pk[2], pk[3]));
+                            __stcs(reinterpret_cast<uint4*>(yp) + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+                        }
                     }
                 }
             }
@@ -622,11 +697,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-            const cuuint32_t* box, CUtensorMapSwizzle sw) {
+            const cuuint32_t* box, CUtensorMapSwizzle sw,
+            CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), dims,
+    CUresult r = fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims,
                     strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -662,28 +738,31 @@ int pick_bn(int64_t b) {
     return 0;
 }
 
-template <int LAYOUT, int BN>
+template <int LAYOUT, int BN, typename T = float>
 cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     using C = Tf32Cfg<LAYOUT, BN>;
+    constexpr cuuint32_t BK = 128 / sizeof(T);
+    constexpr cuuint64_t ES = sizeof(T);
+    const CUtensorMapDataType dt = ElemTraits<T>::tma;
     CUtensorMap xmap, kmap;
     {
         const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
-        const cuuint64_t ks[1] = {(cuuint64_t)h.c * 4};
-        const cuuint32_t kb[2] = {BKC, BN};
-        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+        const cuuint64_t ks[1] = {(cuuint64_t)h.c * ES};
+        const cuuint32_t kb[2] = {BK, BN};
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return cudaErrorInvalidValue;
     }
     if (LAYOUT == KS_LAYOUT_BSL) {
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
-        const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
-        const cuuint32_t xb[3] = {BM, 1, BKC};
-        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+        const cuuint64_t xs[2] = {(cuuint64_t)call.B * ES, (cuuint64_t)(h.d * call.B) * ES};
+        const cuuint32_t xb[3] = {BM, 1, BK};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
     } else {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
-        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
-        const cuuint32_t xb[2] = {BKC, BM};
-        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * ES};
+        const cuuint32_t xb[2] = {BK, BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_kernel<LAYOUT, BN>;
+    auto kern = ks_tf32_kernel<LAYOUT, BN, T>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -694,7 +773,8 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.bias, call.B, (int)h.a,
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, reinterpret_cast<T*>(call.Y),
+                                                              reinterpret_cast<const T*>(call.bias), call.B, (int)h.a,
                                                               (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags());
     ks::count_launch();
     return cudaGetLastError();
@@ -741,25 +821,17 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
 
 bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % BKJ == 0 && pick_bn_j(h.b) != 0; }
 
-template <int LAYOUT>
+template <int LAYOUT, typename T = float>
 cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn(h.b)) {
-        case 256: return launch_bn<LAYOUT, 256>(h, call);
-        case 240: return launch_bn<LAYOUT, 240>(h, call);
-        case 224: return launch_bn<LAYOUT, 224>(h, call);
-        case 208: return launch_bn<LAYOUT, 208>(h, call);
-        case 192: return launch_bn<LAYOUT, 192>(h, call);
-        case 176: return launch_bn<LAYOUT, 176>(h, call);
-        case 160: return launch_bn<LAYOUT, 160>(h, call);
-        case 144: return launch_bn<LAYOUT, 144>(h, call);
-        case 128: return launch_bn<LAYOUT, 128>(h, call);
-        case 112: return launch_bn<LAYOUT, 112>(h, call);
-        case 96: return launch_bn<LAYOUT, 96>(h, call);
-        case 80: return launch_bn<LAYOUT, 80>(h, call);
-        case 64: return launch_bn<LAYOUT, 64>(h, call);
-        case 48: return launch_bn<LAYOUT, 48>(h, call);
-        case 32: return launch_bn<LAYOUT, 32>(h, call);
-        case 16: return launch_bn<LAYOUT, 16>(h, call);
+        case 128: return launch_bn<LAYOUT, 128, T>(h, call);
+        case 112: return launch_bn<LAYOUT, 112, T>(h, call);
+        case 96: return launch_bn<LAYOUT, 96, T>(h, call);
+        case 80: return launch_bn<LAYOUT, 80, T>(h, call);
+        case 64: return launch_bn<LAYOUT, 64, T>(h, call);
+        case 48: return launch_bn<LAYOUT, 48, T>(h, call);
+        case 32: return launch_bn<LAYOUT, 32, T>(h, call);
+        case 16: return launch_bn<LAYOUT, 16, T>(h, call);
     }
     return cudaErrorInvalidValue;
 }
@@ -790,6 +862,27 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
         case 16: return launch_bsfj<16>(h, call);
     }
     return cudaErrorInvalidValue;
+}
+
+// ---- half precision (NEXT-3): the same warp-specialised tcgen05 kernel with
+// kind::f16 (BF16 or FP16 operands, FP32 accumulation, output rounded to
+// nearest-even).  BSL any d; BSF d = 1.
+bool half_supports(const ks_handle_s& h, const KsCall& call) {
+    if (h.b < 16 || h.c < 16 || h.c % 16 != 0 || pick_bn(h.b) == 0) return false;
+    if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31)) return false;
+    if (call.B >= (int64_t(1) << 31)) return false;
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(call.X), ya = reinterpret_cast<uintptr_t>(call.Y);
+    if (xa & 15) return false;
+    if (call.layout == KS_LAYOUT_BSL) return call.B % 8 == 0 && (ya & 1) == 0;
+    return h.d == 1 && (ya & 15) == 0;
+}
+
+cudaError_t half_launch(const ks_handle_s& h, const KsCall& call) {
+    if (h.dtype == KS_DTYPE_BF16)
+        return call.layout == KS_LAYOUT_BSL ? launch_layout<KS_LAYOUT_BSL, __nv_bfloat16>(h, call)
+                                            : launch_layout<KS_LAYOUT_BSF, __nv_bfloat16>(h, call);
+    return call.layout == KS_LAYOUT_BSL ? launch_layout<KS_LAYOUT_BSL, __half>(h, call)
+                                        : launch_layout<KS_LAYOUT_BSF, __half>(h, call);
 }
 
 }  // namespace ks

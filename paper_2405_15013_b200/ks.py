@@ -25,7 +25,10 @@ STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_C
           8: "KS_ERR_CUDA"}
 
 # Every symbol include/ks.h declares (tests check the .so exports them all).
-EXPORTS = ["ks_pack_weights", "ks_free", "ks_get_pattern", "ks_set_math", "ks_set_kernel",
+DTYPE_F32, DTYPE_BF16, DTYPE_F16 = 0, 1, 2
+
+EXPORTS = ["ks_pack_weights", "ks_pack_weights_ex", "ks_get_dtype", "ks_matmul_any", "ks_chain_any",
+           "ks_free", "ks_get_pattern", "ks_set_math", "ks_set_kernel",
            "ks_plan", "ks_matmul", "ks_chain", "ks_chain_ex", "ks_matmul_bias", "ks_chain_bias",
            "ks_set_chain_fusion",
            "ks_chain_fusion_eligible", "ks_chain_host", "ks_read_packed",
@@ -55,6 +58,14 @@ def load_library(path: str = LIB_PATH):
     st = ctypes.c_int
     lib.ks_pack_weights.argtypes = [i64, i64, i64, i64, fp]
     lib.ks_pack_weights.restype = vp
+    lib.ks_pack_weights_ex.argtypes = [i64, i64, i64, i64, fp, ctypes.c_int]
+    lib.ks_pack_weights_ex.restype = vp
+    lib.ks_get_dtype.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+    lib.ks_get_dtype.restype = st
+    lib.ks_matmul_any.argtypes = [vp, fp, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_matmul_any.restype = st
+    lib.ks_chain_any.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, fp, i64, ctypes.c_int, vp]
+    lib.ks_chain_any.restype = st
     lib.ks_free.argtypes = [vp]
     lib.ks_free.restype = None
     lib.ks_get_pattern.argtypes = [vp, ctypes.POINTER(i64)]
@@ -162,14 +173,18 @@ class Factor:
                 raise ValueError(f"K must have a*b*c*d = {self.nnz} values")
             ptr = arr.ctypes.data
             self._keep = arr
-        else:  # torch tensor (host or device)
+        self.dtype = DTYPE_F32
+        if not isinstance(K, np.ndarray):  # torch tensor (host or device)
             if K.numel() != self.nnz or not K.is_contiguous():
                 raise ValueError(f"K must be contiguous with a*b*c*d = {self.nnz} values")
             import torch
-            if K.dtype != torch.float32:
-                raise TypeError("K must be float32")
+            dt = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16, torch.float16: DTYPE_F16}.get(K.dtype)
+            if dt is None:
+                raise TypeError("K must be float32, bfloat16 or float16")
+            self.dtype = dt
             ptr = K.data_ptr()
-        h = lib.ks_pack_weights(a, b, c, d, ctypes.c_void_p(ptr))
+            self._keep = K
+        h = lib.ks_pack_weights_ex(a, b, c, d, ctypes.c_void_p(ptr), self.dtype)
         if not h:
             _check(lib.ks_last_error())
         self._h = ctypes.c_void_p(h)
@@ -197,7 +212,7 @@ class Factor:
         return tuple(out)
 
     def read_packed(self, variant: int) -> np.ndarray:
-        out = np.empty(self.nnz, dtype=np.float32)
+        out = np.empty(self.nnz, dtype=np.float32 if self.dtype == DTYPE_F32 else np.uint16)
         _check(_lib.ks_read_packed(self._h, int(variant), ctypes.c_void_p(out.ctypes.data), self.nnz))
         return out
 
@@ -229,8 +244,12 @@ def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None
     if B is None:
         B = X.shape[0] if lay == BSF else X.shape[1]
     if Y is None:
-        Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=torch.float32)
-    if bias is None:
+        Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=X.dtype)
+    if f.dtype != DTYPE_F32:
+        bp = _dev_ptr(bias, "bias") if bias is not None else None
+        _check(_lib.ks_matmul_any(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, int(B), lay,
+                                  _stream_ptr(stream)))
+    elif bias is None:
         _check(_lib.ks_matmul(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), int(B), lay, _stream_ptr(stream)))
     else:
         _check(_lib.ks_matmul_bias(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), _dev_ptr(bias, "bias"), int(B),
@@ -251,8 +270,12 @@ def chain(factors, X, Y=None, layout="bsf", stream=None, bias=None):
     B = X.shape[0] if lay == BSF else X.shape[1]
     M = factors[0].M
     if Y is None:
-        Y = torch.empty((B, M) if lay == BSF else (M, B), device=X.device, dtype=torch.float32)
-    if bias is None:
+        Y = torch.empty((B, M) if lay == BSF else (M, B), device=X.device, dtype=X.dtype)
+    if factors[0].dtype != DTYPE_F32:
+        bp = _dev_ptr(bias, "bias") if bias is not None else None
+        _check(_lib.ks_chain_any(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp,
+                                 int(B), lay, _stream_ptr(stream)))
+    elif bias is None:
         _check(_lib.ks_chain_ex(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"),
                                 int(B), lay, _stream_ptr(stream)))
     else:
