@@ -47,7 +47,6 @@ def _time(fn, flush, reps, warm=3):
 
 
 def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool = True):
-    import numpy as np
     import torch
 
     import ksgen
@@ -56,25 +55,27 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
     pats = patterns or ksgen.grid.sweep_patterns()
     B = ksgen.configs.SWEEP_BATCH
     torch.backends.cuda.matmul.allow_tf32 = (math == "tf32")
+    dt = {"bf16": torch.bfloat16, "f16": torch.float16}.get(math, torch.float32)
+    esize = 2 if dt != torch.float32 else 4
     props = torch.cuda.get_device_properties(dev)
     flush = torch.empty(2 * props.L2_cache_size, dtype=torch.uint8, device=dev)
     nmax = max(p[0] * p[2] * p[3] for p in pats)
     g = torch.Generator(device=dev)
     g.manual_seed(0)
-    Xfull = torch.randn((B, nmax), generator=g, device=dev, dtype=torch.float32)
+    Xfull = torch.randn((B, nmax), generator=g, device=dev, dtype=torch.float32).to(dt)
     rows = []
     for p in pats:
         a, b, c, d = p
         M, N = a * b * d, a * c * d
-        K4 = ksgen.k4_uniform(*p, seed=1000)
+        K4 = torch.from_numpy(ksgen.k4_uniform(*p, seed=1000)).to(dt)
         f = ksb.Factor(*p, K4)
         if math == "tf32":
             f.set_math(ksb.MATH_TF32)
-        Kb = torch.from_numpy(np.ascontiguousarray(K4.transpose(0, 3, 1, 2).reshape(a * d, b, c))).to(dev)
+        Kb = K4.permute(0, 3, 1, 2).reshape(a * d, b, c).contiguous().to(dev)
         rec = {"pattern": list(p)}
         for lay in ("bsf", "bsl"):
             X = Xfull[:, :N].contiguous() if lay == "bsf" else Xfull[:, :N].t().contiguous()
-            Y = torch.empty((B, M) if lay == "bsf" else (M, B), device=dev)
+            Y = torch.empty((B, M) if lay == "bsf" else (M, B), device=dev, dtype=dt)
             t_ks = _time(lambda: ksb.matmul(f, X, Y, layout=lay), flush, reps)
             bfn = bmm_bsf if lay == "bsf" else bmm_bsl
             t_bmm = _time(lambda: bfn(X, Kb, a, b, c, d), flush, reps)
@@ -82,9 +83,9 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
                 ref = bfn(X, Kb, a, b, c, d)
                 ksb.matmul(f, X, Y, layout=lay)
                 torch.cuda.synchronize()
-                err = float((Y - ref).abs().max() / ref.abs().max())
+                err = float((Y.float() - ref.float()).abs().max() / ref.float().abs().max())
                 rec[f"{lay}_err_vs_bmm"] = err
-            byts = 4 * (B * N + a * b * c * d + B * M)
+            byts = esize * (B * N + a * b * c * d + B * M)
             rec[f"{lay}_plan"] = f.plan(B, lay)
             rec[f"{lay}_ks_ms"] = round(t_ks, 5)
             rec[f"{lay}_bmm_ms"] = round(t_bmm, 5)

@@ -490,11 +490,11 @@ struct TileJ {
     int i, j0, k0, n0;
 };
 
-__device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_t nnb, int BN) {
+__device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_t nnb, int BN, int J = JJ) {
     TileJ t;
     t.k0 = (int)(tile % nkc) * BN;
     tile /= nkc;
-    t.j0 = (int)(tile % njg) * JJ;              // j-groups of one (i, n-block) run back to back
+    t.j0 = (int)(tile % njg) * J;               // j-groups of one (i, n-block) run back to back
     tile /= njg;
     t.n0 = (int)(tile % nnb) * BM;
     t.i = (int)(tile / nnb);
@@ -681,6 +681,279 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     }
 }
 
+// ==========================================================================
+// Half precision, BSF with d > 1 (NEXT-3).  J j-values per tile, chosen so the
+// X gather is a legal TMA box (inner extent a multiple of 16 bytes):
+//   J = d  (d <= 8 or d == 12): the J columns of all 16 l of a block are one
+//          contiguous run of 16*d halves of an X row -> 2-D box {16 d + 8, 128 n};
+//   J = 8  (d % 8 == 0):       3-D box {8 j, 17 l, 128 n} of X viewed [B][a c][d].
+// Either way a staged row n holds [16 l][J] halves plus 16 bytes of padding, so
+// its pitch 32 J + 16 is an odd number of 16-byte units and the transposers'
+// 16-byte reads of 8 consecutive rows hit 8 different bank groups.  Each
+// transposer thread unpacks its row into J K-major A rows of 16 halves (32 B,
+// SWIZZLE_32B); per stage the MMA warp runs one K = 16 kind::f16 step into each
+// of J accumulators (2 x J x BN <= 512 TMEM columns); the epilogue writes the J
+// contiguous outputs of each (n, k) as one vector when J is even.
+// ==========================================================================
+constexpr int BKH = 16;                        // l per stage (one UMMA k-step of 32 B)
+constexpr int AH_BYTES = BM * BKH * 2;         // 4 KB per j
+
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(256 >> 4) << 32;            // 8 rows x 32 B
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)6 << 61;                     // SWIZZLE_32B
+    return d;
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+template <int J, int BN>
+struct HalfJCfg {
+    static constexpr int PITCH = 32 * J + 16;             // staged row: [16 l][J] halves + 16 B
+    static constexpr int STG = BM * PITCH;
+    static constexpr int BJ_BYTES = BN * BKH * 2;         // per j, BN * 32 B
+    static constexpr int SLOT = J * (AH_BYTES + BJ_BYTES);
+    static constexpr int P = 2;
+    static constexpr int S_FIT = (212 * 1024 - P * STG) / SLOT;
+    static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
+    static constexpr int BAR_OFF = S * SLOT + P * STG;
+    static constexpr int SMEM = BAR_OFF + 256 + 1024;
+    static constexpr int TMEM_COLS = 2 * J * BN <= 256 ? 256 : 512;
+    static constexpr int EC = J > 4 ? 8 : 16;             // epilogue columns per TMEM load
+    static_assert(J * BN <= 256 && BN % 16 == 0, "J accumulators, double-buffered");
+    static_assert(S >= 2, "pipeline too shallow");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+template <typename T, int J, int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                    T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                    int64_t ntiles) {
+    using C = HalfJCfg<J, BN>;
+    constexpr int S = C::S;
+    constexpr int P = C::P;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    const uint32_t full0 = smem_u32(&bars[0]);
+    const uint32_t empty0 = smem_u32(&bars[S]);
+    const uint32_t accf0 = smem_u32(&bars[2 * S]);
+    const uint32_t acce0 = smem_u32(&bars[2 * S + 2]);
+    const uint32_t sfull0 = smem_u32(&bars[2 * S + 4]);
+    const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + P]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * P]);
+    const uint32_t slot0 = smem_u32(smem);        // S x [J A tiles (4 KB) | J B tiles (BN*32 B)]
+    const uint32_t stg0 = slot0 + S * C::SLOT;    // P x staging
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int nkc = b / BN;
+    const int njg = d / J;
+    const bool contig = (J == d);                 // 2-D box over X rows, else 3-D {8 j, 17 l, n}
+    const int64_t nnb = (B + BM - 1) / BM;
+    const int64_t M = (int64_t)a * b * d;
+    const int nk = c / BKH;                       // c % 16 == 0
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t G = my_tiles * nk;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1 + NTRANS);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(accf0 + 8 * s, 1);
+            mbar_init(acce0 + 8 * s, NEPI);
+        }
+        for (int p = 0; p < P; ++p) {
+            mbar_init(sfull0 + 8 * p, 1);
+            mbar_init(sempty0 + 8 * p, NTRANS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            auto issue_x = [&](int64_t gx) {
+                const TileJ tc = decode_j(blockIdx.x + (gx / nk) * gridDim.x, nkc, njg, nnb, BN, J);
+                const int l0 = (int)(gx % nk) * BKH;
+                const int p = (int)(gx % P);
+                if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
+                mbar_expect_tx(sfull0 + 8 * p, C::STG);
+                if (contig)
+                    tma_2d(stg0 + p * C::STG, &xmap, (tc.i * c + l0) * d, tc.n0, sfull0 + 8 * p);
+                else
+                    tma_3d(stg0 + p * C::STG, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
+            };
+            for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
+            for (int64_t g = 0; g < G; ++g) {
+                if (g + P - 1 < G) issue_x(g + P - 1);
+                const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
+                const int l0 = (int)(g % nk) * BKH;
+                const int st = (int)(g % S);
+                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                mbar_expect_tx(full0 + 8 * st, J * C::BJ_BYTES);
+                const uint32_t sb = slot0 + st * C::SLOT + J * AH_BYTES;
+                for (int jj = 0; jj < J; ++jj)
+                    tma_2d(sb + jj * C::BJ_BYTES, &kmap, l0, ((tc.i * d + tc.j0 + jj) * b) + tc.k0, full0 + 8 * st);
+            }
+        }
+    } else if (warp <= 4) {
+        // staging row r: [16 l][J] halves -> J K-major SW32 A rows of 16 halves
+        const int r = tid - 32;
+        const uint32_t rowoff = (uint32_t)((r / 8) * 256 + (r % 8) * 32);
+        const int sw = (r % 8) / 4;
+        for (int64_t g = 0; g < G; ++g) {
+            const int p = (int)(g % P);
+            mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
+            uint32_t w[8 * J];
+            const uint32_t src = stg0 + p * C::STG + r * C::PITCH;
+#pragma unroll
+            for (int q = 0; q < 2 * J; ++q)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w[4 * q]), "=r"(w[4 * q + 1]), "=r"(w[4 * q + 2]), "=r"(w[4 * q + 3])
+                             : "r"(src + q * 16));
+            fence_proxy_async();          // generic reads before the TMA (async proxy) refill
+            mbar_arrive(sempty0 + 8 * p);
+            const int st = (int)(g % S);
+            if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+            const uint32_t sa = slot0 + st * C::SLOT + rowoff;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) {
+                uint32_t o[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {         // halves l = 2q, 2q+1 of column jj
+                    const int e0 = (2 * q) * J + jj, e1 = (2 * q + 1) * J + jj;
+                    const uint32_t sel = (e0 & 1 ? 0x32u : 0x10u) | ((e1 & 1 ? 0x76u : 0x54u) << 8);
+                    o[q] = __byte_perm(w[e0 >> 1], w[e1 >> 1], sel);
+                }
+                sts128(sa + jj * AH_BYTES + ((0 ^ sw) * 16), __uint_as_float(o[0]), __uint_as_float(o[1]),
+                       __uint_as_float(o[2]), __uint_as_float(o[3]));
+                sts128(sa + jj * AH_BYTES + ((1 ^ sw) * 16), __uint_as_float(o[4]), __uint_as_float(o[5]),
+                       __uint_as_float(o[6]), __uint_as_float(o[7]));
+            }
+            fence_proxy_async();
+            mbar_arrive(full0 + 8 * st);
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc_t<T>(BN);
+            int64_t g = 0, it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int ab = (int)(it & 1);
+                if (it >= 2) mbar_wait(acce0 + 8 * ab, (uint32_t)(((it / 2) - 1) & 1));
+                tc_fence_after();
+                for (int t = 0; t < nk; ++t, ++g) {
+                    const int st = (int)(g % S);
+                    mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+                    tc_fence_after();
+                    const uint32_t sa = slot0 + st * C::SLOT;
+                    const uint32_t sb = sa + J * AH_BYTES;
+#pragma unroll
+                    for (int jj = 0; jj < J; ++jj)
+                        mma_f16(tmem + (uint32_t)((ab * J + jj) * BN), sw32_desc(sa + jj * AH_BYTES),
+                                sw32_desc(sb + jj * C::BJ_BYTES), idesc, t > 0 ? 1u : 0u);
+                    mma_commit(empty0 + 8 * st);
+                }
+                mma_commit(accf0 + 8 * ab);
+            }
+        }
+        __syncwarp();
+    } else {
+        constexpr int EC = C::EC;
+        const int lq = warp & 3;
+        const int row = lq * 32 + lane;
+        int64_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const TileJ tc = decode_j(tile, nkc, njg, nnb, BN, J);
+            const int ab = (int)(it & 1);
+            mbar_wait(accf0 + 8 * ab, (uint32_t)((it / 2) & 1));
+            tc_fence_after();
+            const int64_t n = (int64_t)tc.n0 + row;
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * J * BN);
+#pragma unroll 1
+            for (int col = 0; col < BN; col += EC) {
+                float v[J][EC];
+#pragma unroll
+                for (int jj = 0; jj < J; ++jj) {
+                    if constexpr (EC == 16) tmem_ld16(tbase + jj * BN + col, v[jj]);
+                    else tmem_ld8(tbase + jj * BN + col, v[jj]);
+                }
+                if (n < B) {
+                    const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+                    T* yp = Y + n * M + r0;
+#pragma unroll
+                    for (int e = 0; e < EC; ++e) {
+                        uint16_t o[J];
+#pragma unroll
+                        for (int jj = 0; jj < J; ++jj) {
+                            float x = v[jj][e];
+                            if (bias) x += ElemTraits<T>::to_f(bias[r0 + (int64_t)e * d + jj]);   // NEXT-2
+                            const T h = ElemTraits<T>::from_f(x);
+                            o[jj] = reinterpret_cast<const uint16_t&>(h);
+                        }
+                        T* dst = yp + (int64_t)e * d;
+                        if constexpr (J % 2 == 0) {
+                            uint32_t pk[J / 2];
+#pragma unroll
+                            for (int q = 0; q < J / 2; ++q) pk[q] = (uint32_t)o[2 * q] | ((uint32_t)o[2 * q + 1] << 16);
+                            if constexpr (J % 8 == 0) {
+#pragma unroll
+                                for (int q = 0; q < J / 8; ++q)
+                                    __stcs(reinterpret_cast<uint4*>(dst) + q,
+                                           make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
+                            } else if constexpr (J % 4 == 0) {
+#pragma unroll
+                                for (int q = 0; q < J / 4; ++q)
+                                    __stcs(reinterpret_cast<uint2*>(dst) + q, make_uint2(pk[2 * q], pk[2 * q + 1]));
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < J / 2; ++q) __stcs(reinterpret_cast<unsigned int*>(dst) + q, pk[q]);
+                            }
+                        } else {
+                            uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+#pragma unroll
+                            for (int jj = 0; jj < J; ++jj) d16[jj] = o[jj];
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(acce0 + 8 * ab);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+    }
+}
+
 // ------------------------------------------------------------------ host ------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -821,6 +1094,83 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
 
 bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % BKJ == 0 && pick_bn_j(h.b) != 0; }
 
+// Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
+int pick_j_half(int64_t d) {
+    if (d == 2 || d == 3 || d == 4 || d == 6 || d == 8 || d == 12) return (int)d;
+    return d % 8 == 0 ? 8 : 0;
+}
+int pick_bn_half(int64_t b, int J) {
+    for (int bn : {128, 96, 64, 48, 32, 16})
+        if (b % bn == 0 && J * bn <= 256) return bn;
+    return 0;
+}
+
+template <typename T, int J, int BN>
+cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
+    using C = HalfJCfg<J, BN>;
+    const CUtensorMapDataType dt = ElemTraits<T>::tma;
+    CUtensorMap xmap, kmap;
+    {
+        const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
+        const cuuint64_t ks[1] = {(cuuint64_t)h.c * 2};
+        const cuuint32_t kb[2] = {BKH, BN};
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_32B, dt)) return cudaErrorInvalidValue;
+    }
+    if (J == h.d) {
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 2};
+        const cuuint32_t xb[2] = {(cuuint32_t)(BKH * J + 8), BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
+    } else {
+        const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
+        const cuuint64_t xs[2] = {(cuuint64_t)h.d * 2, (cuuint64_t)h.N * 2};
+        const cuuint32_t xb[3] = {8, BKH + 1, BM};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_half_bsfj_kernel<T, J, BN>;
+    static bool attr[64] = {false};
+    if (!attr[h.device & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr[h.device & 63] = true;
+    }
+    const int64_t ntiles = (h.b / BN) * (h.d / J) * ((call.B + BM - 1) / BM) * h.a;
+    int64_t slots = (int64_t)ks::num_sms(h.device);
+    if (max_grid() > 0) slots = max_grid();
+    const int64_t grid = ntiles < slots ? ntiles : slots;
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, reinterpret_cast<T*>(call.Y),
+                                                              reinterpret_cast<const T*>(call.bias), call.B, (int)h.a,
+                                                              (int)h.b, (int)h.c, (int)h.d, ntiles);
+    ks::count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T, int J>
+cudaError_t launch_halfj_bn(const ks_handle_s& h, const KsCall& call) {
+    switch (pick_bn_half(h.b, J)) {
+        case 128: if constexpr (J * 128 <= 256) return launch_halfj<T, J, 128>(h, call); break;
+        case 96: if constexpr (J * 96 <= 256) return launch_halfj<T, J, 96>(h, call); break;
+        case 64: if constexpr (J * 64 <= 256) return launch_halfj<T, J, 64>(h, call); break;
+        case 48: if constexpr (J * 48 <= 256) return launch_halfj<T, J, 48>(h, call); break;
+        case 32: if constexpr (J * 32 <= 256) return launch_halfj<T, J, 32>(h, call); break;
+        case 16: return launch_halfj<T, J, 16>(h, call);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_halfj_any(const ks_handle_s& h, const KsCall& call) {
+    switch (pick_j_half(h.d)) {
+        case 2: return launch_halfj_bn<T, 2>(h, call);
+        case 3: return launch_halfj_bn<T, 3>(h, call);
+        case 4: return launch_halfj_bn<T, 4>(h, call);
+        case 6: return launch_halfj_bn<T, 6>(h, call);
+        case 8: return launch_halfj_bn<T, 8>(h, call);
+        case 12: return launch_halfj_bn<T, 12>(h, call);
+    }
+    return cudaErrorInvalidValue;
+}
+
 template <int LAYOUT, typename T = float>
 cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn(h.b)) {
@@ -874,15 +1224,20 @@ bool half_supports(const ks_handle_s& h, const KsCall& call) {
     const uintptr_t xa = reinterpret_cast<uintptr_t>(call.X), ya = reinterpret_cast<uintptr_t>(call.Y);
     if (xa & 15) return false;
     if (call.layout == KS_LAYOUT_BSL) return call.B % 8 == 0 && (ya & 1) == 0;
-    return h.d == 1 && (ya & 15) == 0;
+    if (ya & 15) return false;
+    if (h.d == 1) return true;
+    // BSF d > 1: J-column gather (bias read as scalars, any 2-byte alignment)
+    const int J = pick_j_half(h.d);
+    return J != 0 && pick_bn_half(h.b, J) != 0 && (J != h.d || (h.N * 2) % 16 == 0);
 }
 
 cudaError_t half_launch(const ks_handle_s& h, const KsCall& call) {
-    if (h.dtype == KS_DTYPE_BF16)
-        return call.layout == KS_LAYOUT_BSL ? launch_layout<KS_LAYOUT_BSL, __nv_bfloat16>(h, call)
-                                            : launch_layout<KS_LAYOUT_BSF, __nv_bfloat16>(h, call);
-    return call.layout == KS_LAYOUT_BSL ? launch_layout<KS_LAYOUT_BSL, __half>(h, call)
-                                        : launch_layout<KS_LAYOUT_BSF, __half>(h, call);
+    const bool bf = h.dtype == KS_DTYPE_BF16;
+    if (call.layout == KS_LAYOUT_BSL)
+        return bf ? launch_layout<KS_LAYOUT_BSL, __nv_bfloat16>(h, call) : launch_layout<KS_LAYOUT_BSL, __half>(h, call);
+    if (h.d == 1)
+        return bf ? launch_layout<KS_LAYOUT_BSF, __nv_bfloat16>(h, call) : launch_layout<KS_LAYOUT_BSF, __half>(h, call);
+    return bf ? launch_halfj_any<__nv_bfloat16>(h, call) : launch_halfj_any<__half>(h, call);
 }
 
 }  // namespace ks

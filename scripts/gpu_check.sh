@@ -18,8 +18,9 @@ if [[ $STAGES == *bench* ]]; then
   timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
 fi
 if [[ $STAGES == *sweep* ]]; then
-  timeout 900 python bench_sweep.py fp32 > gpurun_out/sweep_fp32.json 2> gpurun_out/sweep.err
-  timeout 900 python bench_sweep.py tf32 > gpurun_out/sweep_tf32.json 2> gpurun_out/sweep_tf32.err
+  for m in ${SWEEP_MODES:-fp32 tf32}; do
+    timeout 900 python bench_sweep.py $m > gpurun_out/sweep_$m.json 2> gpurun_out/sweep_$m.err
+  done
 fi
 if [[ $STAGES == *ncu* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \

@@ -33,4 +33,20 @@ for p, lay, B in [((1, 64, 64, 4), "bsf", 1024), ((1, 64, 64, 4), "bsl", 1024), 
         r = bad[0]
         badc = np.nonzero(np.abs(Yh[r] - ref[r]) > 5e-3 * np.abs(ref).max())[0]
         print("   row", r, "bad cols", len(badc), badc[:20])
+
+# half precision (kind::f16), incl. the BSF J-column gather: normwise <= 2 u_bf16
+for p, lay, B in [((1, 64, 64, 4), "bsf", 1024), ((2, 48, 48, 8), "bsf", 512), ((1, 32, 48, 16), "bsf", 700),
+                  ((1, 64, 64, 1), "bsf", 1024), ((2, 96, 96, 3), "bsl", 776)]:
+    M, N, _ = O.dims(p)
+    K4 = torch.from_numpy(ksgen.k4_uniform(*p, seed=3)).bfloat16()
+    X = torch.from_numpy(ksgen.x_normal(B, N, seed=4)).bfloat16()
+    f = ksb.Factor(*p, K4)
+    Xd = (X if lay == "bsf" else X.t().contiguous()).cuda()
+    Y = ksb.matmul(f, Xd, layout=lay).float().cpu().numpy()
+    Yh = Y if lay == "bsf" else Y.T
+    ref = O.matmul(p, K4.float().numpy(), X.float().numpy())
+    e = O.normwise_error(Yh, ref)
+    print(p, lay, B, "bf16 maxgrid", os.environ.get("KS_TF32_MAXGRID"), "err", e)
+    if e > 2 * 2.0 ** -8:
+        worst = 1.0
 sys.exit(0 if worst <= 5e-3 else 1)
