@@ -159,9 +159,12 @@ struct Tf32Cfg {
     static constexpr int CTAS = BN <= 128 ? 2 : 1;                                // CTAs per SM
     static constexpr int BUDGET = CTAS == 2 ? 110 * 1024 : 200 * 1024;
     static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 ? 3 : 2) : 3) : 0;   // staging
-    static constexpr int S_FIT = (BUDGET - P * STG_BYTES) / SLOT;
+    // BSF: 4 epilogue warps x 32 rows x (4 + 1) 16-byte units of store scratch (WarpStore<float, 1, 16>)
+    static constexpr int SCR = LAYOUT == KS_LAYOUT_BSL ? 0 : 4 * 32 * 5 * 16;
+    static constexpr int S_FIT = (BUDGET - P * STG_BYTES - SCR) / SLOT;
     static constexpr int S = S_FIT > 6 ? 6 : S_FIT;                              // operand slots
-    static constexpr int BAR_OFF = S * SLOT + P * STG_BYTES;
+    static constexpr int SCR_OFF = S * SLOT + P * STG_BYTES;
+    static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;                            // + barriers + align pad
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
@@ -210,6 +213,65 @@ template <> struct ElemTraits<__half> {
     __device__ static __half from_f(float v) { return __float2half_rn(v); }
 };
 
+// BSF epilogue store through a warp-private shared-memory scratch.  Lane l holds
+// row n0w + l of the tile: v[j][k] is the output at element offset
+// off0 + k*d + j of that row of Y (row pitch ldy).  Each row's KB x J values are
+// packed into 16-byte units (row-major [k][j], pitch UR + 1 units: an odd
+// number, so the per-row writes are bank-conflict-free) and read back so that
+// consecutive lanes store consecutive units: one coalesced STG.128 per lane per
+// pass instead of 32 rows' worth of sectors per store instruction.  A unit
+// never straddles a run of J outputs unless the runs are contiguous (J == d).
+template <typename T, int J, int KB>
+struct WarpStore {
+    static constexpr int EPU = 16 / (int)sizeof(T);           // elements per 16-byte unit
+    static constexpr int UR = KB * J / EPU;                     // units per row
+    static constexpr int PITCH = (UR + 1) * 16;
+    static constexpr int BYTES = 32 * PITCH;                    // per warp
+    static_assert((KB * J) % EPU == 0 && UR % 2 == 0, "whole units, odd pitch");
+};
+
+template <typename T, int J, int KB>
+__device__ __forceinline__ void warp_store_rows(uint32_t scr, const float (&v)[J][KB], T* __restrict__ Y,
+                                                int64_t n0w, int64_t B, int64_t ldy, int64_t off0, int d, int lane) {
+    using W = WarpStore<T, J, KB>;
+    constexpr int EPU = W::EPU, UR = W::UR;
+#pragma unroll
+    for (int q = 0; q < UR; ++q) {
+        uint32_t w[4];
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int e = q * 4 + x;
+                w[x] = __float_as_uint(v[e % J][e / J]);
+            }
+        } else {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int e0 = q * 8 + 2 * x, e1 = e0 + 1;
+                const T lo = ElemTraits<T>::from_f(v[e0 % J][e0 / J]), hi = ElemTraits<T>::from_f(v[e1 % J][e1 / J]);
+                w[x] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) | ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
+            }
+        }
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(scr + lane * W::PITCH + q * 16), "r"(w[0]),
+                     "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < UR; ++t) {
+        const int u = t * 32 + lane;
+        const int r = u / UR, q = u % UR;
+        uint32_t w[4];
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(scr + r * W::PITCH + q * 16) : "memory");
+        const int e0 = q * EPU;
+        const int64_t n = n0w + r;
+        if (n < B)
+            __stcs(reinterpret_cast<uint4*>(Y + n * ldy + off0 + (int64_t)(e0 / J) * d + (e0 % J)),
+                   make_uint4(w[0], w[1], w[2], w[3]));
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
     asm volatile(
@@ -250,6 +312,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * (P > 0 ? P : 1)]);
     const uint32_t slot0 = smem_u32(smem);                 // S x (A 16 KB | B BN*128 B), 1 KB aligned
     const uint32_t stg0 = slot0 + S * C::SLOT;             // P x 16 KB staging (BSL)
+    const uint32_t scr0 = slot0 + C::SCR_OFF;              // BSF epilogue store scratch
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -318,7 +381,50 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         }
     } else if (warp <= 4) {
         // ---------------- BSL transposers: staging [l][n] -> K-major SW128 A ----------------
-        if (LAYOUT == KS_LAYOUT_BSL) {
+        if constexpr (LAYOUT == KS_LAYOUT_BSL && sizeof(T) == 2) {
+            // Half: thread t owns the batch-row pair (2p, 2p+1) for l in [32h, 32h+32).
+            // One LDS.32 fetches both rows' values at one l (a warp reads 128
+            // contiguous bytes); PRMT pairs (l, l+1) per row; 4 STS.128 per row.
+            // Lanes with (p >> 2) odd write their odd row first, so the 8 lanes of
+            // a store phase hit 8 different rows mod 8 (conflict-free SW128).
+            const int t = tid - 32;
+            const int p = t & 63, hh = t >> 6;
+            const int s = (p >> 2) & 1;
+            const int rA = 2 * p + s, rB = 2 * p + 1 - s;
+            const uint32_t selA = s ? 0x7632u : 0x5410u, selB = s ? 0x5410u : 0x7632u;
+            const uint32_t offA = (uint32_t)((rA / 8) * 1024 + (rA % 8) * 128);
+            const uint32_t offB = (uint32_t)((rB / 8) * 1024 + (rB % 8) * 128);
+            for (int64_t g = 0; g < G; ++g) {
+                const int pp = (int)(g % P);
+                mbar_wait(sfull0 + 8 * pp, (uint32_t)((g / P) & 1));
+                uint32_t w[32];
+                const uint32_t src = stg0 + pp * STG_BYTES + (uint32_t)(hh * 32) * (BM * 2) + 4 * p;
+#pragma unroll
+                for (int l = 0; l < 32; ++l)
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[l]) : "r"(src + l * (BM * 2)));
+                fence_proxy_async();      // generic reads before the TMA (async proxy) refill
+                mbar_arrive(sempty0 + 8 * pp);
+                const int st = (int)(g % S);
+                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                uint32_t oa[16], ob[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    oa[q] = __byte_perm(w[2 * q], w[2 * q + 1], selA);
+                    ob[q] = __byte_perm(w[2 * q], w[2 * q + 1], selB);
+                }
+                const uint32_t base = slot0 + st * C::SLOT;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int ch = 4 * hh + k;
+                    sts128(base + offA + ((ch ^ (rA % 8)) * 16), __uint_as_float(oa[4 * k]), __uint_as_float(oa[4 * k + 1]),
+                           __uint_as_float(oa[4 * k + 2]), __uint_as_float(oa[4 * k + 3]));
+                    sts128(base + offB + ((ch ^ (rB % 8)) * 16), __uint_as_float(ob[4 * k]), __uint_as_float(ob[4 * k + 1]),
+                           __uint_as_float(ob[4 * k + 2]), __uint_as_float(ob[4 * k + 3]));
+                }
+                fence_proxy_async();
+                mbar_arrive(full0 + 8 * st);
+            }
+        } else if constexpr (LAYOUT == KS_LAYOUT_BSL) {
             const int r = tid - 32;                                    // batch row in the tile
             const uint32_t rowoff = (uint32_t)((r / 8) * 1024 + (r % 8) * 128);
             for (int64_t g = 0; g < G; ++g) {
@@ -326,20 +432,10 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
                 // column r of the staged [BKC l][128 n] chunk, as 32-bit words
                 uint32_t w[32];
-                const uint32_t src = stg0 + p * STG_BYTES + (uint32_t)sizeof(T) * r;
-                if constexpr (sizeof(T) == 4) {
+                const uint32_t src = stg0 + p * STG_BYTES + 4 * r;
 #pragma unroll
-                    for (int l = 0; l < 32; ++l)
-                        w[l] = (dbg & 2) ? 0u : __float_as_uint(lds32(src + l * (BM * 4)));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) {       // pack l = 2q, 2q+1 (little endian)
-                        uint16_t lo, hi;
-                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(lo) : "r"(src + (2 * q) * (BM * 2)));
-                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hi) : "r"(src + (2 * q + 1) * (BM * 2)));
-                        w[q] = (uint32_t)lo | ((uint32_t)hi << 16);
-                    }
-                }
+                for (int l = 0; l < 32; ++l)
+                    w[l] = (dbg & 2) ? 0u : __float_as_uint(lds32(src + l * (BM * 4)));
                 fence_proxy_async();      // generic reads before the TMA (async proxy) refill
                 mbar_arrive(sempty0 + 8 * p);
                 const int st = (int)(g % S);
@@ -399,38 +495,40 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * BN);
 #pragma unroll 1
             for (int col = 0; col < BN; col += 16) {
-                float v[16];
+                float vv[1][16];
+                float* v = vv[0];
                 tmem_ld16(tbase + col, v);
                 if (bias) {                       // KSLinear bias (NEXT-2), per output row r
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
                         v[e] += ElemTraits<T>::to_f(bias[(int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j]);
                 }
-                if (n < B && !(dbg & 1)) {
-                    if (LAYOUT == KS_LAYOUT_BSL) {
+                if constexpr (LAYOUT != KS_LAYOUT_BSL) {
+                    // BSF (d = 1): row n's 16 outputs are contiguous; coalesce through scratch
+                    if (!(dbg & 1))
+                        warp_store_rows<T, 1, 16>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, 1, 16>::BYTES, vv, Y,
+                                                  (int64_t)tc.n0 + lq * 32, B, M, (int64_t)tc.i * b + tc.k0 + col, 1, lane);
+                } else if constexpr (sizeof(T) == 2) {
+                    // lanes (n, n+1) swap halves so each stores one 32-bit pair:
+                    // the even lane (v_e(n), v_e(n+1)) in row r_e, the odd lane
+                    // (v_{e+1}(n-1), v_{e+1}(n)) in row r_{e+1} (B % 8 == 0: aligned,
+                    // and n, n+1 are both in or both out of range)
+                    const bool odd = lane & 1;
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            const int64_t r = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j;
-                            if constexpr (sizeof(T) == 4) __stcs(Y + r * B + n, v[e]);
-                            else Y[r * B + n] = ElemTraits<T>::from_f(v[e]);
-                        }
-                    } else {
-                        T* yp = Y + n * M + (int64_t)tc.i * b + tc.k0 + col;
-                        if constexpr (sizeof(T) == 4) {
+                    for (int e = 0; e < 16; e += 2) {
+                        const float x = __shfl_xor_sync(0xffffffffu, odd ? v[e] : v[e + 1], 1);
+                        const T lo = ElemTraits<T>::from_f(odd ? x : v[e]);
+                        const T hi = ElemTraits<T>::from_f(odd ? v[e + 1] : x);
+                        const uint32_t pk = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
+                                            ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
+                        const int64_t r = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e + (odd ? 1 : 0)) * d + tc.j;
+                        if (n < B && !(dbg & 1)) __stcs(reinterpret_cast<unsigned int*>(Y + r * B + (n & ~int64_t(1))), pk);
+                    }
+                } else if (n < B && !(dbg & 1)) {
 #pragma unroll
-                            for (int e = 0; e < 16; e += 4)
-                                __stcs(reinterpret_cast<float4*>(yp + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
-                        } else {
-                            uint32_t pk[8];
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const T lo = ElemTraits<T>::from_f(v[2 * e]), hi = ElemTraits<T>::from_f(v[2 * e + 1]);
-                                pk[e] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
-                                        ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
-                            }
-                            __stcs(reinterpret_cast<uint4*>(yp), make_uint4(pk[0], pk[1], pk[2], pk[3]));
-                            __stcs(reinterpret_cast<uint4*>(yp) + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]));
-                        }
+                    for (int e = 0; e < 16; ++e) {
+                        const int64_t r = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j;
+                        __stcs(Y + r * B + n, v[e]);
                     }
                 }
             }
@@ -453,8 +551,10 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 // of 4 KS blocks at once with full 16-byte vectors (SURVEY §7 hard part 1).
 // Transposer warps split the staged [n][l][j] chunk into four K-major
 // 64-byte-swizzled A tiles (one per j); the MMA warp runs 4 accumulators
-// (4 x BN <= 256 TMEM columns, double-buffered); the epilogue writes the 4 j
-// of each (n, k) as one float4.
+// (4 x BN <= 256 TMEM columns, double-buffered); the epilogue stores through
+// warp_store_rows (coalesced 16-byte units; measured on the half variant: the
+// direct per-row float4 stores touched 32 sectors per instruction, 4x ideal,
+// and made the epilogue the bottleneck).
 // ==========================================================================
 constexpr int BKJ = 16;                       // l per stage (2 UMMA k-steps)
 constexpr int JJ = 4;
@@ -477,10 +577,13 @@ struct Tf32JCfg {
     static constexpr int B_BYTES = BN * BKJ * 4;          // per j, BN * 64 B
     static constexpr int SLOT = JJ * (AJ_BYTES + B_BYTES);
     static constexpr int P = 2;
-    static constexpr int S_FIT = (200 * 1024 - P * STGJ_BYTES) / SLOT;
+    static constexpr int SCR = 4 * WarpStore<float, JJ, 16>::BYTES;    // epilogue store scratch
+    static constexpr int S_FIT = (212 * 1024 - P * STGJ_BYTES - SCR) / SLOT;
     static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
-    static constexpr int BAR_OFF = S * SLOT + P * STGJ_BYTES;
+    static constexpr int SCR_OFF = S * SLOT + P * STGJ_BYTES;
+    static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
+    static_assert(SMEM <= 227 * 1024, "shared memory");
     static constexpr int TMEM_COLS = 2 * JJ * BN <= 256 ? 256 : 512;
     static_assert(JJ * BN <= 256 && BN % 16 == 0, "4 accumulators, double-buffered");
     static_assert(S >= 2, "pipeline too shallow");
@@ -521,6 +624,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * P]);
     const uint32_t slot0 = smem_u32(smem);        // S x [4 A tiles (8 KB) | 4 B tiles (BN*64 B)]
     const uint32_t stg0 = slot0 + S * C::SLOT;    // P x 32 KB staging
+    const uint32_t scr0 = slot0 + C::SCR_OFF;     // epilogue store scratch
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -655,19 +759,16 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 float v[JJ][16];
 #pragma unroll
                 for (int jj = 0; jj < JJ; ++jj) tmem_ld16(tbase + jj * BN + col, v[jj]);
-                if (n < B) {
-                    const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
-                    float* yp = Y + n * M + r0;
+                const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+                if (bias) {                       // KSLinear bias (NEXT-2)
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        float4 o = make_float4(v[0][e], v[1][e], v[2][e], v[3][e]);
-                        if (bias) {               // KSLinear bias (NEXT-2)
-                            const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + r0 + (int64_t)e * d));
-                            o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
-                        }
-                        __stcs(reinterpret_cast<float4*>(yp + (int64_t)e * d), o);
+                        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + r0 + (int64_t)e * d));
+                        v[0][e] += bb.x; v[1][e] += bb.y; v[2][e] += bb.z; v[3][e] += bb.w;
                     }
                 }
+                warp_store_rows<float, JJ, 16>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, JJ, 16>::BYTES, v, Y,
+                                               (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
             }
             tc_fence_before();
             mbar_arrive(acce0 + 8 * ab);
@@ -684,7 +785,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 // ==========================================================================
 // Half precision, BSF with d > 1 (NEXT-3).  J j-values per tile, chosen so the
 // X gather is a legal TMA box (inner extent a multiple of 16 bytes):
-//   J = d  (d <= 8 or d == 12): the J columns of all 16 l of a block are one
+//   J = d  (d in {2, 3, 4, 6, 8}): the J columns of all 16 l of a block are one
 //          contiguous run of 16*d halves of an X row -> 2-D box {16 d + 8, 128 n};
 //   J = 8  (d % 8 == 0):       3-D box {8 j, 17 l, 128 n} of X viewed [B][a c][d].
 // Either way a staged row n holds [16 l][J] halves plus 16 bytes of padding, so
@@ -692,8 +793,8 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 // 16-byte reads of 8 consecutive rows hit 8 different bank groups.  Each
 // transposer thread unpacks its row into J K-major A rows of 16 halves (32 B,
 // SWIZZLE_32B); per stage the MMA warp runs one K = 16 kind::f16 step into each
-// of J accumulators (2 x J x BN <= 512 TMEM columns); the epilogue writes the J
-// contiguous outputs of each (n, k) as one vector when J is even.
+// of J accumulators (2 x J x BN <= 512 TMEM columns); the epilogue stores
+// through warp_store_rows (coalesced 16-byte units).
 // ==========================================================================
 constexpr int BKH = 16;                        // l per stage (one UMMA k-step of 32 B)
 constexpr int AH_BYTES = BM * BKH * 2;         // 4 KB per j
@@ -725,12 +826,14 @@ struct HalfJCfg {
     static constexpr int BJ_BYTES = BN * BKH * 2;         // per j, BN * 32 B
     static constexpr int SLOT = J * (AH_BYTES + BJ_BYTES);
     static constexpr int P = 2;
-    static constexpr int S_FIT = (212 * 1024 - P * STG) / SLOT;
+    static constexpr int EC = J > 4 ? 8 : 16;             // epilogue columns per TMEM load
+    static constexpr int SCR = 4 * WarpStore<__half, J, EC>::BYTES;     // epilogue store scratch
+    static constexpr int S_FIT = (212 * 1024 - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
-    static constexpr int BAR_OFF = S * SLOT + P * STG;
+    static constexpr int SCR_OFF = S * SLOT + P * STG;
+    static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
     static constexpr int TMEM_COLS = 2 * J * BN <= 256 ? 256 : 512;
-    static constexpr int EC = J > 4 ? 8 : 16;             // epilogue columns per TMEM load
     static_assert(J * BN <= 256 && BN % 16 == 0, "J accumulators, double-buffered");
     static_assert(S >= 2, "pipeline too shallow");
     static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -756,6 +859,7 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * P]);
     const uint32_t slot0 = smem_u32(smem);        // S x [J A tiles (4 KB) | J B tiles (BN*32 B)]
     const uint32_t stg0 = slot0 + S * C::SLOT;    // P x staging
+    const uint32_t scr0 = slot0 + C::SCR_OFF;     // epilogue store scratch
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -903,44 +1007,15 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     if constexpr (EC == 16) tmem_ld16(tbase + jj * BN + col, v[jj]);
                     else tmem_ld8(tbase + jj * BN + col, v[jj]);
                 }
-                if (n < B) {
-                    const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
-                    T* yp = Y + n * M + r0;
+                const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+                if (bias) {                       // KSLinear bias (NEXT-2)
 #pragma unroll
-                    for (int e = 0; e < EC; ++e) {
-                        uint16_t o[J];
+                    for (int e = 0; e < EC; ++e)
 #pragma unroll
-                        for (int jj = 0; jj < J; ++jj) {
-                            float x = v[jj][e];
-                            if (bias) x += ElemTraits<T>::to_f(bias[r0 + (int64_t)e * d + jj]);   // NEXT-2
-                            const T h = ElemTraits<T>::from_f(x);
-                            o[jj] = reinterpret_cast<const uint16_t&>(h);
-                        }
-                        T* dst = yp + (int64_t)e * d;
-                        if constexpr (J % 2 == 0) {
-                            uint32_t pk[J / 2];
-#pragma unroll
-                            for (int q = 0; q < J / 2; ++q) pk[q] = (uint32_t)o[2 * q] | ((uint32_t)o[2 * q + 1] << 16);
-                            if constexpr (J % 8 == 0) {
-#pragma unroll
-                                for (int q = 0; q < J / 8; ++q)
-                                    __stcs(reinterpret_cast<uint4*>(dst) + q,
-                                           make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
-                            } else if constexpr (J % 4 == 0) {
-#pragma unroll
-                                for (int q = 0; q < J / 4; ++q)
-                                    __stcs(reinterpret_cast<uint2*>(dst) + q, make_uint2(pk[2 * q], pk[2 * q + 1]));
-                            } else {
-#pragma unroll
-                                for (int q = 0; q < J / 2; ++q) __stcs(reinterpret_cast<unsigned int*>(dst) + q, pk[q]);
-                            }
-                        } else {
-                            uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
-#pragma unroll
-                            for (int jj = 0; jj < J; ++jj) d16[jj] = o[jj];
-                        }
-                    }
+                        for (int jj = 0; jj < J; ++jj) v[jj][e] += ElemTraits<T>::to_f(bias[r0 + (int64_t)e * d + jj]);
                 }
+                warp_store_rows<T, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<T, J, EC>::BYTES, v, Y,
+                                          (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
             }
             tc_fence_before();
             mbar_arrive(acce0 + 8 * ab);
@@ -1096,7 +1171,7 @@ bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % BKJ == 0 && p
 
 // Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
 int pick_j_half(int64_t d) {
-    if (d == 2 || d == 3 || d == 4 || d == 6 || d == 8 || d == 12) return (int)d;
+    if (d == 2 || d == 3 || d == 4 || d == 6 || d == 8) return (int)d;
     return d % 8 == 0 ? 8 : 0;
 }
 int pick_bn_half(int64_t b, int J) {
@@ -1166,7 +1241,6 @@ cudaError_t launch_halfj_any(const ks_handle_s& h, const KsCall& call) {
         case 4: return launch_halfj_bn<T, 4>(h, call);
         case 6: return launch_halfj_bn<T, 6>(h, call);
         case 8: return launch_halfj_bn<T, 8>(h, call);
-        case 12: return launch_halfj_bn<T, 12>(h, call);
     }
     return cudaErrorInvalidValue;
 }
