@@ -56,6 +56,8 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);
 // half precision handles (NEXT-3): tcgen05 kind::f16 kernel and a generic one
 bool half_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t half_launch(const ks_handle_s& h, const KsCall& call);
+bool half_bsl_supports(const ks_handle_s& h, const KsCall& call);      // ks_half_bsl.cu (swap-AB)
+cudaError_t half_bsl_launch(const ks_handle_s& h, const KsCall& call);
 cudaError_t generic_half_launch(const ks_handle_s& h, const KsCall& call);
 cudaError_t pack_half(const ks_handle_s& h, cudaStream_t s);
 

@@ -30,124 +30,16 @@
 // X is fed as raw FP32 bits (the tensor core uses the TF32 part: truncation of
 // the 13 low mantissa bits); FP32 accumulation.  Contract: normwise error
 // <= 5e-3 (north star); R9/R10 give the per-element envelope.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
-
-#include <cstdlib>
-
-#include "ks_internal.h"
+#include "ks_umma.cuh"
 
 namespace {
 
-constexpr int BM = 128;        // batch rows per tile = UMMA M
 constexpr int BKC = 32;        // l per pipeline stage (4 UMMA k-steps of 8)
 constexpr int NTRANS = 128;    // transposer threads (warps 1-4)
 constexpr int NEPI = 128;      // epilogue threads (warps 6-9)
 constexpr int NTHREADS = 320;
 constexpr int A_BYTES = BM * BKC * 4;      // 16 KB
 constexpr int STG_BYTES = BKC * BM * 4;    // 16 KB staging chunk [32 l][128 n]
-
-// ---- PTX wrappers ----------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@P1 bra DONE;\n"
-        "bra LAB_WAIT;\n"
-        "DONE:\n"
-        "}\n" ::"r"(bar), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
-}
-__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
-}
-__device__ __forceinline__ float lds32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-
-// UMMA shared-memory descriptor for a K-major, 128-byte-swizzled operand:
-// start address, LBO = 16 B (unused for swizzled K-major), SBO = 1024 B
-// (stride between 8-row groups), version 1 (sm_100), layout type 2 (SW128).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(1024 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
-}
-
-// Instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128.
-__host__ __device__ constexpr uint32_t make_idesc(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
-}
 
 template <int LAYOUT, int BN>
 struct Tf32Cfg {
@@ -190,110 +82,13 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-// Element type T: float (kind::tf32, the TF32 path) or __nv_bfloat16 / __half
-// (kind::f16, the half-precision path, NEXT-3).  A 128-byte operand row holds
-// BK = 128 / sizeof(T) elements; one MMA consumes 32 bytes of K (KSTEP elements).
-template <typename T> struct ElemTraits;
-template <> struct ElemTraits<float> {
-    static constexpr uint32_t fmt = 2;  // TF32
-    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    __device__ static float to_f(float v) { return v; }
-    __device__ static float from_f(float v) { return v; }
-};
-template <> struct ElemTraits<__nv_bfloat16> {
-    static constexpr uint32_t fmt = 1;  // BF16
-    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    __device__ static float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
-    __device__ static __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
-};
-template <> struct ElemTraits<__half> {
-    static constexpr uint32_t fmt = 0;  // F16
-    static constexpr CUtensorMapDataType tma = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    __device__ static float to_f(__half v) { return __half2float(v); }
-    __device__ static __half from_f(float v) { return __float2half_rn(v); }
-};
-
-// BSF epilogue store through a warp-private shared-memory scratch.  Lane l holds
-// row n0w + l of the tile: v[j][k] is the output at element offset
-// off0 + k*d + j of that row of Y (row pitch ldy).  Each row's KB x J values are
-// packed into 16-byte units (row-major [k][j], pitch UR + 1 units: an odd
-// number, so the per-row writes are bank-conflict-free) and read back so that
-// consecutive lanes store consecutive units: one coalesced STG.128 per lane per
-// pass instead of 32 rows' worth of sectors per store instruction.  A unit
-// never straddles a run of J outputs unless the runs are contiguous (J == d).
-template <typename T, int J, int KB>
-struct WarpStore {
-    static constexpr int EPU = 16 / (int)sizeof(T);           // elements per 16-byte unit
-    static constexpr int UR = KB * J / EPU;                     // units per row
-    static constexpr int PITCH = (UR + 1) * 16;
-    static constexpr int BYTES = 32 * PITCH;                    // per warp
-    static_assert((KB * J) % EPU == 0 && UR % 2 == 0, "whole units, odd pitch");
-};
-
-template <typename T, int J, int KB>
-__device__ __forceinline__ void warp_store_rows(uint32_t scr, const float (&v)[J][KB], T* __restrict__ Y,
-                                                int64_t n0w, int64_t B, int64_t ldy, int64_t off0, int d, int lane) {
-    using W = WarpStore<T, J, KB>;
-    constexpr int EPU = W::EPU, UR = W::UR;
-#pragma unroll
-    for (int q = 0; q < UR; ++q) {
-        uint32_t w[4];
-        if constexpr (sizeof(T) == 4) {
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int e = q * 4 + x;
-                w[x] = __float_as_uint(v[e % J][e / J]);
-            }
-        } else {
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int e0 = q * 8 + 2 * x, e1 = e0 + 1;
-                const T lo = ElemTraits<T>::from_f(v[e0 % J][e0 / J]), hi = ElemTraits<T>::from_f(v[e1 % J][e1 / J]);
-                w[x] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) | ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
-            }
-        }
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(scr + lane * W::PITCH + q * 16), "r"(w[0]),
-                     "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < UR; ++t) {
-        const int u = t * 32 + lane;
-        const int r = u / UR, q = u % UR;
-        uint32_t w[4];
-        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(scr + r * W::PITCH + q * 16) : "memory");
-        const int e0 = q * EPU;
-        const int64_t n = n0w + r;
-        if (n < B)
-            __stcs(reinterpret_cast<uint4*>(Y + n * ldy + off0 + (int64_t)(e0 / J) * d + (e0 % J)),
-                   make_uint4(w[0], w[1], w[2], w[3]));
-    }
-    __syncwarp();
-}
-
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
-}
-
-template <typename T>
-__host__ __device__ constexpr uint32_t make_idesc_t(int n) {
-    return (1u << 4) | (ElemTraits<T>::fmt << 7) | (ElemTraits<T>::fmt << 10) | ((uint32_t)(n >> 3) << 17) |
-           ((uint32_t)(BM >> 4) << 24);
-}
-
 template <int LAYOUT, int BN, typename T = float>
 __global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
                int64_t ntiles, int dbg) {
     using C = Tf32Cfg<LAYOUT, BN>;
+    static_assert(LAYOUT != KS_LAYOUT_BSL || sizeof(T) == 4, "half BSL runs the swap-AB kernel (ks_half_bsl.cu)");
     constexpr int BKC = 128 / (int)sizeof(T);        // K elements per stage (one 128-byte row)
     constexpr int KSTEP = 32 / (int)sizeof(T);       // K elements per MMA
     constexpr int S = C::S;
@@ -381,50 +176,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         }
     } else if (warp <= 4) {
         // ---------------- BSL transposers: staging [l][n] -> K-major SW128 A ----------------
-        if constexpr (LAYOUT == KS_LAYOUT_BSL && sizeof(T) == 2) {
-            // Half: thread t owns the batch-row pair (2p, 2p+1) for l in [32h, 32h+32).
-            // One LDS.32 fetches both rows' values at one l (a warp reads 128
-            // contiguous bytes); PRMT pairs (l, l+1) per row; 4 STS.128 per row.
-            // Lanes with (p >> 2) odd write their odd row first, so the 8 lanes of
-            // a store phase hit 8 different rows mod 8 (conflict-free SW128).
-            const int t = tid - 32;
-            const int p = t & 63, hh = t >> 6;
-            const int s = (p >> 2) & 1;
-            const int rA = 2 * p + s, rB = 2 * p + 1 - s;
-            const uint32_t selA = s ? 0x7632u : 0x5410u, selB = s ? 0x5410u : 0x7632u;
-            const uint32_t offA = (uint32_t)((rA / 8) * 1024 + (rA % 8) * 128);
-            const uint32_t offB = (uint32_t)((rB / 8) * 1024 + (rB % 8) * 128);
-            for (int64_t g = 0; g < G; ++g) {
-                const int pp = (int)(g % P);
-                mbar_wait(sfull0 + 8 * pp, (uint32_t)((g / P) & 1));
-                uint32_t w[32];
-                const uint32_t src = stg0 + pp * STG_BYTES + (uint32_t)(hh * 32) * (BM * 2) + 4 * p;
-#pragma unroll
-                for (int l = 0; l < 32; ++l)
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[l]) : "r"(src + l * (BM * 2)));
-                fence_proxy_async();      // generic reads before the TMA (async proxy) refill
-                mbar_arrive(sempty0 + 8 * pp);
-                const int st = (int)(g % S);
-                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
-                uint32_t oa[16], ob[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    oa[q] = __byte_perm(w[2 * q], w[2 * q + 1], selA);
-                    ob[q] = __byte_perm(w[2 * q], w[2 * q + 1], selB);
-                }
-                const uint32_t base = slot0 + st * C::SLOT;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int ch = 4 * hh + k;
-                    sts128(base + offA + ((ch ^ (rA % 8)) * 16), __uint_as_float(oa[4 * k]), __uint_as_float(oa[4 * k + 1]),
-                           __uint_as_float(oa[4 * k + 2]), __uint_as_float(oa[4 * k + 3]));
-                    sts128(base + offB + ((ch ^ (rB % 8)) * 16), __uint_as_float(ob[4 * k]), __uint_as_float(ob[4 * k + 1]),
-                           __uint_as_float(ob[4 * k + 2]), __uint_as_float(ob[4 * k + 3]));
-                }
-                fence_proxy_async();
-                mbar_arrive(full0 + 8 * st);
-            }
-        } else if constexpr (LAYOUT == KS_LAYOUT_BSL) {
+        if constexpr (LAYOUT == KS_LAYOUT_BSL) {
             const int r = tid - 32;                                    // batch row in the tile
             const uint32_t rowoff = (uint32_t)((r / 8) * 1024 + (r % 8) * 128);
             for (int64_t g = 0; g < G; ++g) {
@@ -508,22 +260,6 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     if (!(dbg & 1))
                         warp_store_rows<T, 1, 16>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, 1, 16>::BYTES, vv, Y,
                                                   (int64_t)tc.n0 + lq * 32, B, M, (int64_t)tc.i * b + tc.k0 + col, 1, lane);
-                } else if constexpr (sizeof(T) == 2) {
-                    // lanes (n, n+1) swap halves so each stores one 32-bit pair:
-                    // the even lane (v_e(n), v_e(n+1)) in row r_e, the odd lane
-                    // (v_{e+1}(n-1), v_{e+1}(n)) in row r_{e+1} (B % 8 == 0: aligned,
-                    // and n, n+1 are both in or both out of range)
-                    const bool odd = lane & 1;
-#pragma unroll
-                    for (int e = 0; e < 16; e += 2) {
-                        const float x = __shfl_xor_sync(0xffffffffu, odd ? v[e] : v[e + 1], 1);
-                        const T lo = ElemTraits<T>::from_f(odd ? x : v[e]);
-                        const T hi = ElemTraits<T>::from_f(odd ? v[e + 1] : x);
-                        const uint32_t pk = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
-                                            ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
-                        const int64_t r = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e + (odd ? 1 : 0)) * d + tc.j;
-                        if (n < B && !(dbg & 1)) __stcs(reinterpret_cast<unsigned int*>(Y + r * B + (n & ~int64_t(1))), pk);
-                    }
                 } else if (n < B && !(dbg & 1)) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
@@ -561,16 +297,6 @@ constexpr int JJ = 4;
 constexpr int AJ_BYTES = BM * BKJ * 4;        // 8 KB per j
 constexpr int STGJ_ROW = (BKJ + 1) * JJ * 4;  // 272 B: box {4 j, 17 l, 128 n}, 1 l of padding
 constexpr int STGJ_BYTES = BM * STGJ_ROW;      // 34 KB staging chunk [128 n][17 l][4 j]
-
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(512 >> 4) << 32;            // 8 rows x 64 B
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)4 << 61;                     // SWIZZLE_64B
-    return d;
-}
 
 template <int BN>
 struct Tf32JCfg {
@@ -799,26 +525,6 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 constexpr int BKH = 16;                        // l per stage (one UMMA k-step of 32 B)
 constexpr int AH_BYTES = BM * BKH * 2;         // 4 KB per j
 
-__device__ __forceinline__ uint64_t sw32_desc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(256 >> 4) << 32;            // 8 rows x 32 B
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)6 << 61;                     // SWIZZLE_32B
-    return d;
-}
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
-}
-
 template <int J, int BN>
 struct HalfJCfg {
     static constexpr int PITCH = 32 * J + 16;             // staged row: [16 l][J] halves + 16 B
@@ -1030,52 +736,6 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 }
 
 // ------------------------------------------------------------------ host ------
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-            const cuuint32_t* box, CUtensorMapSwizzle sw,
-            CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims,
-                    strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// KS_TF32_DEBUG (profiling experiments only): bit 0 skips the epilogue's global
-// stores, bit 1 skips the transposers' shared-memory reads.  0 in production.
-// KS_TF32_MAXGRID (tests): cap the persistent grid so small problems exercise
-// several tiles per CTA.  0 / unset in production.
-int max_grid() {
-    static int v = [] {
-        const char* e = getenv("KS_TF32_MAXGRID");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
-int debug_flags() {
-    static int v = [] {
-        const char* e = getenv("KS_TF32_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
 // Output-tile width: the whole block when b <= 128 (two CTAs per SM fit), else
 // the largest divisor <= 128 (b/BN tiles share one X tile through L2: the tile
 // order runs the k-chunks of a tile back to back).
@@ -1296,8 +956,8 @@ bool half_supports(const ks_handle_s& h, const KsCall& call) {
     if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31)) return false;
     if (call.B >= (int64_t(1) << 31)) return false;
     const uintptr_t xa = reinterpret_cast<uintptr_t>(call.X), ya = reinterpret_cast<uintptr_t>(call.Y);
+    if (call.layout == KS_LAYOUT_BSL) return half_bsl_supports(h, call);
     if (xa & 15) return false;
-    if (call.layout == KS_LAYOUT_BSL) return call.B % 8 == 0 && (ya & 1) == 0;
     if (ya & 15) return false;
     if (h.d == 1) return true;
     // BSF d > 1: J-column gather (bias read as scalars, any 2-byte alignment)
@@ -1307,8 +967,7 @@ bool half_supports(const ks_handle_s& h, const KsCall& call) {
 
 cudaError_t half_launch(const ks_handle_s& h, const KsCall& call) {
     const bool bf = h.dtype == KS_DTYPE_BF16;
-    if (call.layout == KS_LAYOUT_BSL)
-        return bf ? launch_layout<KS_LAYOUT_BSL, __nv_bfloat16>(h, call) : launch_layout<KS_LAYOUT_BSL, __half>(h, call);
+    if (call.layout == KS_LAYOUT_BSL) return half_bsl_launch(h, call);
     if (h.d == 1)
         return bf ? launch_layout<KS_LAYOUT_BSF, __nv_bfloat16>(h, call) : launch_layout<KS_LAYOUT_BSF, __half>(h, call);
     return bf ? launch_halfj_any<__nv_bfloat16>(h, call) : launch_halfj_any<__half>(h, call);
