@@ -375,7 +375,7 @@ def run_ours(args):
         # second half of the metric: configs[2] median speedup vs bmm+permute
         from bench_sweep import run_sweep
         sw = {}
-        for math in ("fp32", "tf32"):
+        for math in ("fp32", "f32x3", "tf32", "bf16"):
             r = run_sweep(dev, reps=5, math=math)
             r.pop("rows")
             sw[math] = r

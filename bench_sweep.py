@@ -1,5 +1,7 @@
 """configs[2] sweep: the 88 paper-grid patterns with b = c in {48,64,96,128},
-a*d <= 64, B = 25088, FP32.
+a*d <= 64, B = 25088, FP32.  Also math = "tf32";
+"f32x3" (the FP32-accurate 3xTF32 tensor-core mode, against the true-FP32
+bmm); "bf16" / "f16" (NEXT-3, against torch.bmm in the same half format).
 
 For every pattern and layout, times ks_matmul (one fused launch) against the
 paper's bmm+permute baseline (App. A listing; BSL = the
@@ -54,7 +56,7 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
 
     pats = patterns or ksgen.grid.sweep_patterns()
     B = ksgen.configs.SWEEP_BATCH
-    torch.backends.cuda.matmul.allow_tf32 = (math == "tf32")
+    torch.backends.cuda.matmul.allow_tf32 = (math == "tf32")   # f32x3 is compared with true-FP32 bmm
     dt = {"bf16": torch.bfloat16, "f16": torch.float16}.get(math, torch.float32)
     esize = 2 if dt != torch.float32 else 4
     props = torch.cuda.get_device_properties(dev)
@@ -69,8 +71,8 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
         M, N = a * b * d, a * c * d
         K4 = torch.from_numpy(ksgen.k4_uniform(*p, seed=1000)).to(dt)
         f = ksb.Factor(*p, K4)
-        if math == "tf32":
-            f.set_math(ksb.MATH_TF32)
+        if math in ("tf32", "f32x3"):
+            f.set_math(ksb.MATH_TF32 if math == "tf32" else ksb.MATH_F32X3)
         Kb = K4.permute(0, 3, 1, 2).reshape(a * d, b, c).contiguous().to(dev)
         rec = {"pattern": list(p)}
         for lay in ("bsf", "bsl"):

@@ -16,7 +16,9 @@
  * Conventions shared by every entry point
  *  - Element type: IEEE float32 for X, K, Y.  Arithmetic is FP32 FFMA on
  *    CUDA cores (KS_MATH_FP32, default) or TF32 tensor cores with FP32
- *    accumulation (KS_MATH_TF32; only where b,c >= 16).
+ *    accumulation (KS_MATH_TF32; only where b,c >= 16), or FP32 accuracy on
+ *    the tensor cores through the 3xTF32 split x k ~ x_lo k_hi + x_hi k_lo +
+ *    x_hi k_hi (KS_MATH_F32X3; b,c >= 16; not in the paper -- see DESIGN.md).
  *  - Indexing is 64-bit throughout.  B = 0 is a no-op returning KS_OK.
  *  - Pointers named X / Y below are CUDA DEVICE pointers (e.g. a torch
  *    tensor's data_ptr()) on the device the handle was packed on, contiguous,
@@ -55,7 +57,7 @@ typedef enum { KS_LAYOUT_BSF = 0, KS_LAYOUT_BSL = 1 } ks_layout_t;
 
 /* Arithmetic.  TF32: operands rounded to TF32 (K: round-to-nearest-away at
  * pack time; X: per kernel), products accumulated in FP32. */
-typedef enum { KS_MATH_FP32 = 0, KS_MATH_TF32 = 1 } ks_math_t;
+typedef enum { KS_MATH_FP32 = 0, KS_MATH_TF32 = 1, KS_MATH_F32X3 = 2 } ks_math_t;
 
 /* Storage / operand type of a handle and of the X, Y, bias it is used with.
  * F32 handles follow ks_math_t.  BF16 / F16 handles (the
@@ -116,9 +118,13 @@ void ks_free(ks_handle_t h);
 /* Pattern of a handle: out[0..3] = a,b,c,d.                               */
 ks_status_t ks_get_pattern(ks_handle_t h, int64_t out[4]);
 
-/* Select the arithmetic.  KS_MATH_TF32 needs b >= 16 and c >= 16
- * (north star: tensor cores only where each block is a dense contraction);
- * otherwise KS_ERR_UNSUPPORTED and the math is unchanged.                  */
+/* Select the arithmetic.  KS_MATH_TF32 and KS_MATH_F32X3 need b >= 16 and
+ * c >= 16 (north star: tensor cores only where each block is a dense
+ * contraction); otherwise KS_ERR_UNSUPPORTED and the math is unchanged.
+ * KS_MATH_F32X3 allocates and packs the low halves rna_tf32(K - rna_tf32(K)) on the
+ * handle's device the first time (synchronous).  Calls the F32X3 tensor-core
+ * kernels cannot take (BSF with d > 1 and d % 4 != 0) run the FP32 CUDA-core
+ * kernels.                                                                 */
 ks_status_t ks_set_math(ks_handle_t h, ks_math_t m);
 
 /* Force a kernel family (tests / benchmarks).  KS_KERNEL_AUTO restores the
@@ -201,7 +207,9 @@ ks_status_t ks_chain_host(const ks_handle_t* handles, int L, const float* X_host
 /* Copy one packed variant of K back to host (tests check the index maps
  * bit-exactly).  variant 0: canonical a*b*c*d;  1: tile-contiguous K^T,
  * [i*d+j][l][k] (a*d*c*b floats);  2: TF32-rounded tiles [i*d+j][k][l]
- * (a*d*b*c floats).  count must equal the variant's element count.  Half
+ * (a*d*b*c floats);  3: the F32X3 low halves rna_tf32(K - rna_tf32(K)), same order
+ * as 2 (only after ks_set_math(h, KS_MATH_F32X3)).  count must equal the
+ * variant's element count.  Half
  * handles copy elements of their dtype (2 bytes each): variant 0 canonical,
  * 2 tensor-core tiles [i*d+j][k][l] (unrounded); variant 1 does not exist.  */
 ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst_host, int64_t count);

@@ -14,6 +14,7 @@ struct ks_handle_s {
     float* k_canon;       // [a][b][c][d]            (boundary order)
     float* k_tile;        // [i*d+j][l][k]  = K^T tiles
     float* k_tf32;        // [i*d+j][k][l]  TF32-rounded, K-major B operand
+    float* k_lo;          // [i*d+j][k][l]  rna_tf32(K - k_tf32) (3xTF32 low part), from ks_set_math(F32X3)
     ks_math_t math;
     ks_kernel_t forced;
     int dtype = KS_DTYPE_F32;   // element type of K, X, Y (half handles: k_canon / k_tf32
@@ -37,6 +38,7 @@ void count_launch();
 
 // ---- packing (ks_pack.cu) --------------------------------------------------
 cudaError_t pack_tiles(const ks_handle_s& h, cudaStream_t s);
+cudaError_t pack_lo(const ks_handle_s& h, cudaStream_t s);        // fills h.k_lo
 
 // ---- kernel families ---------------------------------------------------------
 // Each family exposes `supports` (pure host predicate, no CUDA calls) and

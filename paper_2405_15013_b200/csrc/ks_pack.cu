@@ -4,6 +4,8 @@
 //                                            tile, k fastest
 //   k_tf32[(i*d+j)][k][l]  = rna_tf32(K4[i][k][l][j])   K-major B operand of the
 //                                            tcgen05 TF32 kernel, pre-rounded
+//   k_lo  [(i*d+j)][k][l]  = rna_tf32(K4[i][k][l][j] - k_tf32[...]) -- the low
+//                                            part of the 3xTF32 split (F32X3)
 // Excluded from timing.
 #include "ks_internal.h"
 
@@ -35,6 +37,22 @@ __global__ void pack_kernel(const float* __restrict__ k4, float* __restrict__ ti
     }
 }
 
+__global__ void pack_lo_kernel(const float* __restrict__ k4, float* __restrict__ lo, int64_t a, int64_t b,
+                               int64_t c, int64_t d) {
+    const int64_t nnz = a * b * c * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e % d;
+        int64_t t = e / d;
+        const int64_t l = t % c;
+        t /= c;
+        const int64_t k = t % b;
+        const int64_t i = t / b;
+        const float v = k4[e];
+        lo[((i * d + j) * b + k) * c + l] = round_tf32_rna(v - round_tf32_rna(v));
+    }
+}
+
 // Half handles: a pure permutation of the 16-bit values into [i*d+j][k][l]
 // (the tensor-core weight tiles); no rounding.
 __global__ void pack_half_kernel(const uint16_t* __restrict__ k4, uint16_t* __restrict__ mma, int64_t a,
@@ -62,6 +80,15 @@ cudaError_t pack_half(const ks_handle_s& h, cudaStream_t s) {
     if (blocks > 65535 * 8) blocks = 65535 * 8;
     pack_half_kernel<<<(unsigned)blocks, threads, 0, s>>>(reinterpret_cast<const uint16_t*>(h.k_canon),
                                                           reinterpret_cast<uint16_t*>(h.k_tf32), h.a, h.b, h.c, h.d);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pack_lo(const ks_handle_s& h, cudaStream_t s) {
+    const int threads = 256;
+    int64_t blocks = (h.nnz + threads - 1) / threads;
+    if (blocks > 65535 * 8) blocks = 65535 * 8;
+    pack_lo_kernel<<<(unsigned)blocks, threads, 0, s>>>(h.k_canon, h.k_lo, h.a, h.b, h.c, h.d);
     count_launch();
     return cudaGetLastError();
 }

@@ -122,7 +122,7 @@ ks_kernel_t choose(const ks_handle_s& h, const KsCall& call) {
             default: return KS_KERNEL_AUTO;
         }
     }
-    if (h.math == KS_MATH_TF32 && ks::tf32_supports(h, call)) return KS_KERNEL_TF32;
+    if ((h.math == KS_MATH_TF32 || h.math == KS_MATH_F32X3) && ks::tf32_supports(h, call)) return KS_KERNEL_TF32;
     if (ks::stream_supports(h, call)) return KS_KERNEL_STREAM;
     if (ks::ffma_supports(h, call)) return KS_KERNEL_FFMA;
     return KS_KERNEL_GENERIC;
@@ -351,6 +351,7 @@ void ks_free(ks_handle_t h) {
     cudaFree(h->k_canon);
     cudaFree(h->k_tile);
     cudaFree(h->k_tf32);
+    cudaFree(h->k_lo);
     if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
     delete h;
 }
@@ -363,12 +364,27 @@ ks_status_t ks_get_pattern(ks_handle_t h, int64_t out[4]) {
 
 ks_status_t ks_set_math(ks_handle_t h, ks_math_t m) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
-    if (m != KS_MATH_FP32 && m != KS_MATH_TF32) return fail(KS_ERR_INVALID_ARG, "bad math %d", (int)m);
-    if (m == KS_MATH_TF32 && h->dtype != KS_DTYPE_F32)
+    if (m != KS_MATH_FP32 && m != KS_MATH_TF32 && m != KS_MATH_F32X3)
+        return fail(KS_ERR_INVALID_ARG, "bad math %d", (int)m);
+    if (m != KS_MATH_FP32 && h->dtype != KS_DTYPE_F32)
         return fail(KS_ERR_UNSUPPORTED, "math applies to F32 handles (half handles use kind::f16)");
-    if (m == KS_MATH_TF32 && (h->b < 16 || h->c < 16))
-        return fail(KS_ERR_UNSUPPORTED, "TF32 needs b,c >= 16 (pattern has b=%lld c=%lld)",
+    if (m != KS_MATH_FP32 && (h->b < 16 || h->c < 16))
+        return fail(KS_ERR_UNSUPPORTED, "tensor-core math needs b,c >= 16 (pattern has b=%lld c=%lld)",
                     (long long)h->b, (long long)h->c);
+    if (m == KS_MATH_F32X3 && !h->k_lo) {      // the low halves of the 3xTF32 split, once per handle
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != h->device) cudaSetDevice(h->device);
+        float* lo = nullptr;
+        cudaError_t e = cudaMalloc(&lo, sizeof(float) * (size_t)h->nnz);
+        if (e == cudaSuccess) {
+            h->k_lo = lo;
+            if ((e = ks::pack_lo(*h, 0)) == cudaSuccess) e = cudaStreamSynchronize(0);
+            if (e != cudaSuccess) { cudaFree(lo); h->k_lo = nullptr; }
+        }
+        if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
+        if (e != cudaSuccess) return fail_cuda(e, "ks_set_math(F32X3) pack");
+    }
     h->math = m;
     return ok();
 }
@@ -511,8 +527,9 @@ ks_status_t ks_chain_host(const ks_handle_t* hs, int L, const float* Xh, float* 
 ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst, int64_t count) {
     if (!h || !dst) return fail(KS_ERR_INVALID_ARG, "NULL argument");
     if (count != h->nnz) return fail(KS_ERR_INVALID_ARG, "count must be a*b*c*d = %lld", (long long)h->nnz);
-    const float* src = variant == 0 ? h->k_canon : variant == 1 ? h->k_tile : variant == 2 ? h->k_tf32 : nullptr;
-    if (!src) return fail(KS_ERR_INVALID_ARG, "variant must be 0, 1 or 2");
+    const float* src = variant == 0 ? h->k_canon : variant == 1 ? h->k_tile : variant == 2 ? h->k_tf32
+                     : variant == 3 ? h->k_lo : nullptr;
+    if (!src) return fail(KS_ERR_INVALID_ARG, "variant must be 0, 1, 2 or 3 (3 after ks_set_math(F32X3))");
     cudaError_t e = cudaMemcpy(dst, src, (size_t)h->esize() * (size_t)count, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail_cuda(e, "ks_read_packed");
     return ok();

@@ -34,35 +34,61 @@
 
 namespace {
 
-constexpr int BKC = 32;        // l per pipeline stage (4 UMMA k-steps of 8)
 constexpr int NTRANS = 128;    // transposer threads (warps 1-4)
 constexpr int NEPI = 128;      // epilogue threads (warps 6-9)
 constexpr int NTHREADS = 320;
-constexpr int A_BYTES = BM * BKC * 4;      // 16 KB
-constexpr int STG_BYTES = BKC * BM * 4;    // 16 KB staging chunk [32 l][128 n]
 
-template <int LAYOUT, int BN>
+// RB = bytes of K per operand row per stage: 128 (SWIZZLE_128B; TF32 32 l, half
+// 64 l) or 64 (SWIZZLE_64B, 16 l) for the 3xTF32 split (X3), whose doubled A
+// and B tiles would not leave room for two CTAs per SM at 128.
+template <int LAYOUT, int BN, bool X3 = false>
 struct Tf32Cfg {
-    static constexpr int B_BYTES = BN * BKC * 4;          // BN * 128 B (multiple of 1 KB)
+    static constexpr int RB = X3 ? 64 : 128;
+    static constexpr int A_TILE = BM * RB;                // 16 KB (8 KB for X3)
+    static constexpr int B_TILE = BN * RB;
+    static constexpr int NA = X3 ? 2 : 1;                 // X3: A = x (raw) and x_lo; B = k_hi and k_lo
+    static constexpr int A_BYTES = NA * A_TILE;
+    static constexpr int B_BYTES = NA * B_TILE;
     static constexpr int SLOT = A_BYTES + B_BYTES;
+    static constexpr int STG = BM * RB;                   // BSL staging chunk [RB/4 l][128 n] (FP32)
     // Two co-resident CTAs per SM (TMEM 2 x 2*BN <= 512 columns, ~110 KB smem each)
     // measured ~1.4x faster than one deep-pipelined CTA: more independent
     // tiles in flight hide TMA latency better than a deeper ring.
     static constexpr int CTAS = BN <= 128 ? 2 : 1;                                // CTAs per SM
     static constexpr int BUDGET = CTAS == 2 ? 110 * 1024 : 200 * 1024;
-    static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 ? 3 : 2) : 3) : 0;   // staging
+    static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 || X3 ? 3 : 2) : 3) : 0;   // staging
     // BSF: 4 epilogue warps x 32 rows x (4 + 1) 16-byte units of store scratch (WarpStore<float, 1, 16>)
     static constexpr int SCR = LAYOUT == KS_LAYOUT_BSL ? 0 : 4 * 32 * 5 * 16;
-    static constexpr int S_FIT = (BUDGET - P * STG_BYTES - SCR) / SLOT;
+    static constexpr int S_FIT = (BUDGET - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 6 ? 6 : S_FIT;                              // operand slots
-    static constexpr int SCR_OFF = S * SLOT + P * STG_BYTES;
+    static constexpr int SCR_OFF = S * SLOT + P * STG;
     static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;                            // + barriers + align pad
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
     static_assert(BN % 16 == 0 && BN <= 256, "UMMA N for M=128");
     static_assert(S >= 2, "pipeline too shallow");
+    static_assert((3 * S + 4 + 2 * (P > 0 ? P : 1)) * 8 + 4 <= 256, "barrier area");
 };
+
+template <int RB>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
+    if constexpr (RB == 128) return sw128_desc(addr);
+    else return sw64_desc(addr);
+}
+
+// 3xTF32 (X3) split of x: hi = rna_tf32(x), lo = rna_tf32(x - hi) (x - hi is
+// exact in FP32), so x = hi + lo up to 2^-22 |x| and the MMA's own TF32 read of
+// both parts is exact.
+__device__ __forceinline__ uint32_t rna_tf32(uint32_t xbits) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(__uint_as_float(xbits)));
+    return r;
+}
+__device__ __forceinline__ void tf32_split(uint32_t x, uint32_t& hi, uint32_t& lo) {
+    hi = rna_tf32(x);
+    lo = rna_tf32(__float_as_uint(__uint_as_float(x) - __uint_as_float(hi)));
+}
 
 struct TileCoord {
     int i, j, k0;
@@ -82,31 +108,35 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-template <int LAYOUT, int BN, typename T = float>
-__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN>::CTAS)
+template <int LAYOUT, int BN, typename T = float, bool X3 = false>
+__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-               T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
-               int64_t ntiles, int dbg) {
-    using C = Tf32Cfg<LAYOUT, BN>;
+               const __grid_constant__ CUtensorMap kmap_lo, T* __restrict__ Y, const T* __restrict__ bias,
+               int64_t B, int a, int b, int c, int d, int64_t ntiles, int dbg) {
+    using C = Tf32Cfg<LAYOUT, BN, X3>;
     static_assert(LAYOUT != KS_LAYOUT_BSL || sizeof(T) == 4, "half BSL runs the swap-AB kernel (ks_half_bsl.cu)");
-    constexpr int BKC = 128 / (int)sizeof(T);        // K elements per stage (one 128-byte row)
+    static_assert(!X3 || sizeof(T) == 4, "3xTF32 is an FP32 mode");
+    constexpr int RB = C::RB;
+    constexpr int BKC = RB / (int)sizeof(T);         // K elements per stage (one operand row)
     constexpr int KSTEP = 32 / (int)sizeof(T);       // K elements per MMA
+    constexpr int NCH = RB / 16;                     // 16-byte chunks per operand row
     constexpr int S = C::S;
     constexpr int P = C::P > 0 ? C::P : 1;      // (BSF: no staging; P only names unused barriers)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     // [0,S) full  [S,2S) empty  [2S,2S+2) acc_full  [2S+2,2S+4) acc_empty
-    // [2S+4, 2S+4+P) stg_full  [.., +P) stg_empty   then the TMEM slot
+    // [2S+4, 2S+4+P) stg_full  [.., +P) stg_empty  [.., +S) split_full (BSF X3)  then the TMEM slot
     const uint32_t full0 = smem_u32(&bars[0]);
     const uint32_t empty0 = smem_u32(&bars[S]);
     const uint32_t accf0 = smem_u32(&bars[2 * S]);
     const uint32_t acce0 = smem_u32(&bars[2 * S + 2]);
     const uint32_t sfull0 = smem_u32(&bars[2 * S + 4]);
-    const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + (P > 0 ? P : 1)]);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * (P > 0 ? P : 1)]);
-    const uint32_t slot0 = smem_u32(smem);                 // S x (A 16 KB | B BN*128 B), 1 KB aligned
-    const uint32_t stg0 = slot0 + S * C::SLOT;             // P x 16 KB staging (BSL)
+    const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + P]);
+    const uint32_t xfull0 = smem_u32(&bars[2 * S + 4 + 2 * P]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[3 * S + 4 + 2 * P]);
+    const uint32_t slot0 = smem_u32(smem);                 // S x (A tiles | B tiles), 1 KB aligned
+    const uint32_t stg0 = slot0 + S * C::SLOT;             // P x staging (BSL)
     const uint32_t scr0 = slot0 + C::SCR_OFF;              // BSF epilogue store scratch
 
     const int tid = threadIdx.x;
@@ -118,11 +148,15 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     const int nk = (c + BKC - 1) / BKC;
     const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t G = my_tiles * nk;
+    // the MMA waits for the transposers (BSL), the splitters (BSF X3) or the TMA (BSF)
+    constexpr bool SPLIT = X3 && LAYOUT != KS_LAYOUT_BSL;
+    const uint32_t ready0 = SPLIT ? xfull0 : full0;
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, LAYOUT == KS_LAYOUT_BSL ? 1 + NTRANS : 2);
             mbar_init(empty0 + 8 * s, 1);
+            mbar_init(xfull0 + 8 * s, NTRANS);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(accf0 + 8 * s, 1);
@@ -135,6 +169,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+        if (X3) asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap_lo) : "memory");
     }
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -155,8 +190,8 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 const int l0 = (int)(gx % nk) * BKC;
                 const int p = (int)(gx % P);
                 if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
-                mbar_expect_tx(sfull0 + 8 * p, STG_BYTES);
-                tma_3d(stg0 + p * STG_BYTES, &xmap, tc.n0, tc.j, tc.i * c + l0, sfull0 + 8 * p);
+                mbar_expect_tx(sfull0 + 8 * p, C::STG);
+                tma_3d(stg0 + p * C::STG, &xmap, tc.n0, tc.j, tc.i * c + l0, sfull0 + 8 * p);
             };
             if (LAYOUT == KS_LAYOUT_BSL)
                 for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
@@ -166,39 +201,77 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 const int l0 = (int)(g % nk) * BKC;
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                const uint32_t sa = slot0 + st * C::SLOT;
                 if (LAYOUT != KS_LAYOUT_BSL) {
-                    mbar_expect_tx(full0 + 8 * st, A_BYTES);
-                    tma_2d(slot0 + st * C::SLOT, &xmap, tc.i * c + l0, tc.n0, full0 + 8 * st);
+                    mbar_expect_tx(full0 + 8 * st, C::A_TILE);
+                    tma_2d(sa, &xmap, tc.i * c + l0, tc.n0, full0 + 8 * st);
                 }
                 mbar_expect_tx(full0 + 8 * st, C::B_BYTES);
-                tma_2d(slot0 + st * C::SLOT + A_BYTES, &kmap, l0, tc.q * b + tc.k0, full0 + 8 * st);
+                tma_2d(sa + C::A_BYTES, &kmap, l0, tc.q * b + tc.k0, full0 + 8 * st);
+                if (X3) tma_2d(sa + C::A_BYTES + C::B_TILE, &kmap_lo, l0, tc.q * b + tc.k0, full0 + 8 * st);
             }
         }
     } else if (warp <= 4) {
-        // ---------------- BSL transposers: staging [l][n] -> K-major SW128 A ----------------
+        const int r = tid - 32;                                    // batch row in the tile
+        const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
+        const int sw = RB == 128 ? (r % 8) : (r % 8) / 2;          // SW128 / SW64 chunk XOR
         if constexpr (LAYOUT == KS_LAYOUT_BSL) {
-            const int r = tid - 32;                                    // batch row in the tile
-            const uint32_t rowoff = (uint32_t)((r / 8) * 1024 + (r % 8) * 128);
+            // ---------------- BSL transposers: staging [l][n] -> K-major A (and x_lo for X3) ----------------
             for (int64_t g = 0; g < G; ++g) {
                 const int p = (int)(g % P);
                 mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
                 // column r of the staged [BKC l][128 n] chunk, as 32-bit words
-                uint32_t w[32];
-                const uint32_t src = stg0 + p * STG_BYTES + 4 * r;
+                uint32_t w[BKC];
+                const uint32_t src = stg0 + p * C::STG + 4 * r;
 #pragma unroll
-                for (int l = 0; l < 32; ++l)
+                for (int l = 0; l < BKC; ++l)
                     w[l] = (dbg & 2) ? 0u : __float_as_uint(lds32(src + l * (BM * 4)));
                 fence_proxy_async();      // generic reads before the TMA (async proxy) refill
                 mbar_arrive(sempty0 + 8 * p);
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
                 const uint32_t dst = slot0 + st * C::SLOT + rowoff;
+                if constexpr (X3) {
 #pragma unroll
-                for (int ch = 0; ch < 8; ++ch)
-                    sts128(dst + ((ch ^ (r % 8)) * 16), __uint_as_float(w[4 * ch]), __uint_as_float(w[4 * ch + 1]),
-                           __uint_as_float(w[4 * ch + 2]), __uint_as_float(w[4 * ch + 3]));
+                    for (int ch = 0; ch < NCH; ++ch) {
+                        uint32_t hi[4], lo[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) tf32_split(w[4 * ch + e], hi[e], lo[e]);
+                        sts128(dst + ((ch ^ sw) * 16), __uint_as_float(hi[0]), __uint_as_float(hi[1]),
+                               __uint_as_float(hi[2]), __uint_as_float(hi[3]));
+                        sts128(dst + C::A_TILE + ((ch ^ sw) * 16), __uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                               __uint_as_float(lo[2]), __uint_as_float(lo[3]));
+                    }
+                } else {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch)
+                        sts128(dst + ((ch ^ sw) * 16), __uint_as_float(w[4 * ch]), __uint_as_float(w[4 * ch + 1]),
+                               __uint_as_float(w[4 * ch + 2]), __uint_as_float(w[4 * ch + 3]));
+                }
                 fence_proxy_async();
                 mbar_arrive(full0 + 8 * st);
+            }
+        } else if constexpr (SPLIT) {
+            // ---------------- BSF X3 splitters: A (x, TMA-loaded) -> hi in place + lo tile ----------------
+            for (int64_t g = 0; g < G; ++g) {
+                const int st = (int)(g % S);
+                mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+                const uint32_t base = slot0 + st * C::SLOT + rowoff;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {        // same swizzled position in both tiles;
+                    const uint32_t off = ((ch ^ sw) * 16);    // visiting chunks in XOR order is conflict-free
+                    uint32_t v[4], hi[4], lo[4];
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(base + off));
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) tf32_split(v[e], hi[e], lo[e]);
+                    sts128(base + off, __uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(hi[2]),
+                           __uint_as_float(hi[3]));
+                    sts128(base + C::A_TILE + off, __uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                           __uint_as_float(lo[2]), __uint_as_float(lo[3]));
+                }
+                fence_proxy_async();
+                mbar_arrive(xfull0 + 8 * st);
             }
         }
     } else if (warp == 5) {
@@ -214,18 +287,25 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 const uint32_t dtm = tmem + (uint32_t)(ab * BN);
                 for (int t = 0; t < nk; ++t, ++g) {
                     const int st = (int)(g % S);
-                    mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+                    mbar_wait(ready0 + 8 * st, (uint32_t)((g / S) & 1));
                     tc_fence_after();
                     const uint32_t sa = slot0 + st * C::SLOT;
-                    const uint32_t sb = sa + A_BYTES;
+                    const uint32_t sb = sa + C::A_BYTES;
                     const int ksteps = min(BKC / KSTEP, (c - t * BKC) / KSTEP);
                     for (int s = 0; s < ksteps; ++s) {
-                        if constexpr (sizeof(T) == 4)
-                            mma_tf32(dtm, sw128_desc(sa + 32 * s), sw128_desc(sb + 32 * s), idesc,
-                                     (t > 0 || s > 0) ? 1u : 0u);
-                        else
-                            mma_f16(dtm, sw128_desc(sa + 32 * s), sw128_desc(sb + 32 * s), idesc,
-                                    (t > 0 || s > 0) ? 1u : 0u);
+                        const uint32_t acc = (t > 0 || s > 0) ? 1u : 0u;
+                        if constexpr (X3) {
+                            // x k ~ x_lo k_hi + x_hi k_lo + x_hi k_hi (all operands exact TF32)
+                            mma_tf32(dtm, kmajor_desc<RB>(sa + C::A_TILE + 32 * s), kmajor_desc<RB>(sb + 32 * s),
+                                     idesc, acc);
+                            mma_tf32(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + C::B_TILE + 32 * s),
+                                     idesc, 1u);
+                            mma_tf32(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + 32 * s), idesc, 1u);
+                        } else if constexpr (sizeof(T) == 4) {
+                            mma_tf32(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + 32 * s), idesc, acc);
+                        } else {
+                            mma_f16(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + 32 * s), idesc, acc);
+                        }
                     }
                     mma_commit(empty0 + 8 * st);
                 }
@@ -292,21 +372,25 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 // direct per-row float4 stores touched 32 sectors per instruction, 4x ideal,
 // and made the epilogue the bottleneck).
 // ==========================================================================
-constexpr int BKJ = 16;                       // l per stage (2 UMMA k-steps)
 constexpr int JJ = 4;
-constexpr int AJ_BYTES = BM * BKJ * 4;        // 8 KB per j
-constexpr int STGJ_ROW = (BKJ + 1) * JJ * 4;  // 272 B: box {4 j, 17 l, 128 n}, 1 l of padding
-constexpr int STGJ_BYTES = BM * STGJ_ROW;      // 34 KB staging chunk [128 n][17 l][4 j]
 
-template <int BN>
+// X3 (3xTF32) halves the l per stage (8: one MMA k-step, 32-byte SWIZZLE_32B
+// rows) so that the doubled A and B tiles still leave a 2-deep pipeline.
+template <int BN, bool X3 = false>
 struct Tf32JCfg {
-    static constexpr int B_BYTES = BN * BKJ * 4;          // per j, BN * 64 B
-    static constexpr int SLOT = JJ * (AJ_BYTES + B_BYTES);
+    static constexpr int BKJ = X3 ? 8 : 16;               // l per stage
+    static constexpr int RB = BKJ * 4;                    // operand row bytes (SW32 / SW64)
+    static constexpr int NA = X3 ? 2 : 1;                 // hi (+ lo) tiles
+    static constexpr int AJ_TILE = BM * RB;               // per j
+    static constexpr int BJ_TILE = BN * RB;
+    static constexpr int SLOT = JJ * NA * (AJ_TILE + BJ_TILE);
+    static constexpr int STG_ROW = (BKJ + 1) * JJ * 4;    // box {4 j, BKJ+1 l, 128 n}: 1 l of padding
+    static constexpr int STG = BM * STG_ROW;              // (odd number of 16-byte units per row)
     static constexpr int P = 2;
     static constexpr int SCR = 4 * WarpStore<float, JJ, 16>::BYTES;    // epilogue store scratch
-    static constexpr int S_FIT = (212 * 1024 - P * STGJ_BYTES - SCR) / SLOT;
+    static constexpr int S_FIT = (212 * 1024 - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
-    static constexpr int SCR_OFF = S * SLOT + P * STGJ_BYTES;
+    static constexpr int SCR_OFF = S * SLOT + P * STG;
     static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
     static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -314,6 +398,12 @@ struct Tf32JCfg {
     static_assert(JJ * BN <= 256 && BN % 16 == 0, "4 accumulators, double-buffered");
     static_assert(S >= 2, "pipeline too shallow");
 };
+
+template <int RB>
+__device__ __forceinline__ uint64_t kmajor_desc_j(uint32_t addr) {
+    if constexpr (RB == 64) return sw64_desc(addr);
+    else return sw32_desc(addr);
+}
 
 struct TileJ {
     int i, j0, k0, n0;
@@ -330,14 +420,17 @@ __device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_
     return t;
 }
 
-template <int BN>
+template <int BN, bool X3 = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                    float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c,
-                    int d, int64_t ntiles) {
-    using C = Tf32JCfg<BN>;
+                    const __grid_constant__ CUtensorMap kmap_lo, float* __restrict__ Y,
+                    const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles) {
+    using C = Tf32JCfg<BN, X3>;
     constexpr int S = C::S;
     constexpr int P = C::P;
+    constexpr int BKJ = C::BKJ;
+    constexpr int RB = C::RB;
+    constexpr int NCH = RB / 16;                  // 16-byte chunks per A row
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -348,9 +441,11 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     const uint32_t sfull0 = smem_u32(&bars[2 * S + 4]);
     const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + P]);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * P]);
-    const uint32_t slot0 = smem_u32(smem);        // S x [4 A tiles (8 KB) | 4 B tiles (BN*64 B)]
-    const uint32_t stg0 = slot0 + S * C::SLOT;    // P x 32 KB staging
+    // slot: [A hi (4 j)] [A lo (4 j), X3] [B hi (4 j)] [B lo (4 j), X3]
+    const uint32_t slot0 = smem_u32(smem);
+    const uint32_t stg0 = slot0 + S * C::SLOT;    // P x staging
     const uint32_t scr0 = slot0 + C::SCR_OFF;     // epilogue store scratch
+    constexpr int A_ALL = JJ * C::NA * C::AJ_TILE;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -379,6 +474,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+        if (X3) asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap_lo) : "memory");
     }
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -397,8 +493,8 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 const int l0 = (int)(gx % nk) * BKJ;
                 const int p = (int)(gx % P);
                 if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
-                mbar_expect_tx(sfull0 + 8 * p, STGJ_BYTES);
-                tma_3d(stg0 + p * STGJ_BYTES, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
+                mbar_expect_tx(sfull0 + 8 * p, C::STG);
+                tma_3d(stg0 + p * C::STG, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
             };
             for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
             for (int64_t g = 0; g < G; ++g) {
@@ -407,24 +503,27 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 const int l0 = (int)(g % nk) * BKJ;
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
-                mbar_expect_tx(full0 + 8 * st, JJ * C::B_BYTES);
-                const uint32_t sb = slot0 + st * C::SLOT + JJ * AJ_BYTES;
-                for (int jj = 0; jj < JJ; ++jj)
-                    tma_2d(sb + jj * C::B_BYTES, &kmap, l0, ((tc.i * d + tc.j0 + jj) * b) + tc.k0, full0 + 8 * st);
+                mbar_expect_tx(full0 + 8 * st, JJ * C::NA * C::BJ_TILE);
+                const uint32_t sb = slot0 + st * C::SLOT + A_ALL;
+                for (int jj = 0; jj < JJ; ++jj) {
+                    const int row = ((tc.i * d + tc.j0 + jj) * b) + tc.k0;
+                    tma_2d(sb + jj * C::BJ_TILE, &kmap, l0, row, full0 + 8 * st);
+                    if (X3) tma_2d(sb + (JJ + jj) * C::BJ_TILE, &kmap_lo, l0, row, full0 + 8 * st);
+                }
             }
         }
     } else if (warp <= 4) {
-        // staging [n][l][j] (256 B per row n) -> 4 K-major SW64 A tiles
+        // staging [n][l][j] (STG_ROW bytes per row n) -> 4 K-major A tiles (+ 4 lo tiles for X3)
         const int r = tid - 32;
-        const uint32_t rowoff = (uint32_t)((r / 8) * 512 + (r % 8) * 64);
-        const int sw = (r % 8) / 2;
+        const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
+        const int sw = RB == 64 ? (r % 8) / 2 : (r % 8) / 4;       // SW64 / SW32 chunk XOR
         for (int64_t g = 0; g < G; ++g) {
             const int p = (int)(g % P);
             mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
             float v[BKJ][JJ];
-            // rows are 17 l long (the box carries one extra l as padding), so the 8
+            // rows are BKJ+1 l long (the box carries one extra l as padding), so the 8
             // rows of a shared-memory phase fall on 8 different 16-byte bank groups
-            const uint32_t src = stg0 + p * STGJ_BYTES + r * STGJ_ROW;
+            const uint32_t src = stg0 + p * C::STG + r * C::STG_ROW;
 #pragma unroll
             for (int l = 0; l < BKJ; ++l)
                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -437,9 +536,20 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
             for (int jj = 0; jj < JJ; ++jj)
 #pragma unroll
-                for (int ch = 0; ch < BKJ / 4; ++ch)
-                    sts128(sa + jj * AJ_BYTES + ((ch ^ sw) * 16), v[4 * ch][jj], v[4 * ch + 1][jj],
-                           v[4 * ch + 2][jj], v[4 * ch + 3][jj]);
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const uint32_t off = jj * C::AJ_TILE + ((ch ^ sw) * 16);
+                    if constexpr (X3) {
+                        uint32_t hi[4], lo[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) tf32_split(__float_as_uint(v[4 * ch + e][jj]), hi[e], lo[e]);
+                        sts128(sa + off, __uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(hi[2]),
+                               __uint_as_float(hi[3]));
+                        sts128(sa + JJ * C::AJ_TILE + off, __uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                               __uint_as_float(lo[2]), __uint_as_float(lo[3]));
+                    } else {
+                        sts128(sa + off, v[4 * ch][jj], v[4 * ch + 1][jj], v[4 * ch + 2][jj], v[4 * ch + 3][jj]);
+                    }
+                }
             fence_proxy_async();
             mbar_arrive(full0 + 8 * st);
         }
@@ -456,13 +566,23 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
                     tc_fence_after();
                     const uint32_t sa = slot0 + st * C::SLOT;
-                    const uint32_t sb = sa + JJ * AJ_BYTES;
+                    const uint32_t sb = sa + A_ALL;
 #pragma unroll
-                    for (int jj = 0; jj < JJ; ++jj)
+                    for (int jj = 0; jj < JJ; ++jj) {
+                        const uint32_t dtm = tmem + (uint32_t)((ab * JJ + jj) * BN);
 #pragma unroll
-                        for (int s = 0; s < BKJ / 8; ++s)
-                            mma_tf32(tmem + (uint32_t)((ab * JJ + jj) * BN), sw64_desc(sa + jj * AJ_BYTES + 32 * s),
-                                     sw64_desc(sb + jj * C::B_BYTES + 32 * s), idesc, (t > 0 || s > 0) ? 1u : 0u);
+                        for (int s = 0; s < BKJ / 8; ++s) {
+                            const uint32_t acc = (t > 0 || s > 0) ? 1u : 0u;
+                            const uint32_t ah = sa + jj * C::AJ_TILE + 32 * s, bh = sb + jj * C::BJ_TILE + 32 * s;
+                            if constexpr (X3) {    // x_lo k_hi + x_hi k_lo + x_hi k_hi
+                                mma_tf32(dtm, kmajor_desc_j<RB>(ah + JJ * C::AJ_TILE), kmajor_desc_j<RB>(bh), idesc, acc);
+                                mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh + JJ * C::BJ_TILE), idesc, 1u);
+                                mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh), idesc, 1u);
+                            } else {
+                                mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh), idesc, acc);
+                            }
+                        }
+                    }
                     mma_commit(empty0 + 8 * st);
                 }
                 mma_commit(accf0 + 8 * ab);
@@ -471,14 +591,12 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         __syncwarp();
     } else {
         const int lq = warp & 3;
-        const int row = lq * 32 + lane;
         int64_t it = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const TileJ tc = decode_j(tile, nkc, njg, nnb, BN);
             const int ab = (int)(it & 1);
             mbar_wait(accf0 + 8 * ab, (uint32_t)((it / 2) & 1));
             tc_fence_after();
-            const int64_t n = (int64_t)tc.n0 + row;
             const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * JJ * BN);
 #pragma unroll 1
             for (int col = 0; col < BN; col += 16) {
@@ -746,18 +864,21 @@ int pick_bn(int64_t b) {
     return 0;
 }
 
-template <int LAYOUT, int BN, typename T = float>
+template <int LAYOUT, int BN, typename T = float, bool X3 = false>
 cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
-    using C = Tf32Cfg<LAYOUT, BN>;
-    constexpr cuuint32_t BK = 128 / sizeof(T);
+    using C = Tf32Cfg<LAYOUT, BN, X3>;
+    constexpr cuuint32_t BK = C::RB / sizeof(T);
     constexpr cuuint64_t ES = sizeof(T);
+    constexpr CUtensorMapSwizzle SW = C::RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     const CUtensorMapDataType dt = ElemTraits<T>::tma;
-    CUtensorMap xmap, kmap;
+    CUtensorMap xmap, kmap, kmap_lo;
     {
         const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
         const cuuint64_t ks[1] = {(cuuint64_t)h.c * ES};
         const cuuint32_t kb[2] = {BK, BN};
-        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return cudaErrorInvalidValue;
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, SW, dt)) return cudaErrorInvalidValue;
+        kmap_lo = kmap;
+        if (X3 && !encode(&kmap_lo, h.k_lo, 2, kd, ks, kb, SW, dt)) return cudaErrorInvalidValue;
     }
     if (LAYOUT == KS_LAYOUT_BSL) {
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
@@ -768,9 +889,9 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * ES};
         const cuuint32_t xb[2] = {BK, BM};
-        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return cudaErrorInvalidValue;
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, SW, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_kernel<LAYOUT, BN, T>;
+    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -781,7 +902,7 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, reinterpret_cast<T*>(call.Y),
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, kmap_lo, reinterpret_cast<T*>(call.Y),
                                                               reinterpret_cast<const T*>(call.bias), call.B, (int)h.a,
                                                               (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags());
     ks::count_launch();
@@ -794,23 +915,26 @@ int pick_bn_j(int64_t b) {
     return 0;
 }
 
-template <int BN>
+template <int BN, bool X3 = false>
 cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
-    using C = Tf32JCfg<BN>;
-    CUtensorMap xmap, kmap;
+    using C = Tf32JCfg<BN, X3>;
+    constexpr CUtensorMapSwizzle SW = C::RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUtensorMap xmap, kmap, kmap_lo;
     {
         const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
         const cuuint64_t ks[1] = {(cuuint64_t)h.c * 4};
-        const cuuint32_t kb[2] = {BKJ, BN};
-        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+        const cuuint32_t kb[2] = {(cuuint32_t)C::BKJ, BN};
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, SW)) return cudaErrorInvalidValue;
+        kmap_lo = kmap;
+        if (X3 && !encode(&kmap_lo, h.k_lo, 2, kd, ks, kb, SW)) return cudaErrorInvalidValue;
     }
     {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
-        const cuuint32_t xb[3] = {JJ, BKJ + 1, BM};
+        const cuuint32_t xb[3] = {JJ, (cuuint32_t)C::BKJ + 1, BM};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_bsfj_kernel<BN>;
+    auto kern = ks_tf32_bsfj_kernel<BN, X3>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -821,13 +945,24 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, call.Y, call.bias, call.B, (int)h.a,
+    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, kmap_lo, call.Y, call.bias, call.B, (int)h.a,
                                                               (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
     return cudaGetLastError();
 }
 
-bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % BKJ == 0 && pick_bn_j(h.b) != 0; }
+template <bool X3>
+cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
+    switch (pick_bn_j(h.b)) {
+        case 64: return launch_bsfj<64, X3>(h, call);
+        case 48: return launch_bsfj<48, X3>(h, call);
+        case 32: return launch_bsfj<32, X3>(h, call);
+        case 16: return launch_bsfj<16, X3>(h, call);
+    }
+    return cudaErrorInvalidValue;
+}
+
+bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % 16 == 0 && pick_bn_j(h.b) != 0; }
 
 // Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
 int pick_j_half(int64_t d) {
@@ -905,17 +1040,17 @@ cudaError_t launch_halfj_any(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
-template <int LAYOUT, typename T = float>
+template <int LAYOUT, typename T = float, bool X3 = false>
 cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn(h.b)) {
-        case 128: return launch_bn<LAYOUT, 128, T>(h, call);
-        case 112: return launch_bn<LAYOUT, 112, T>(h, call);
-        case 96: return launch_bn<LAYOUT, 96, T>(h, call);
-        case 80: return launch_bn<LAYOUT, 80, T>(h, call);
-        case 64: return launch_bn<LAYOUT, 64, T>(h, call);
-        case 48: return launch_bn<LAYOUT, 48, T>(h, call);
-        case 32: return launch_bn<LAYOUT, 32, T>(h, call);
-        case 16: return launch_bn<LAYOUT, 16, T>(h, call);
+        case 128: return launch_bn<LAYOUT, 128, T, X3>(h, call);
+        case 112: return launch_bn<LAYOUT, 112, T, X3>(h, call);
+        case 96: return launch_bn<LAYOUT, 96, T, X3>(h, call);
+        case 80: return launch_bn<LAYOUT, 80, T, X3>(h, call);
+        case 64: return launch_bn<LAYOUT, 64, T, X3>(h, call);
+        case 48: return launch_bn<LAYOUT, 48, T, X3>(h, call);
+        case 32: return launch_bn<LAYOUT, 32, T, X3>(h, call);
+        case 16: return launch_bn<LAYOUT, 16, T, X3>(h, call);
     }
     return cudaErrorInvalidValue;
 }
@@ -933,19 +1068,20 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0 && (ya & 3) == 0;
     if (ya & 15) return false;
     // BSF: d = 1 direct; d % 4 == 0 four-j gather (its bias loads are 16-byte vectors)
+    if (h.math == KS_MATH_F32X3 && !h.k_lo) return false;
     return h.d == 1 || (bsfj_ok(h) && (reinterpret_cast<uintptr_t>(call.bias) & 15) == 0);
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
+    if (h.math == KS_MATH_F32X3) {
+        if (!h.k_lo) return cudaErrorInvalidValue;
+        if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL, float, true>(h, call);
+        if (h.d == 1) return launch_layout<KS_LAYOUT_BSF, float, true>(h, call);
+        return launch_bsfj_any<true>(h, call);
+    }
     if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL>(h, call);
     if (h.d == 1) return launch_layout<KS_LAYOUT_BSF>(h, call);
-    switch (pick_bn_j(h.b)) {
-        case 64: return launch_bsfj<64>(h, call);
-        case 48: return launch_bsfj<48>(h, call);
-        case 32: return launch_bsfj<32>(h, call);
-        case 16: return launch_bsfj<16>(h, call);
-    }
-    return cudaErrorInvalidValue;
+    return launch_bsfj_any<false>(h, call);
 }
 
 // ---- half precision (NEXT-3): the same warp-specialised tcgen05 kernel with

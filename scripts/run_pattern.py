@@ -26,8 +26,8 @@ a, b, c, d = args.p
 M, N = a * b * d, a * c * d
 dt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[args.dtype]
 f = ksb.Factor(a, b, c, d, torch.from_numpy(ksgen.k4_uniform(a, b, c, d, seed=1)).to(dt))
-if args.math == "tf32":
-    f.set_math(ksb.MATH_TF32)
+if args.math in ("tf32", "f32x3"):
+    f.set_math(ksb.MATH_TF32 if args.math == "tf32" else ksb.MATH_F32X3)
 if args.kernel != "auto":
     f.set_kernel({"generic": 1, "stream": 2, "ffma": 3, "tf32": 4}[args.kernel])
 dev = torch.device("cuda:0")
