@@ -171,7 +171,11 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
     extern __shared__ __align__(128) float4 sm4[];
     __shared__ __align__(8) uint64_t full[2];
     const int N = P.N;
-    float* buf[2] = {reinterpret_cast<float*>(sm4), reinterpret_cast<float*>(sm4) + (size_t)R * N};
+    // buffer b at smf + b*R*N: indexing the shared symbol directly (not through an
+    // array of pointers) keeps the accesses in the shared window (LDS/STS, not
+    // generic LD/ST -- measured: the pointer array made every row access generic)
+    float* const smf = reinterpret_cast<float*>(sm4);
+    auto buf = [&](int64_t k) { return smf + (size_t)(k & 1) * R * N; };
     const int64_t ngroups = (B + R - 1) / R;
     const int64_t mine = ngroups > blockIdx.x ? (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     auto group_rows = [&](int64_t k) {
@@ -184,7 +188,7 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
         const uint32_t bar = smem_u32(&full[k & 1]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(smem_u32(buf[k & 1])), "l"(X + row0 * N), "r"(bytes), "r"(bar) : "memory");
+                     ::"r"(smem_u32(buf(k))), "l"(X + row0 * N), "r"(bytes), "r"(bar) : "memory");
     };
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[0])));
@@ -207,7 +211,7 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
                 "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}\n" ::"r"(bar), "r"(par) : "memory");
         }
-        float* sm = buf[k & 1];
+        float* sm = buf(k);
         const int rows = group_rows(k);
         int f = 0;
         for (int ps = 0; ps < P.npass; ++ps) {
