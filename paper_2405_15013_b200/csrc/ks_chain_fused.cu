@@ -170,6 +170,8 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
                       const __grid_constant__ FusedParams P, int R) {
     extern __shared__ __align__(128) float4 sm4[];
     __shared__ __align__(8) uint64_t full[2];
+    pdl_wait();
+    pdl_launch_dependents();
     const int N = P.N;
     // buffer b at smf + b*R*N: indexing the shared symbol directly (not through an
     // array of pointers) keeps the accesses in the shared window (LDS/STS, not
@@ -304,19 +306,13 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
     int64_t groups = (call.B + R - 1) / R;
     const int64_t grid = groups < sms ? groups : sms;             // persistent, one CTA per SM
     cudaError_t e;
-    if (hs[0]->b == 2) {
-        e = cudaFuncSetAttribute(ks_chain_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        ks_chain_fused_kernel<2><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.bias, call.B, P,
-                                                                                 (int)R);
-    } else {
-        e = cudaFuncSetAttribute(ks_chain_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        ks_chain_fused_kernel<4><<<(unsigned)grid, THREADS, smem, call.stream>>>(call.X, call.Y, call.bias, call.B, P,
-                                                                                 (int)R);
-    }
+    auto kern = hs[0]->b == 2 ? ks_chain_fused_kernel<2> : ks_chain_fused_kernel<4>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(kern, dim3((unsigned)grid), dim3(THREADS), smem, call.stream, call.X, call.Y, call.bias, call.B, P,
+                   (int)R);
     count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace ks

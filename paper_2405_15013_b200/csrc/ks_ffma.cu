@@ -66,6 +66,8 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
                const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
     using C = Cfg<LAYOUT, J, WPJM, WPJN, TN>;
     using VT = typename VecJ<J>::T;
+    pdl_wait();
+    pdl_launch_dependents();
     extern __shared__ __align__(16) float smem[];
     float* As = smem;                         // [2][BK][J][BMJ]
     float* Bs = smem + 2 * C::A_ELEMS;        // [2][BK][J][BN]
@@ -331,10 +333,11 @@ cudaError_t launch_cfg(const ks_handle_s& h, const KsCall& call) {
     const int64_t nnb = (call.B + C::BMJ - 1) / C::BMJ;
     const int64_t blocks = nkc * nnb * (h.a * h.d / J);
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    kern<<<(unsigned)blocks, C::THREADS, C::SMEM_BYTES, call.stream>>>(
-        call.X, h.k_tile, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d);
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(C::THREADS), C::SMEM_BYTES, call.stream,
+                                         call.X, (const float*)h.k_tile, call.Y, call.bias, call.B, (int)h.a,
+                                         (int)h.b, (int)h.c, (int)h.d);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 template <int LAYOUT, int J>

@@ -18,6 +18,8 @@ template <int LAYOUT>
 __global__ void __launch_bounds__(256) ks_generic_kernel(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
     const float* __restrict__ bias, int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int64_t M = a * b * d, N = a * c * d;
     const int64_t total = B * M;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -48,6 +50,8 @@ template <typename T, int LAYOUT>
 __global__ void __launch_bounds__(256) ks_generic_half_kernel(
     const T* __restrict__ X, const T* __restrict__ K4, T* __restrict__ Y, const T* __restrict__ bias,
     int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int64_t M = a * b * d, N = a * c * d;
     const int64_t total = B * M;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -84,14 +88,12 @@ cudaError_t launch_generic_half(const ks_handle_s& h, const KsCall& call) {
     T* Y = reinterpret_cast<T*>(call.Y);
     const T* K = reinterpret_cast<const T*>(h.k_canon);
     const T* bias = reinterpret_cast<const T*>(call.bias);
-    if (call.layout == KS_LAYOUT_BSF)
-        ks_generic_half_kernel<T, KS_LAYOUT_BSF><<<(unsigned)blocks, threads, 0, call.stream>>>(
-            X, K, Y, bias, call.B, h.a, h.b, h.c, h.d);
-    else
-        ks_generic_half_kernel<T, KS_LAYOUT_BSL><<<(unsigned)blocks, threads, 0, call.stream>>>(
-            X, K, Y, bias, call.B, h.a, h.b, h.c, h.d);
+    auto kern = call.layout == KS_LAYOUT_BSF ? ks_generic_half_kernel<T, KS_LAYOUT_BSF>
+                                             : ks_generic_half_kernel<T, KS_LAYOUT_BSL>;
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, X, K, Y, bias,
+                                         call.B, (int64_t)h.a, (int64_t)h.b, (int64_t)h.c, (int64_t)h.d);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace
@@ -112,14 +114,12 @@ cudaError_t generic_launch(const ks_handle_s& h, const KsCall& call) {
     const int64_t cap = (int64_t)num_sms(h.device) * 8 * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    if (call.layout == KS_LAYOUT_BSF)
-        ks_generic_kernel<KS_LAYOUT_BSF><<<(unsigned)blocks, threads, 0, call.stream>>>(
-            call.X, h.k_canon, call.Y, call.bias, call.B, h.a, h.b, h.c, h.d);
-    else
-        ks_generic_kernel<KS_LAYOUT_BSL><<<(unsigned)blocks, threads, 0, call.stream>>>(
-            call.X, h.k_canon, call.Y, call.bias, call.B, h.a, h.b, h.c, h.d);
+    auto kern = call.layout == KS_LAYOUT_BSF ? ks_generic_kernel<KS_LAYOUT_BSF> : ks_generic_kernel<KS_LAYOUT_BSL>;
+    const cudaError_t e = launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, call.X,
+                                     (const float*)h.k_canon, call.Y, call.bias, call.B, (int64_t)h.a, (int64_t)h.b,
+                                     (int64_t)h.c, (int64_t)h.d);
     count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace ks

@@ -115,6 +115,8 @@ ks_half_bsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();                 // the prologue above overlaps the previous kernel's drain (PDL)
+    pdl_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -254,11 +256,11 @@ cudaError_t launch_hb(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, HB_THREADS, C::SMEM, call.stream>>>(xmap, kmap, reinterpret_cast<T*>(call.Y),
-                                                                 reinterpret_cast<const T*>(call.bias), call.B,
-                                                                 (int)h.a, (int)h.b, (int)h.c, (int)h.d, BN, ntiles);
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(HB_THREADS), C::SMEM, call.stream, xmap,
+                                         kmap, reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias),
+                                         call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, BN, ntiles);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace

@@ -70,3 +70,35 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
 int num_sms(int device);
 
 }  // namespace ks
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Kernels launched through launch_pdl may be scheduled while the previous
+// kernel in the stream drains (its CTAs exit); each such kernel calls
+// pdl_wait() before its first global-memory access, which returns once the
+// previous grid has completed and its writes are visible.  Only the prologue
+// (launch, shared-memory carve-out, barrier init, TMEM alloc) overlaps.
+// KS_PDL=0 disables it (experiments).
+namespace ks {
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}  // namespace ks
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -279,6 +280,14 @@ int num_sms(int device) {
         cache[device] = n > 0 ? n : 148;
     }
     return cache[device];
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("KS_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 }  // namespace ks
 

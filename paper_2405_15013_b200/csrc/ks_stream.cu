@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
     const float* __restrict__ bias, int64_t B, int a, int d) {
     using T = typename Vec<V>::T;
+    pdl_wait();
+    pdl_launch_dependents();
     const int dv = d / V;
     const int64_t P = (int64_t)a * dv;                 // items per batch row
     const int64_t chunks = (B + RT - 1) / RT;
@@ -114,6 +116,8 @@ __global__ void __launch_bounds__(256) ks_stream_bsl(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
     const float* __restrict__ bias, int64_t B, int a, int d, int64_t nblocks) {
     using T = typename Vec<V>::T;
+    pdl_wait();
+    pdl_launch_dependents();
     const int64_t NV = B / V;
     const int64_t q = blockIdx.x / nblocks;          // q = i*d + j
     const int64_t nb = blockIdx.x - q * nblocks;
@@ -162,10 +166,10 @@ cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
     const int64_t P = h.a * (h.d / V);
     const int64_t items = P * ((call.B + RT - 1) / RT);
     const int64_t blocks = (items + threads - 1) / threads;
-    ks_stream_bsf<BB, CC, V, RT><<<(unsigned)blocks, threads, 0, call.stream>>>(
-        call.X, h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d);
+    cudaError_t e = ks::launch_pdl(ks_stream_bsf<BB, CC, V, RT>, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
+                                   call.X, (const float*)h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 template <int BB, int CC, int V>
@@ -176,10 +180,11 @@ cudaError_t launch_bsl(const ks_handle_s& h, const KsCall& call) {
     if (NV < 256) threads = (int)((NV + 31) / 32 * 32);
     const int64_t nblocks = (NV + (int64_t)threads * RT - 1) / ((int64_t)threads * RT);
     const int64_t blocks = h.a * h.d * nblocks;
-    ks_stream_bsl<BB, CC, V, RT><<<(unsigned)blocks, threads, 0, call.stream>>>(
-        call.X, h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d, nblocks);
+    cudaError_t e = ks::launch_pdl(ks_stream_bsl<BB, CC, V, RT>, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
+                                   call.X, (const float*)h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d,
+                                   nblocks);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 int pick_vec(const ks_handle_s& h, const KsCall& call) {

@@ -180,6 +180,8 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();                 // the prologue above overlaps the previous kernel's drain (PDL)
+    pdl_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -485,6 +487,8 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();                 // the prologue above overlaps the previous kernel's drain (PDL)
+    pdl_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -723,6 +727,8 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();                 // the prologue above overlaps the previous kernel's drain (PDL)
+    pdl_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -902,11 +908,11 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device) * C::CTAS;
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, kmap_lo, reinterpret_cast<T*>(call.Y),
-                                                              reinterpret_cast<const T*>(call.bias), call.B, (int)h.a,
-                                                              (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags());
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
+                                         kmap_lo, reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias),
+                                         call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags());
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 int pick_bn_j(int64_t b) {
@@ -945,10 +951,11 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, kmap_lo, call.Y, call.bias, call.B, (int)h.a,
-                                                              (int)h.b, (int)h.c, (int)h.d, ntiles);
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
+                                         kmap_lo, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
+                                         ntiles);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 template <bool X3>
@@ -1008,11 +1015,11 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
     int64_t slots = (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
-    kern<<<(unsigned)grid, NTHREADS, C::SMEM, call.stream>>>(xmap, kmap, reinterpret_cast<T*>(call.Y),
-                                                              reinterpret_cast<const T*>(call.bias), call.B, (int)h.a,
-                                                              (int)h.b, (int)h.c, (int)h.d, ntiles);
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
+                                         reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias), call.B,
+                                         (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 template <typename T, int J>
