@@ -1,6 +1,35 @@
-"""Summarise ncu outputs from gpurun_out/ into profiles/ (launch shares + full-set metrics)."""
-import csv, io, json, subprocess, sys
+"""Summarise ncu outputs from gpurun_out/ into profiles/ (launch shares + full-set metrics).
+
+    python scripts/ncu_summary.py TAG            # every gpurun_out/prof_*.raw.csv (scripts/prof_final.sh)
+    python scripts/ncu_summary.py TAG REP.ncu-rep  # one report
+
+Per capture: duration, DRAM bytes read/written (the roofline "traffic"), DRAM
+throughput, SM / L1 / L2 throughput, tensor-pipe instructions, registers, grid,
+warp stall mix.  The launch list gives each kernel family's share of the GPU
+time of `bench.py --steps 2 --warmup 1` (ncu --metrics gpu__time_duration.sum).
+"""
+import csv
+import glob
+import io
+import json
+import os
+import subprocess
+import sys
 from collections import defaultdict
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tc.sum", "launch__grid_size", "launch__block_size",
+        "launch__shared_mem_per_block_dynamic",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__m_l1tex2xbar_write_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
+        "smsp__cycles_active.avg"]
+
 
 def launches(path):
     lines = [l for l in open(path) if not l.startswith("==")]
@@ -16,34 +45,49 @@ def launches(path):
                     "share": round(sum(v) / tot, 4)})
     return out
 
-WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
-        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum",
-        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
-        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_tc.sum", "launch__grid_size", "launch__block_size",
-        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"]
 
-def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    r = list(csv.reader(io.StringIO(raw)))
+def _rows(raw_text):
+    r = list(csv.reader(io.StringIO(raw_text)))
     hdr, units = r[0], r[1]
     res = []
     for row in r[2:]:
-        d = {"kernel": row[hdr.index("Kernel Name")][:120]}
+        if len(row) != len(hdr):
+            continue
+        d = {"kernel": row[hdr.index("Kernel Name")][:140]}
         for w in WANT:
             if w in hdr:
                 d[w] = f"{row[hdr.index(w)]} {units[hdr.index(w)]}".strip()
+        try:
+            rd = float(row[hdr.index("dram__bytes_read.sum")].replace(",", ""))
+            wr = float(row[hdr.index("dram__bytes_write.sum")].replace(",", ""))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            d["dram_traffic_bytes"] = int(rd * scale[units[hdr.index("dram__bytes_read.sum")]] +
+                                          wr * scale[units[hdr.index("dram__bytes_write.sum")]])
+        except (ValueError, KeyError):
+            pass
         res.append(d)
     return res
 
+
+def full(path):
+    if path.endswith(".csv"):
+        return _rows(open(path).read())
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    return _rows(raw)
+
+
 if __name__ == "__main__":
     tag = sys.argv[1]
-    out = {"launch_list": launches("gpurun_out/launches.csv")}
-    try:
-        out["full_set"] = full(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/prof_full.ncu-rep")
-    except Exception as e:
-        out["full_set_error"] = str(e)
+    out = {}
+    if os.path.exists("gpurun_out/launches.csv"):
+        out["launch_list"] = launches("gpurun_out/launches.csv")
+    srcs = sys.argv[2:] or sorted(glob.glob("gpurun_out/prof_*.raw.csv"))
+    out["captures"] = {}
+    for s in srcs:
+        name = os.path.basename(s).replace(".raw.csv", "").replace(".ncu-rep", "")
+        try:
+            out["captures"][name] = full(s)
+        except Exception as e:  # noqa: BLE001
+            out["captures"][name] = {"error": str(e)}
     json.dump(out, open(f"profiles/{tag}.json", "w"), indent=1)
-    print(json.dumps(out, indent=1)[:4000])
+    print(json.dumps(out, indent=1)[:3000])
