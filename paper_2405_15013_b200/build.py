@@ -43,7 +43,7 @@ def _compile(src: str, verbose: bool) -> str:
     hm = _headers_mtime()
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hm):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *os.environ.get("KS_NVCC_FLAGS", "").split(), "-c", src, "-o", obj]
     if verbose and src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

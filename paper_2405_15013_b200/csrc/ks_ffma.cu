@@ -25,6 +25,10 @@
 // arithmetic as the generic and streaming kernels (bit-identical results).
 #include "ks_internal.h"
 
+#ifndef KS_FFMA_MINB
+#define KS_FFMA_MINB 2      // CTAs per SM the register allocation targets (experiments: -DKS_FFMA_MINB=1)
+#endif
+
 namespace {
 
 constexpr int BK = 8;
@@ -61,7 +65,7 @@ struct Cfg {
 };
 
 template <int LAYOUT, int J, int WPJM, int WPJN, int TN>
-__global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN>::THREADS, 2)
+__global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN>::THREADS, KS_FFMA_MINB)
 ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float* __restrict__ Y,
                const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
     using C = Cfg<LAYOUT, J, WPJM, WPJN, TN>;
@@ -104,40 +108,36 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
 
     const float* kt_base = Kt + ((int64_t)i * d + j0) * c * b + k0;   // + jj*c*b + l*b + k
 
+    // Batch rows past B (last tile) load a clamped, valid row instead of a
+    // conditional zero: their outputs are never stored, and an unconditional
+    // load needs no select after it -- measured: the zero/select form made the
+    // compiler wait for the prefetch at the top of the FFMA loop (36% of the
+    // BSF kernel's stall samples on one MOV).
     auto load_tile = [&](int t) {
         const int l0 = t * BK;
         if (LAYOUT == KS_LAYOUT_BSL) {
 #pragma unroll
             for (int r = 0; r < C::A_PER_T; ++r) {
                 const int idx = tid + r * C::THREADS;
-                ra[r] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (idx < C::A_VECS) {
                     const int l = idx / (C::BMJ / 4);
                     const int n4 = idx % (C::BMJ / 4);
-                    const int64_t n = n0 + 4 * n4;
-                    if (n < B) {
-                        const int64_t s = (int64_t)i * c * d + (int64_t)(l0 + l) * d + j0;
-                        ra[r] = __ldg(reinterpret_cast<const float4*>(X + s * B + n));
-                    }
+                    const int64_t n = min(n0 + 4 * n4, B - 4);          // B % 4 == 0
+                    const int64_t s = (int64_t)i * c * d + (int64_t)(l0 + l) * d + j0;
+                    ra[r] = __ldg(reinterpret_cast<const float4*>(X + s * B + n));
                 }
             }
         } else {
 #pragma unroll
             for (int r = 0; r < C::A_PER_T; ++r) {
                 const int idx = tid + r * C::THREADS;
-                VT v;
-                if constexpr (J == 1) v = 0.f;
-                else if constexpr (J == 2) v = make_float2(0.f, 0.f);
-                else v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (idx < C::A_VECS) {
                     const int n = idx % C::BMJ;
                     const int l = idx / C::BMJ;
-                    if (n0 + n < B) {
-                        const float* p = X + (n0 + n) * N + (int64_t)i * c * d + (int64_t)(l0 + l) * d + j0;
-                        v = __ldg(reinterpret_cast<const VT*>(p));
-                    }
+                    const int64_t nn = min(n0 + n, B - 1);
+                    const float* p = X + nn * N + (int64_t)i * c * d + (int64_t)(l0 + l) * d + j0;
+                    rv[r] = __ldg(reinterpret_cast<const VT*>(p));
                 }
-                rv[r] = v;
             }
         }
 #pragma unroll
