@@ -44,6 +44,10 @@ def parse_args(argv=None):
     ap.add_argument("--workload", default="fft",
                     choices=["fft", "tiny", "vit_up", "vit_down", "gpt2_down", "gpt2_up"])
     ap.add_argument("--layout", choices=["bsf", "bsl"], default="bsf")
+    ap.add_argument("--math", choices=["fp32", "tf32", "f32x3"], default="fp32",
+                    help="per-factor math: FP32 CUDA cores (default), TF32 or 3xTF32 on tcgen05")
+    ap.add_argument("--no-baselines", action="store_true",
+                    help="skip the bmm+permute / dense cuBLAS timing of the same chain")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch override")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -179,6 +183,11 @@ def run_ours(args):
     lay = args.layout
     K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
     facs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    math_id = {"fp32": None, "tf32": ksb.MATH_TF32, "f32x3": ksb.MATH_F32X3}[args.math]
+    if math_id is not None:
+        for f in facs:
+            f.set_math(math_id)
+    tol = 5e-3 if args.math == "tf32" else 1e-5          # north star: 1e-5 FP32, 5e-3 TF32 (normwise, R9)
     dims = [pats[-1][0] * pats[-1][2] * pats[-1][3]] + [p[0] * p[1] * p[3] for p in reversed(pats)]
     X_host = ksgen.x_normal(B, dims[0], seed=rank)
     X_host_l = X_host if lay == "bsf" else ksgen.to_bsl(X_host)
@@ -351,7 +360,7 @@ def run_ours(args):
             ref = oracle.chain(pats, K4s, Xr, rows=vrows)
             errs.append(oracle.normwise_error(part.cpu().numpy(), ref))
         verify = {"rows_per_rank": len(vrows), "ranks": world, "max_normwise_err": max(errs),
-                  "tolerance": 1e-5, "ok": bool(max(errs) <= 1e-5)}
+                  "tolerance": tol, "ok": bool(max(errs) <= tol)}
 
     peaks, src = measured_peaks()
     peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
@@ -361,11 +370,12 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(tot_ms_max / K, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {"fp32": "f32", "tf32": "tf32 (fp32 accumulate)", "f32x3": "3xtf32 (fp32-accurate)"}[args.math],
         "data": "synthetic (X ~ N(0,1), K ~ U[-1/sqrt(c),1/sqrt(c)], PAPER.md:1220), seeded",
         "config": {"workload": wl["name"], "baseline_config_index": wl["cfg_index"],
                    "patterns": [list(p) for p in pats], "batch_per_gpu": B, "global_batch": B * world,
-                   "layout": lay, "parallelism": f"batch-partitioned x{world}, no collective",
+                   "layout": lay, "math": args.math, "parallelism": f"batch-partitioned x{world}, no collective",
                    "l2": "flushed between timed steps (2x L2 write, untimed)",
                    "bytes_per_step_per_gpu": step_bytes},
         "hbm_frac_of_" + src: round(value / world / peak, 4),
@@ -387,6 +397,8 @@ def run_ours(args):
         "plans": plans,
     }
     line["verify"] = verify
+    if not args.no_baselines:
+        line["baselines"] = chain_baselines(pats, K4s, X, lay, args.math, flush, stream, tot_ms_max / K, dev)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(pats, K4s, X_host, B, budget_s=15.0)
     if not args.no_sweep and world == 1:
@@ -423,6 +435,64 @@ def cpu_baseline(pats, K4s, X_host, B, budget_s=15.0):
     return {"value": round(byts / dt / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{R} of {B} batch rows of the workload, FP64 naive dense triple loop (oracle/ks_oracle.c)",
             "seconds": round(dt, 3)}
+
+
+def chain_baselines(pats, K4s, X, lay, math, flush, stream, ks_ms, dev, reps=10):
+    """The same chain through the paper's bmm+permute listing (App. A,
+    PAPER.md:813-832, one bmm + two permutation copies per factor) and through
+    one dense cuBLAS GEMM with the collapsed product W = K_1...K_L (PAPER.md:
+    892-897), same inputs, L2 flushed before every rep, median.
+    Timing only: the library never calls these."""
+    import numpy as np
+    import torch
+    from bench_sweep import bmm_bsf, bmm_bsl
+    torch.backends.cuda.matmul.allow_tf32 = (math == "tf32")   # f32x3 vs true-FP32 baselines
+    Kbs = [torch.from_numpy(k.transpose(0, 3, 1, 2).reshape(p[0] * p[3], p[1], p[2]).copy()).to(dev)
+           for p, k in zip(pats, K4s)]
+    bfn = bmm_bsf if lay == "bsf" else bmm_bsl
+
+    def bmm_chain():
+        Z = X
+        for p, Kb in zip(reversed(pats), reversed(Kbs)):
+            Z = bfn(Z, Kb, *p)
+        return Z
+
+    def dense_of(p, k):
+        a, b, c, d = p
+        D = np.zeros((a * b * d, a * c * d), dtype=np.float64)
+        for i in range(a):
+            for j in range(d):
+                D[np.ix_(i * b * d + np.arange(b) * d + j, i * c * d + np.arange(c) * d + j)] = k[i, :, :, j]
+        return D
+    W = torch.from_numpy(dense_of(pats[0], K4s[0])).to(dev)
+    for p, k in zip(pats[1:], K4s[1:]):
+        W = W @ torch.from_numpy(dense_of(p, k)).to(dev)          # FP64 product on the device
+    Wt = W.float().contiguous()
+    del W
+
+    def dense():
+        return X @ Wt.t() if lay == "bsf" else Wt @ X
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for r in range(reps):
+            flush.fill_(r & 0xFF)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            fn()
+            s1.record(stream)
+            s1.synchronize()
+            ts.append(s0.elapsed_time(s1))
+        return float(np.median(ts))
+    t_bmm, t_dense = timeit(bmm_chain), timeit(dense)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return {"bmm_permute_ms": round(t_bmm, 5), "dense_cublas_ms": round(t_dense, 5),
+            "speedup_vs_bmm_permute": round(t_bmm / ks_ms, 4), "speedup_vs_dense": round(t_dense / ks_ms, 4),
+            "allow_tf32": math == "tf32",
+            "note": "same chain, same inputs: paper's bmm+permute listing per factor (App. A) and one dense "
+                    "cuBLAS GEMM with W = K_1...K_L; median of 10 L2-flushed reps"}
 
 
 # --------------------------------------------------------- reference arm ----
