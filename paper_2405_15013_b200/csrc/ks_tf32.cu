@@ -363,42 +363,59 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 }
 
 // ==========================================================================
-// BSF with d % 4 == 0: J = 4 consecutive j per tile.  In BSF the 4 values
-// X[n, i*c*d + l*d + j0 .. j0+3] are one 16-byte vector, so a TMA 3-D box
-// {4 j, 16 l, 128 n} of X viewed as [B][a*c][d] gathers the d-strided columns
-// of 4 KS blocks at once with full 16-byte vectors (SURVEY §7 hard part 1).
-// Transposer warps split the staged [n][l][j] chunk into four K-major
-// 64-byte-swizzled A tiles (one per j); the MMA warp runs 4 accumulators
-// (4 x BN <= 256 TMEM columns, double-buffered); the epilogue stores through
-// warp_store_rows (coalesced 16-byte units; measured on the half variant: the
-// direct per-row float4 stores touched 32 sectors per instruction, 4x ideal,
-// and made the epilogue the bottleneck).
+// BSF with d > 1: J j-values per tile.  In BSF the d-strided columns of the
+// blocks (i, j0 .. j0+J-1) are gathered by ONE TMA box per pipeline stage:
+//   J = d (d <= 8): the BKJ*d values X[n, (i*c + l0)*d .. (i*c + l0 + BKJ)*d)
+//       of every row are one contiguous run -> 2-D box {BKJ*d + 4, 128 n}: every
+//       loaded byte is used (the 4 extra floats are padding, see below);
+//   J = 4 or 8 (d % J == 0, d > 8): 3-D box {J j, BKJ+1 l, 128 n} of X viewed
+//       as [B][a*c][d]: 4*J-byte runs (J = 4 reads half of each 32-byte sector,
+//       the other half belongs to the next j-group, which runs next and hits L2).
+// Either way a staged row n is [BKJ l][J j] floats plus 16 bytes, so its pitch
+// is an odd number of 16-byte units and the transposers' 16-byte reads of 8
+// consecutive rows hit 8 different bank groups.  Transposer warps split the
+// staged chunk into J K-major A tiles (SWIZZLE_32B for BKJ = 8, 64B for 16);
+// the MMA warp runs J accumulators of BN columns (NACC x J x BN <= 512 TMEM
+// columns; NACC = 2 double-buffers the accumulators so the epilogue overlaps
+// the next tile, NACC = 1 lets BN cover the whole block so X is read once --
+// the ring of S stages keeps prefetching while the epilogue drains).  The
+// epilogue stores through warp_store_rows (coalesced 16-byte units; direct
+// per-row stores touched 32 sectors per instruction, 4x ideal).
 // ==========================================================================
-constexpr int JJ = 4;
-
-// X3 (3xTF32) halves the l per stage (8: one MMA k-step, 32-byte SWIZZLE_32B
-// rows) so that the doubled A and B tiles still leave a 2-deep pipeline.
-template <int BN, bool X3 = false>
+template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false>
 struct Tf32JCfg {
-    static constexpr int BKJ = X3 ? 8 : 16;               // l per stage
     static constexpr int RB = BKJ * 4;                    // operand row bytes (SW32 / SW64)
     static constexpr int NA = X3 ? 2 : 1;                 // hi (+ lo) tiles
     static constexpr int AJ_TILE = BM * RB;               // per j
     static constexpr int BJ_TILE = BN * RB;
-    static constexpr int SLOT = JJ * NA * (AJ_TILE + BJ_TILE);
-    static constexpr int STG_ROW = (BKJ + 1) * JJ * 4;    // box {4 j, BKJ+1 l, 128 n}: 1 l of padding
-    static constexpr int STG = BM * STG_ROW;              // (odd number of 16-byte units per row)
-    static constexpr int P = 2;
-    static constexpr int SCR = 4 * WarpStore<float, JJ, 16>::BYTES;    // epilogue store scratch
-    static constexpr int S_FIT = (212 * 1024 - P * STG - SCR) / SLOT;
-    static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
+    static constexpr int SLOT = J * NA * (AJ_TILE + BJ_TILE);
+    // staged row: [BKJ l][J j] + padding: 4 floats past the run (2-D box), or one
+    // more l (3-D box; J = 8 then gives an even pitch: 2-way read conflicts)
+    static constexpr int STG_ROW = GATHER ? (BKJ + 1) * J * 4 : BKJ * J * 4 + 16;
+    static constexpr int STG = BM * STG_ROW;
+    static constexpr int NACC = 2 * J * BN <= 512 ? 2 : 1;
+    static constexpr int EC = J > 2 ? 8 : 16;             // epilogue columns per TMEM load
+    static constexpr int SCR = 4 * WarpStore<float, J, EC>::BYTES;    // epilogue store scratch
+    // X staging ring: ~96 KB of X loads in flight per SM (Little's law: ~45 GB/s
+    // per SM x ~2 us loaded latency), leaving room for 2 operand slots; measured:
+    // P = 2 at BKJ = 8 (36 KB in flight) left the J = 3 kernel latency-bound.
+    static constexpr int P_WANT = (96 * 1024 + STG - 1) / STG;
+    static constexpr int P_ROOM = (214 * 1024 - 2 * SLOT - SCR) / STG;
+    static constexpr int P_MIN = P_WANT < P_ROOM ? P_WANT : P_ROOM;
+    static constexpr int P = P_MIN < 2 ? 2 : P_MIN > 8 ? 8 : P_MIN;
+    static constexpr int S_FIT = (214 * 1024 - P * STG - SCR) / SLOT;
+    static constexpr int S = S_FIT > 6 ? 6 : S_FIT;
     static constexpr int SCR_OFF = S * SLOT + P * STG;
     static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
+    static constexpr int COLS = NACC * J * BN;
+    static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
     static_assert(SMEM <= 227 * 1024, "shared memory");
-    static constexpr int TMEM_COLS = 2 * JJ * BN <= 256 ? 256 : 512;
-    static_assert(JJ * BN <= 256 && BN % 16 == 0, "4 accumulators, double-buffered");
+    static_assert(J * BN <= 512 && BN % 16 == 0 && BN <= 256, "J accumulators in TMEM");
+    static_assert(BKJ == 8 || BKJ == 16, "SW32 / SW64 operand rows");
+    static_assert((BKJ * J) % 4 == 0, "whole 16-byte staging reads");
     static_assert(S >= 2, "pipeline too shallow");
+    static_assert((2 * S + 2 * NACC + 2 * P) * 8 + 4 <= 256, "barrier area");
 };
 
 template <int RB>
@@ -411,7 +428,7 @@ struct TileJ {
     int i, j0, k0, n0;
 };
 
-__device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_t nnb, int BN, int J = JJ) {
+__device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_t nnb, int BN, int J) {
     TileJ t;
     t.k0 = (int)(tile % nkc) * BN;
     tile /= nkc;
@@ -422,41 +439,42 @@ __device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_
     return t;
 }
 
-template <int BN, bool X3 = false>
+template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     const __grid_constant__ CUtensorMap kmap_lo, float* __restrict__ Y,
                     const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles) {
-    using C = Tf32JCfg<BN, X3>;
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER>;
     constexpr int S = C::S;
     constexpr int P = C::P;
-    constexpr int BKJ = C::BKJ;
     constexpr int RB = C::RB;
+    constexpr int NACC = C::NACC;
     constexpr int NCH = RB / 16;                  // 16-byte chunks per A row
+    constexpr int NV = BKJ * J / 4;               // 16-byte staging reads per row
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     const uint32_t full0 = smem_u32(&bars[0]);
     const uint32_t empty0 = smem_u32(&bars[S]);
     const uint32_t accf0 = smem_u32(&bars[2 * S]);
-    const uint32_t acce0 = smem_u32(&bars[2 * S + 2]);
-    const uint32_t sfull0 = smem_u32(&bars[2 * S + 4]);
-    const uint32_t sempty0 = smem_u32(&bars[2 * S + 4 + P]);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 4 + 2 * P]);
-    // slot: [A hi (4 j)] [A lo (4 j), X3] [B hi (4 j)] [B lo (4 j), X3]
+    const uint32_t acce0 = smem_u32(&bars[2 * S + NACC]);
+    const uint32_t sfull0 = smem_u32(&bars[2 * S + 2 * NACC]);
+    const uint32_t sempty0 = smem_u32(&bars[2 * S + 2 * NACC + P]);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[2 * S + 2 * NACC + 2 * P]);
+    // slot: [A hi (J j)] [A lo (J j), X3] [B hi (J j)] [B lo (J j), X3]
     const uint32_t slot0 = smem_u32(smem);
     const uint32_t stg0 = slot0 + S * C::SLOT;    // P x staging
     const uint32_t scr0 = slot0 + C::SCR_OFF;     // epilogue store scratch
-    constexpr int A_ALL = JJ * C::NA * C::AJ_TILE;
+    constexpr int A_ALL = J * C::NA * C::AJ_TILE;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const int nkc = b / BN;
-    const int njg = d / JJ;
+    const int njg = d / J;
     const int64_t nnb = (B + BM - 1) / BM;
     const int64_t M = (int64_t)a * b * d;
-    const int nk = c / BKJ;                       // c % 16 == 0
+    const int nk = c / BKJ;                       // c % BKJ == 0
     const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t G = my_tiles * nk;
 
@@ -465,7 +483,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             mbar_init(full0 + 8 * s, 1 + NTRANS);
             mbar_init(empty0 + 8 * s, 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NACC; ++s) {
             mbar_init(accf0 + 8 * s, 1);
             mbar_init(acce0 + 8 * s, NEPI);
         }
@@ -493,65 +511,71 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     if (warp == 0) {
         if (lane == 0) {
             auto issue_x = [&](int64_t gx) {
-                const TileJ tc = decode_j(blockIdx.x + (gx / nk) * gridDim.x, nkc, njg, nnb, BN);
+                const TileJ tc = decode_j(blockIdx.x + (gx / nk) * gridDim.x, nkc, njg, nnb, BN, J);
                 const int l0 = (int)(gx % nk) * BKJ;
                 const int p = (int)(gx % P);
                 if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
                 mbar_expect_tx(sfull0 + 8 * p, C::STG);
-                tma_3d(stg0 + p * C::STG, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
+                if constexpr (GATHER)
+                    tma_3d(stg0 + p * C::STG, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
+                else
+                    tma_2d(stg0 + p * C::STG, &xmap, (tc.i * c + l0) * d, tc.n0, sfull0 + 8 * p);
             };
             for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
             for (int64_t g = 0; g < G; ++g) {
                 if (g + P - 1 < G) issue_x(g + P - 1);
-                const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN);
+                const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
                 const int l0 = (int)(g % nk) * BKJ;
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
-                mbar_expect_tx(full0 + 8 * st, JJ * C::NA * C::BJ_TILE);
+                mbar_expect_tx(full0 + 8 * st, J * C::NA * C::BJ_TILE);
                 const uint32_t sb = slot0 + st * C::SLOT + A_ALL;
-                for (int jj = 0; jj < JJ; ++jj) {
+                for (int jj = 0; jj < J; ++jj) {
                     const int row = ((tc.i * d + tc.j0 + jj) * b) + tc.k0;
                     tma_2d(sb + jj * C::BJ_TILE, &kmap, l0, row, full0 + 8 * st);
-                    if (X3) tma_2d(sb + (JJ + jj) * C::BJ_TILE, &kmap_lo, l0, row, full0 + 8 * st);
+                    if (X3) tma_2d(sb + (J + jj) * C::BJ_TILE, &kmap_lo, l0, row, full0 + 8 * st);
                 }
             }
         }
     } else if (warp <= 4) {
-        // staging [n][l][j] (STG_ROW bytes per row n) -> 4 K-major A tiles (+ 4 lo tiles for X3)
+        // staging row r: [BKJ l][J j] floats -> J K-major A rows of BKJ l (+ J lo rows for X3)
         const int r = tid - 32;
         const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
         const int sw = RB == 64 ? (r % 8) / 2 : (r % 8) / 4;       // SW64 / SW32 chunk XOR
         for (int64_t g = 0; g < G; ++g) {
             const int p = (int)(g % P);
             mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
-            float v[BKJ][JJ];
-            // rows are BKJ+1 l long (the box carries one extra l as padding), so the 8
-            // rows of a shared-memory phase fall on 8 different 16-byte bank groups
+            float v[BKJ * J];                     // v[l * J + j]
             const uint32_t src = stg0 + p * C::STG + r * C::STG_ROW;
 #pragma unroll
-            for (int l = 0; l < BKJ; ++l)
+            for (int q = 0; q < NV; ++q)
                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(v[l][0]), "=f"(v[l][1]), "=f"(v[l][2]), "=f"(v[l][3]) : "r"(src + l * 16));
+                             : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                             : "r"(src + q * 16));
             fence_proxy_async();          // generic reads before the TMA (async proxy) refill
             mbar_arrive(sempty0 + 8 * p);
             const int st = (int)(g % S);
             if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
             const uint32_t sa = slot0 + st * C::SLOT + rowoff;
 #pragma unroll
-            for (int jj = 0; jj < JJ; ++jj)
+            for (int jj = 0; jj < J; ++jj)
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     const uint32_t off = jj * C::AJ_TILE + ((ch ^ sw) * 16);
+                    const float x0 = v[(4 * ch) * J + jj], x1 = v[(4 * ch + 1) * J + jj];
+                    const float x2 = v[(4 * ch + 2) * J + jj], x3 = v[(4 * ch + 3) * J + jj];
                     if constexpr (X3) {
                         uint32_t hi[4], lo[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) tf32_split(__float_as_uint(v[4 * ch + e][jj]), hi[e], lo[e]);
+                        tf32_split(__float_as_uint(x0), hi[0], lo[0]);
+                        tf32_split(__float_as_uint(x1), hi[1], lo[1]);
+                        tf32_split(__float_as_uint(x2), hi[2], lo[2]);
+                        tf32_split(__float_as_uint(x3), hi[3], lo[3]);
                         sts128(sa + off, __uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(hi[2]),
                                __uint_as_float(hi[3]));
-                        sts128(sa + JJ * C::AJ_TILE + off, __uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                        sts128(sa + J * C::AJ_TILE + off, __uint_as_float(lo[0]), __uint_as_float(lo[1]),
                                __uint_as_float(lo[2]), __uint_as_float(lo[3]));
                     } else {
-                        sts128(sa + off, v[4 * ch][jj], v[4 * ch + 1][jj], v[4 * ch + 2][jj], v[4 * ch + 3][jj]);
+                        sts128(sa + off, x0, x1, x2, x3);
                     }
                 }
             fence_proxy_async();
@@ -562,8 +586,8 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             constexpr uint32_t idesc = make_idesc(BN);
             int64_t g = 0, it = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-                const int ab = (int)(it & 1);
-                if (it >= 2) mbar_wait(acce0 + 8 * ab, (uint32_t)(((it / 2) - 1) & 1));
+                const int ab = (int)(it % NACC);
+                if (it >= NACC) mbar_wait(acce0 + 8 * ab, (uint32_t)(((it / NACC) - 1) & 1));
                 tc_fence_after();
                 for (int t = 0; t < nk; ++t, ++g) {
                     const int st = (int)(g % S);
@@ -572,15 +596,15 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     const uint32_t sa = slot0 + st * C::SLOT;
                     const uint32_t sb = sa + A_ALL;
 #pragma unroll
-                    for (int jj = 0; jj < JJ; ++jj) {
-                        const uint32_t dtm = tmem + (uint32_t)((ab * JJ + jj) * BN);
+                    for (int jj = 0; jj < J; ++jj) {
+                        const uint32_t dtm = tmem + (uint32_t)((ab * J + jj) * BN);
 #pragma unroll
                         for (int s = 0; s < BKJ / 8; ++s) {
                             const uint32_t acc = (t > 0 || s > 0) ? 1u : 0u;
                             const uint32_t ah = sa + jj * C::AJ_TILE + 32 * s, bh = sb + jj * C::BJ_TILE + 32 * s;
                             if constexpr (X3) {    // x_lo k_hi + x_hi k_lo + x_hi k_hi
-                                mma_tf32(dtm, kmajor_desc_j<RB>(ah + JJ * C::AJ_TILE), kmajor_desc_j<RB>(bh), idesc, acc);
-                                mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh + JJ * C::BJ_TILE), idesc, 1u);
+                                mma_tf32(dtm, kmajor_desc_j<RB>(ah + J * C::AJ_TILE), kmajor_desc_j<RB>(bh), idesc, acc);
+                                mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh + J * C::BJ_TILE), idesc, 1u);
                                 mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh), idesc, 1u);
                             } else {
                                 mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh), idesc, acc);
@@ -594,32 +618,37 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         }
         __syncwarp();
     } else {
+        constexpr int EC = C::EC;
         const int lq = warp & 3;
         int64_t it = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-            const TileJ tc = decode_j(tile, nkc, njg, nnb, BN);
-            const int ab = (int)(it & 1);
-            mbar_wait(accf0 + 8 * ab, (uint32_t)((it / 2) & 1));
+            const TileJ tc = decode_j(tile, nkc, njg, nnb, BN, J);
+            const int ab = (int)(it % NACC);
+            mbar_wait(accf0 + 8 * ab, (uint32_t)((it / NACC) & 1));
             tc_fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * JJ * BN);
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * J * BN);
 #pragma unroll 1
-            for (int col = 0; col < BN; col += 16) {
-                float v[JJ][16];
+            for (int col = 0; col < BN; col += EC) {
+                float v[J][EC];
 #pragma unroll
-                for (int jj = 0; jj < JJ; ++jj) tmem_ld16(tbase + jj * BN + col, v[jj]);
+                for (int jj = 0; jj < J; ++jj) {
+                    if constexpr (EC == 16) tmem_ld16(tbase + jj * BN + col, v[jj]);
+                    else tmem_ld8(tbase + jj * BN + col, v[jj]);
+                }
                 const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
+                if (col + EC >= BN) {             // last TMEM read of this tile: free the accumulator early
+                    tc_fence_before();
+                    mbar_arrive(acce0 + 8 * ab);
+                }
                 if (bias) {                       // KSLinear bias (NEXT-2)
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + r0 + (int64_t)e * d));
-                        v[0][e] += bb.x; v[1][e] += bb.y; v[2][e] += bb.z; v[3][e] += bb.w;
-                    }
+                    for (int e = 0; e < EC; ++e)
+#pragma unroll
+                        for (int jj = 0; jj < J; ++jj) v[jj][e] += __ldg(bias + r0 + (int64_t)e * d + jj);
                 }
-                warp_store_rows<float, JJ, 16>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, JJ, 16>::BYTES, v, Y,
-                                               (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                warp_store_rows<float, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, J, EC>::BYTES, v, Y,
+                                              (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
             }
-            tc_fence_before();
-            mbar_arrive(acce0 + 8 * ab);
         }
     }
     tc_fence_before();
@@ -915,39 +944,85 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
-int pick_bn_j(int64_t b) {
-    for (int bn : {64, 48, 32, 16})
-        if (b % bn == 0) return bn;
-    return 0;
+// ---- TF32 BSF, d > 1 (ks_tf32_bsfj_kernel): plan = (J, BN, gather) ----------
+// J = d for d <= 8 (contiguous 2-D box), else J = 8 (b <= 64) or 4 (3-D gather,
+// d % J == 0).  BN = the largest tile width dividing b with J x BN <= 512 TMEM
+// columns: modelled L2->SM reads per X byte = (b / BN) x (J = 4 gather ? 2 : 1),
+// so a whole-block BN (single-buffered accumulators) beats a split BN.
+struct BsfjPlan {
+    int J = 0, BN = 0;
+    bool gather = false;
+};
+// 3xTF32 doubles every operand tile: J <= 4 there (d = 6 runs FFMA).
+BsfjPlan pick_bsfj(const ks_handle_s& h) {
+    BsfjPlan p;
+    const bool x3 = h.math == KS_MATH_F32X3;
+    if (h.c % 16 != 0) return p;
+    if (h.d >= 2 && h.d <= (x3 ? 4 : 8) && h.d != 5 && h.d != 7) {
+        p.J = (int)h.d;
+    } else if (!x3 && h.d > 8 && h.d % 8 == 0 && h.b <= 64) {
+        p.J = 8;
+        p.gather = true;
+    } else if (h.d > (x3 ? 4 : 8) && h.d % 4 == 0) {
+        p.J = 4;
+        p.gather = true;
+    } else {
+        return p;
+    }
+    for (int bn : {128, 96, 64, 48, 32, 16})
+        if (h.b % bn == 0 && p.J * bn <= 512) {
+            p.BN = bn;
+            break;
+        }
+    if (p.BN == 0) p.J = 0;
+    return p;
 }
 
-template <int BN, bool X3 = false>
+// l per stage: 16 (SWIZZLE_64B rows, half the padding / barrier traffic per
+// byte) when 2 operand slots and >= 64 KB of X staging fit, else 8 (SWIZZLE_32B).
+template <int J, int BN, bool X3, bool GATHER>
+constexpr int bsfj_bkj() {
+    constexpr int NA = X3 ? 2 : 1;
+    constexpr int slot16 = J * NA * (BM + BN) * 64;
+    constexpr int stg16 = BM * (GATHER ? 17 * J * 4 : 16 * J * 4 + 16);
+    constexpr int scr = 4 * WarpStore<float, J, (J > 2 ? 8 : 16)>::BYTES;
+    constexpr int p16 = stg16 >= 32 * 1024 ? 2 : (64 * 1024 + stg16 - 1) / stg16;
+    return 214 * 1024 - p16 * stg16 - scr >= 2 * slot16 ? 16 : 8;
+}
+
+template <int J, int BN, bool X3, bool GATHER>
 cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
-    using C = Tf32JCfg<BN, X3>;
+    constexpr int BKJ = bsfj_bkj<J, BN, X3, GATHER>();
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER>;
     constexpr CUtensorMapSwizzle SW = C::RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUtensorMap xmap, kmap, kmap_lo;
     {
         const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
         const cuuint64_t ks[1] = {(cuuint64_t)h.c * 4};
-        const cuuint32_t kb[2] = {(cuuint32_t)C::BKJ, BN};
+        const cuuint32_t kb[2] = {(cuuint32_t)BKJ, BN};
         if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, SW)) return cudaErrorInvalidValue;
         kmap_lo = kmap;
         if (X3 && !encode(&kmap_lo, h.k_lo, 2, kd, ks, kb, SW)) return cudaErrorInvalidValue;
     }
-    {
+    if (GATHER) {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
-        const cuuint32_t xb[3] = {JJ, (cuuint32_t)C::BKJ + 1, BM};
+        const cuuint32_t xb[3] = {(cuuint32_t)J, (cuuint32_t)BKJ + 1, BM};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    } else {
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
+        const cuuint32_t xb[2] = {(cuuint32_t)(BKJ * J + 4), BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_bsfj_kernel<BN, X3>;
+    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         attr[h.device & 63] = true;
     }
-    const int64_t ntiles = (h.b / BN) * (h.d / JJ) * ((call.B + BM - 1) / BM) * h.a;
+    const int64_t ntiles = (h.b / BN) * (h.d / J) * ((call.B + BM - 1) / BM) * h.a;
     int64_t slots = (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
@@ -958,18 +1033,41 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
-template <bool X3>
-cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
-    switch (pick_bn_j(h.b)) {
-        case 64: return launch_bsfj<64, X3>(h, call);
-        case 48: return launch_bsfj<48, X3>(h, call);
-        case 32: return launch_bsfj<32, X3>(h, call);
-        case 16: return launch_bsfj<16, X3>(h, call);
+template <int J, bool X3, bool GATHER>
+cudaError_t launch_bsfj_bn(const ks_handle_s& h, const KsCall& call, int BN) {
+    switch (BN) {
+        case 128: if constexpr (J * 128 <= 512) return launch_bsfj<J, 128, X3, GATHER>(h, call); break;
+        case 96: if constexpr (J * 96 <= 512) return launch_bsfj<J, 96, X3, GATHER>(h, call); break;
+        case 64: return launch_bsfj<J, 64, X3, GATHER>(h, call);
+        case 48: return launch_bsfj<J, 48, X3, GATHER>(h, call);
+        case 32: return launch_bsfj<J, 32, X3, GATHER>(h, call);
+        case 16: return launch_bsfj<J, 16, X3, GATHER>(h, call);
     }
     return cudaErrorInvalidValue;
 }
 
-bool bsfj_ok(const ks_handle_s& h) { return h.d % JJ == 0 && h.c % 16 == 0 && pick_bn_j(h.b) != 0; }
+template <bool X3>
+cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
+    const BsfjPlan p = pick_bsfj(h);
+    if (p.gather) {
+        if (p.J == 4) return launch_bsfj_bn<4, X3, true>(h, call, p.BN);
+        if constexpr (!X3)
+            if (p.J == 8) return launch_bsfj_bn<8, X3, true>(h, call, p.BN);
+        return cudaErrorInvalidValue;
+    }
+    switch (p.J) {
+        case 2: return launch_bsfj_bn<2, X3, false>(h, call, p.BN);
+        case 3: return launch_bsfj_bn<3, X3, false>(h, call, p.BN);
+        case 4: return launch_bsfj_bn<4, X3, false>(h, call, p.BN);
+    }
+    if constexpr (!X3) {
+        if (p.J == 6) return launch_bsfj_bn<6, X3, false>(h, call, p.BN);
+        if (p.J == 8) return launch_bsfj_bn<8, X3, false>(h, call, p.BN);
+    }
+    return cudaErrorInvalidValue;
+}
+
+bool bsfj_ok(const ks_handle_s& h) { return pick_bsfj(h).J != 0; }
 
 // Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
 int pick_j_half(int64_t d) {
@@ -1074,9 +1172,9 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (xa & 15) return false;                                   // TMA global address
     if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0 && (ya & 3) == 0;
     if (ya & 15) return false;
-    // BSF: d = 1 direct; d % 4 == 0 four-j gather (its bias loads are 16-byte vectors)
+    // BSF: d = 1 direct; d > 1 J-column gather (pick_bsfj; bias read as scalars)
     if (h.math == KS_MATH_F32X3 && !h.k_lo) return false;
-    return h.d == 1 || (bsfj_ok(h) && (reinterpret_cast<uintptr_t>(call.bias) & 15) == 0);
+    return h.d == 1 || bsfj_ok(h);
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {

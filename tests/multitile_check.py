@@ -16,7 +16,7 @@ if os.environ.get("KS_MULTITILE_MATH") == "f32x3":
     worst = 0.0
     for p, lay, B in [((1, 64, 64, 4), "bsl", 1024), ((1, 64, 64, 1), "bsf", 1024), ((2, 96, 96, 1), "bsl", 772),
                       ((2, 128, 128, 1), "bsf", 900), ((1, 48, 48, 3), "bsl", 516), ((1, 64, 64, 4), "bsf", 1024),
-                      ((2, 48, 48, 8), "bsf", 512)]:
+                      ((2, 48, 48, 8), "bsf", 512), ((1, 128, 128, 3), "bsf", 700), ((2, 64, 64, 2), "bsf", 600)]:
         M, N, _ = O.dims(p)
         K4 = ksgen.k4_uniform(*p, seed=3)
         X = ksgen.x_normal(B, N, seed=4)
@@ -33,7 +33,8 @@ if os.environ.get("KS_MULTITILE_MATH") == "f32x3":
 worst = 0.0
 for p, lay, B in [((1, 64, 64, 4), "bsf", 1024), ((1, 64, 64, 4), "bsl", 1024), ((1, 64, 64, 1), "bsf", 1024),
                   ((2, 48, 48, 8), "bsf", 512), ((1, 128, 128, 8), "bsf", 512), ((2, 96, 96, 1), "bsl", 772),
-                  ((1, 256, 64, 16), "bsf", 300)]:
+                  ((1, 256, 64, 16), "bsf", 300), ((1, 128, 128, 3), "bsf", 700), ((1, 128, 128, 12), "bsf", 600),
+                  ((2, 64, 64, 16), "bsf", 520), ((1, 96, 96, 6), "bsf", 400), ((1, 768, 192, 2), "bsf", 300)]:
     M, N, _ = O.dims(p)
     K4 = ksgen.k4_uniform(*p, seed=3)
     X = ksgen.x_normal(B, N, seed=4)

@@ -23,7 +23,8 @@ def to_dev(a):
 
 
 FAMILIES = [((2, 3, 2, 3), "generic", "fp32"), ((4, 2, 2, 8), "stream", "fp32"), ((2, 64, 48, 4), "ffma", "fp32"),
-            ((1, 64, 64, 1), "tf32", "tf32"), ((2, 48, 48, 8), "tf32", "tf32"), ((1, 128, 128, 3), "tf32", "tf32")]
+            ((1, 64, 64, 1), "tf32", "tf32"), ((2, 48, 48, 8), "tf32", "tf32"), ((1, 128, 128, 3), "tf32", "tf32"),
+            ((1, 64, 48, 16), "tf32", "tf32"), ((1, 128, 128, 12), "tf32", "tf32")]
 
 
 @pytest.mark.parametrize("p,family,math", FAMILIES)
@@ -38,8 +39,6 @@ def test_matmul_bias(ksb, p, family, math, layout):
     if math == "tf32":
         f.set_math(ksb.MATH_TF32)
     plan = f.plan(B, layout)
-    if family == "tf32" and layout == "bsf" and p[3] not in (1,) and p[3] % 4:
-        pytest.skip("TF32 BSF needs d == 1 or d % 4 == 0")
     assert plan == family, plan
     Xd = to_dev(X if layout == "bsf" else ksgen.to_bsl(X))
     Y = ksb.matmul(f, Xd, layout=layout, bias=to_dev(bias))

@@ -49,9 +49,10 @@ CASES = [((1, 48, 48, 1), "bsf"), ((1, 64, 64, 1), "bsf"), ((2, 128, 128, 1), "b
          ((64, 64, 64, 1), "bsf"), ((1, 16, 24, 1), "bsf"), ((2, 96, 96, 1), "bsf"),
          ((1, 768, 192, 2), "bsl"), ((1, 256, 64, 16), "bsl"), ((1, 48, 48, 64), "bsl"), ((3, 96, 96, 4), "bsl"),
          ((1, 128, 128, 3), "bsl"), ((2, 16, 24, 3), "bsl"), ((6, 64, 64, 1), "bsl"), ((1, 320, 40, 2), "bsl"),
-         # BSF, d % 4 == 0: four-j gather, 8 l per stage (SWIZZLE_32B)
+         # BSF, d > 1: J = d contiguous (d <= 4), four-j gather (d % 4 == 0, d > 4)
          ((1, 64, 64, 4), "bsf"), ((2, 48, 48, 16), "bsf"), ((1, 128, 128, 8), "bsf"), ((3, 96, 96, 4), "bsf"),
-         ((2, 16, 32, 12), "bsf"), ((1, 256, 64, 16), "bsf")]
+         ((2, 16, 32, 12), "bsf"), ((1, 256, 64, 16), "bsf"), ((1, 128, 128, 3), "bsf"), ((2, 48, 48, 2), "bsf"),
+         ((1, 768, 192, 2), "bsf")]
 
 
 @pytest.mark.parametrize("p,layout", CASES)
@@ -84,8 +85,8 @@ def test_f32x3_integer_bit_exact_with_bias(ksb, p, layout):
     assert np.array_equal(Y.astype(np.float64), O.matmul(p, K4, X) + bias[None, :].astype(np.float64))
 
 
-def test_f32x3_bsf_d_not_multiple_of_4_runs_fp32_cuda_cores(ksb):
-    p = (2, 48, 48, 3)
+def test_f32x3_bsf_d6_runs_fp32_cuda_cores(ksb):
+    p = (2, 48, 48, 6)
     f = ksb.Factor(*p, ksgen.k4_uniform(*p, seed=5)).set_math(ksb.MATH_F32X3)
     assert f.plan(256, "bsf") == "ffma"
     assert f.plan(256, "bsl") == "tf32"

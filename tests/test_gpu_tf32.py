@@ -45,9 +45,12 @@ CASES = [((1, 48, 48, 1), "bsf"), ((1, 64, 64, 1), "bsf"), ((2, 128, 128, 1), "b
          ((6, 64, 64, 1), "bsf"), ((6, 64, 256, 1), "bsf"), ((64, 64, 64, 1), "bsf"), ((1, 256, 64, 16), "bsl"),
          ((1, 48, 48, 64), "bsl"), ((3, 96, 96, 4), "bsl"), ((1, 128, 128, 3), "bsl"), ((2, 16, 24, 3), "bsl"),
          ((1, 16, 16, 1), "bsf"), ((1, 320, 40, 2), "bsl"), ((2, 96, 96, 1), "bsl"), ((6, 64, 64, 1), "bsl"),
-         # BSF, d % 4 == 0: four-j TMA gather
+         # BSF, d > 1: J = d contiguous 2-D box (d <= 8), J = 8 / 4 3-D gather (d > 8)
          ((1, 64, 64, 4), "bsf"), ((2, 48, 48, 16), "bsf"), ((1, 128, 128, 8), "bsf"), ((3, 96, 96, 4), "bsf"),
-         ((1, 64, 256, 16), "bsf"), ((1, 256, 64, 16), "bsf"), ((2, 16, 32, 12), "bsf")]
+         ((1, 64, 256, 16), "bsf"), ((1, 256, 64, 16), "bsf"), ((2, 16, 32, 12), "bsf"),
+         ((1, 768, 192, 2), "bsf"), ((1, 128, 128, 3), "bsf"), ((2, 48, 48, 6), "bsf"), ((1, 96, 96, 6), "bsf"),
+         ((1, 128, 128, 12), "bsf"), ((1, 64, 64, 32), "bsf"), ((2, 96, 96, 16), "bsf"), ((1, 320, 48, 2), "bsf"),
+         ((3, 48, 64, 2), "bsf"), ((1, 112, 32, 3), "bsf"), ((2, 64, 48, 8), "bsf")]
 
 
 @pytest.mark.parametrize("p,layout", CASES)
@@ -71,7 +74,8 @@ def test_tf32_matches_oracle(ksb, p, layout):
 
 
 @pytest.mark.parametrize("p,layout", [((1, 64, 64, 1), "bsf"), ((2, 48, 32, 3), "bsl"), ((64, 64, 64, 1), "bsf"),
-                                      ((1, 256, 64, 16), "bsl")])
+                                      ((1, 256, 64, 16), "bsl"), ((2, 48, 32, 3), "bsf"), ((1, 128, 64, 6), "bsf"),
+                                      ((1, 64, 64, 16), "bsf"), ((1, 128, 128, 12), "bsf")])
 def test_tf32_integer_bit_exact(ksb, p, layout):
     M, N, _ = O.dims(p)
     K4 = ksgen.k4_int(*p, seed=2001)
@@ -91,22 +95,27 @@ def test_tf32_ragged_batches(ksb, B):
     assert O.normwise_error(Yt, O.matmul(p, K4, X)) <= TF32_TOL
 
 
+@pytest.mark.parametrize("layout", ["bsl", "bsf"])
 @pytest.mark.parametrize("name", ["VIT_UP", "VIT_DOWN", "GPT2_DOWN", "GPT2_UP"])
-def test_tf32_model_chains_bsl(ksb, name):
+def test_tf32_model_chains(ksb, name, layout):
     pats = getattr(configs, name)
     K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
     N = configs.chain_dims(pats)[0]
     B = 256
     X = ksgen.x_normal(B, N, seed=0)
     fs = [ksb.Factor(*p, k).set_math(ksb.MATH_TF32) for p, k in zip(pats, K4s)]
-    Y = ksb.chain(fs, to_dev(ksgen.to_bsl(X)), layout="bsl")
+    assert all(f.plan(B, layout) == "tf32" for f in fs)
+    Y = ksb.chain(fs, to_dev(ksgen.to_bsl(X) if layout == "bsl" else X), layout=layout)
     torch.cuda.synchronize()
-    err = O.normwise_error(Y.cpu().numpy().T, O.chain(pats, K4s, X))
+    Yh = Y.cpu().numpy().T if layout == "bsl" else Y.cpu().numpy()
+    err = O.normwise_error(Yh, O.chain(pats, K4s, X))
     assert err <= TF32_TOL, err
 
 
 @pytest.mark.parametrize("p,layout", [((1, 128, 128, 64), "bsl"), ((4, 64, 64, 16), "bsl"), ((1, 96, 96, 1), "bsl"),
-                                      ((1, 128, 128, 64), "bsf"), ((4, 64, 64, 16), "bsf"), ((1, 96, 96, 1), "bsf")])
+                                      ((1, 128, 128, 64), "bsf"), ((4, 64, 64, 16), "bsf"), ((1, 96, 96, 1), "bsf"),
+                                      ((1, 128, 128, 3), "bsf"), ((1, 96, 96, 6), "bsf"), ((1, 48, 48, 2), "bsf"),
+                                      ((3, 64, 64, 16), "bsf")])
 def test_tf32_sweep_full_size_sampled_rows(ksb, p, layout):
     """configs[2] at B = 25088, TF32, both layouts, in bench's launch configuration."""
     B = configs.SWEEP_BATCH
