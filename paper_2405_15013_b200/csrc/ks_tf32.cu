@@ -443,7 +443,8 @@ template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     const __grid_constant__ CUtensorMap kmap_lo, float* __restrict__ Y,
-                    const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles) {
+                    const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles,
+                    int dbg) {
     using C = Tf32JCfg<J, BN, BKJ, X3, GATHER>;
     constexpr int S = C::S;
     constexpr int P = C::P;
@@ -547,11 +548,16 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
             float v[BKJ * J];                     // v[l * J + j]
             const uint32_t src = stg0 + p * C::STG + r * C::STG_ROW;
+            if (dbg & 2) {                // profiling experiment: skip the staging reads
 #pragma unroll
-            for (int q = 0; q < NV; ++q)
-                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
-                             : "r"(src + q * 16));
+                for (int q = 0; q < 4 * NV; ++q) v[q] = 0.f;
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q)
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                                 : "r"(src + q * 16));
+            }
             fence_proxy_async();          // generic reads before the TMA (async proxy) refill
             mbar_arrive(sempty0 + 8 * p);
             const int st = (int)(g % S);
@@ -635,19 +641,20 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     if constexpr (EC == 16) tmem_ld16(tbase + jj * BN + col, v[jj]);
                     else tmem_ld8(tbase + jj * BN + col, v[jj]);
                 }
-                const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
                 if (col + EC >= BN) {             // last TMEM read of this tile: free the accumulator early
                     tc_fence_before();
                     mbar_arrive(acce0 + 8 * ab);
                 }
+                const int64_t r0 = (int64_t)tc.i * b * d + (int64_t)(tc.k0 + col) * d + tc.j0;
                 if (bias) {                       // KSLinear bias (NEXT-2)
 #pragma unroll
                     for (int e = 0; e < EC; ++e)
 #pragma unroll
                         for (int jj = 0; jj < J; ++jj) v[jj][e] += __ldg(bias + r0 + (int64_t)e * d + jj);
                 }
-                warp_store_rows<float, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, J, EC>::BYTES, v, Y,
-                                              (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                if (!(dbg & 1))                   // profiling experiment: skip the stores
+                    warp_store_rows<float, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, J, EC>::BYTES, v, Y,
+                                                  (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
             }
         }
     }
@@ -1028,7 +1035,7 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
                                          kmap_lo, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
-                                         ntiles);
+                                         ntiles, debug_flags());
     ks::count_launch();
     return e;
 }

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libks.so")
+LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_PKG, "lib", "libks.so")   # KS_LIB: A/B experiments only
 
 BSF, BSL = 0, 1
 MATH_FP32, MATH_TF32, MATH_F32X3 = 0, 1, 2
