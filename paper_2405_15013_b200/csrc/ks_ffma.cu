@@ -25,13 +25,14 @@
 // arithmetic as the generic and streaming kernels (bit-identical results).
 #include "ks_internal.h"
 
+#include <cstdlib>
+
 #ifndef KS_FFMA_MINB
 #define KS_FFMA_MINB 2      // CTAs per SM the register allocation targets (experiments: -DKS_FFMA_MINB=1)
 #endif
 
 namespace {
 
-constexpr int BK = 8;
 constexpr int TM = 8;
 
 template <int J> struct VecJ;
@@ -39,8 +40,9 @@ template <> struct VecJ<1> { using T = float; };
 template <> struct VecJ<2> { using T = float2; };
 template <> struct VecJ<4> { using T = float4; };
 
-template <int LAYOUT, int J, int WPJM, int WPJN, int TN>
+template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK>
 struct Cfg {
+    static constexpr int BK = KBK;                   // l per pipeline chunk
     static constexpr int WARPS = J * WPJM * WPJN;
     static constexpr int THREADS = WARPS * 32;
     static constexpr int BMJ = 64 * WPJM;            // batch rows per j
@@ -64,11 +66,12 @@ struct Cfg {
     static_assert(WARPS <= 8, "at most 8 warps");
 };
 
-template <int LAYOUT, int J, int WPJM, int WPJN, int TN>
-__global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN>::THREADS, KS_FFMA_MINB)
+template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK>
+__global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>::THREADS, KS_FFMA_MINB)
 ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float* __restrict__ Y,
                const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
-    using C = Cfg<LAYOUT, J, WPJM, WPJN, TN>;
+    using C = Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>;
+    constexpr int BK = C::BK;
     using VT = typename VecJ<J>::T;
     pdl_wait();
     pdl_launch_dependents();
@@ -311,6 +314,17 @@ bool pick_bn(int64_t b, int J, int* wpjn, int* tn) {
     return false;
 }
 
+// l per pipeline chunk: 16 when c allows (half the barriers and staging
+// overhead per FFMA), else 8.  KS_FFMA_BK=8 forces 8 (experiments).
+int ffma_bk(const ks_handle_s& h) {
+    static const int forced = [] {
+        const char* e = getenv("KS_FFMA_BK");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced == 8) return 8;
+    return h.c % 16 == 0 ? 16 : 8;
+}
+
 int pick_j(const ks_handle_s& h, const KsCall& call) {
     if (call.layout == KS_LAYOUT_BSL) return 1;
     const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
@@ -319,10 +333,10 @@ int pick_j(const ks_handle_s& h, const KsCall& call) {
     return 1;
 }
 
-template <int LAYOUT, int J, int WPJM, int WPJN, int TN>
+template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK>
 cudaError_t launch_cfg(const ks_handle_s& h, const KsCall& call) {
-    using C = Cfg<LAYOUT, J, WPJM, WPJN, TN>;
-    auto kern = ks_ffma_kernel<LAYOUT, J, WPJM, WPJN, TN>;
+    using C = Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>;
+    auto kern = ks_ffma_kernel<LAYOUT, J, WPJM, WPJN, TN, KBK>;
     static bool attr_set[64] = {false};
     if (!attr_set[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -348,7 +362,8 @@ cudaError_t launch_j(const ks_handle_s& h, const KsCall& call) {
 #define KS_FFMA_CASE(WN, T)                                                                \
     if (wpjn == WN && tn == T) {                                                           \
         if constexpr (8 / (J * WN) >= 1 && (8 % (J * WN)) == 0)                            \
-            return launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T>(h, call);                    \
+            return ffma_bk(h) == 16 ? launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T, 16>(h, call)   \
+                                    : launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T, 8>(h, call);   \
     }
     if constexpr (J <= 2) {
         KS_FFMA_CASE(4, 8)
@@ -367,7 +382,7 @@ cudaError_t launch_j(const ks_handle_s& h, const KsCall& call) {
 namespace ks {
 
 bool ffma_supports(const ks_handle_s& h, const KsCall& call) {
-    if (h.c % BK != 0) return false;
+    if (h.c % 8 != 0) return false;
     int wpjn, tn;
     if (!pick_bn(h.b, 1, &wpjn, &tn)) return false;
     if (h.b > (1 << 20) || h.c > (1 << 20) || h.a * h.d > (int64_t(1) << 30)) return false;
@@ -378,6 +393,7 @@ bool ffma_supports(const ks_handle_s& h, const KsCall& call) {
 }
 
 cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call) {
+    if (ffma_ws_supports(h, call)) return ffma_ws_launch(h, call);
     if (call.layout == KS_LAYOUT_BSL) return launch_j<KS_LAYOUT_BSL, 1>(h, call);
     switch (pick_j(h, call)) {
         case 4: return launch_j<KS_LAYOUT_BSF, 4>(h, call);

@@ -1,0 +1,337 @@
+// Warp-specialised FP32 (CUDA-core FFMA) KS kernel for the layouts whose X
+// operand needs no transposition on its way to shared memory: BSL (any d) and
+// BSF with d = 1.  Same arithmetic as ks_ffma.cu / the generic kernel (one FP32
+// FMA chain per output, l ascending: bit-identical results), different
+// machinery:
+//
+//  * persistent CTAs (2 per SM), tiles = output blocks Y[n0:n0+128,
+//    row_{i,j}[k0:k0+BN]] (output-stationary, Alg. 3, each
+//    element written once);
+//  * X and K^T chunks of 16 l arrive by TMA in an S-slot shared-memory ring
+//    (mbarrier with transaction count per slot), running ahead across tile
+//    boundaries -- the short reduction of a KS block (c = 48..128, 3-8 chunks)
+//    made the register-staged kernel's per-tile prologue and global-load latency
+//    visible (22-36% long-scoreboard stalls, ks_ffma.cu).  There is no producer
+//    warp: the LAST of the 8 warps to finish reading a slot (shared-memory
+//    counter, acq_rel) refills it, so a CTA is 8 warps and two CTAs fit the
+//    per-SM-sub-partition register file at 128 registers per thread (a 9th
+//    warp would cap them at 96);
+//  * warp tile 64 x BN/4, thread micro-tile 8 x TN (TN = BN/16), operands from
+//    shared memory, accumulators in registers, the epilogue stores straight from
+//    registers while the other warps / the refills keep going.
+//
+// Operand layouts in shared memory (no permutation pass):
+//   A, BSL:  [16 l][128 n] from the 3-D box {128 n, 1 j, 16 l} of X viewed as
+//            [a c][d][B]; a thread reads float4 of 4 consecutive n per l.
+//   A, BSF:  [128 n][16 l] from the 2-D box {16 l, 128 n}, SWIZZLE_64B; a thread
+//            reads float4 of 4 consecutive l for rows ty + 8m (the swizzle puts
+//            8 consecutive rows on 8 different bank groups).
+//   B:       [16 l][BN k] from k_tile (K^T tiles).
+#include "ks_umma.cuh"
+
+namespace {
+
+constexpr int WS_BK = 16;              // l per chunk
+constexpr int WS_CWARPS = 8;           // warps per CTA, all compute
+constexpr int WS_THREADS = 32 * WS_CWARPS;
+
+template <int LAYOUT, int BN>
+struct WsCfg {
+    static constexpr int TN = BN / 16;                     // outputs per thread
+    static constexpr int A_BYTES = WS_BK * BM * 4;         // 8 KB
+    static constexpr int B_BYTES = WS_BK * BN * 4;
+    static constexpr int SLOT = A_BYTES + B_BYTES;         // multiple of 1 KB (A stays 1 KB aligned)
+    static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
+    static constexpr int BAR_OFF = S * SLOT;
+    static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;     // full barriers, counters, align pad
+    static_assert(BN == 64 || BN == 96 || BN == 128, "TN in {4, 6, 8}");
+    static_assert(SLOT % 1024 == 0, "slot alignment (SWIZZLE_64B A tiles)");
+    static_assert(S >= 3, "ring depth");
+};
+
+template <int LAYOUT, int BN>
+__global__ void __launch_bounds__(WS_THREADS, 2)
+ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                  float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                  int64_t ntiles) {
+    using C = WsCfg<LAYOUT, BN>;
+    constexpr int S = C::S;
+    constexpr int TN = C::TN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t slot0 = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    const uint32_t full0 = smem_u32(&bars[0]);
+    const uint32_t cnt0 = smem_u32(&bars[8]);         // S u32 "warps done with slot" counters
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nkc = b / BN;
+    const int64_t nnb = (B + BM - 1) / BM;
+    const int nk = c / WS_BK;
+    const int64_t M = (int64_t)a * b * d;
+
+    // tile -> (k-chunk fastest, n-block, block q = i*d + j)
+    auto decode = [&](int64_t tile, int& q, int& k0, int64_t& n0) {
+        k0 = (int)(tile % nkc) * BN;
+        tile /= nkc;
+        n0 = (tile % nnb) * BM;
+        q = (int)(tile / nnb);
+    };
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t G = my_tiles * nk;             // chunks this CTA consumes
+    auto issue = [&](int64_t gx) {               // one thread: TMA of chunk gx into slot gx % S
+        int q, k0;
+        int64_t n0;
+        decode(blockIdx.x + (gx / nk) * gridDim.x, q, k0, n0);
+        const int i = q / d, j = q % d;
+        const int st = (int)(gx % S);
+        const int l0 = (int)(gx % nk) * WS_BK;
+        const uint32_t sa = slot0 + st * C::SLOT;
+        mbar_expect_tx(full0 + 8 * st, C::SLOT);
+        if constexpr (LAYOUT == KS_LAYOUT_BSL)
+            tma_3d(sa, &xmap, (int)n0, j, i * c + l0, full0 + 8 * st);
+        else
+            tma_2d(sa, &xmap, i * c + l0, (int)n0, full0 + 8 * st);
+        tma_2d(sa + C::A_BYTES, &kmap, k0, q * c + l0, full0 + 8 * st);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            asm volatile("st.shared.u32 [%0], 0;" ::"r"(cnt0 + 4 * s) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+    }
+    __syncthreads();
+    pdl_wait();                 // the prologue above overlaps the previous kernel's drain (PDL)
+    pdl_launch_dependents();
+    if (tid == 0)
+        for (int64_t gx = 0; gx < S && gx < G; ++gx) issue(gx);
+
+    const int wm = warp >> 2, wn = warp & 3;      // 2 x 4 warps: 64 rows x BN/4 outputs each
+    const int ty = lane >> 2, tx = lane & 3;
+    const int colB = wn * (BN / 4) + tx * TN;
+    int64_t g = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int q, k0;
+        int64_t n0;
+        decode(tile, q, k0, n0);
+        const int i = q / d, j = q % d;
+        float acc[8][TN];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int e = 0; e < TN; ++e) acc[m][e] = 0.f;
+
+        for (int t = 0; t < nk; ++t, ++g) {
+            const int st = (int)(g % S);
+            mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+            const uint32_t sa = slot0 + st * C::SLOT;
+            const uint32_t sb = sa + C::A_BYTES + colB * 4;
+            if constexpr (LAYOUT == KS_LAYOUT_BSL) {
+                // A[l][n]: rows wm*64 + ty*4 + {0..3} and +32
+                const uint32_t pa = sa + (wm * 64 + ty * 4) * 4;
+#pragma unroll
+                for (int l = 0; l < WS_BK; ++l) {
+                    float av[8], bv[TN];
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(av[0]), "=f"(av[1]), "=f"(av[2]), "=f"(av[3]) : "r"(pa + l * BM * 4));
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(av[4]), "=f"(av[5]), "=f"(av[6]), "=f"(av[7]) : "r"(pa + l * BM * 4 + 128));
+                    const uint32_t pb = sb + l * BN * 4;
+                    if constexpr (TN % 4 == 0) {
+#pragma unroll
+                        for (int e = 0; e < TN; e += 4)
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(bv[e]), "=f"(bv[e + 1]), "=f"(bv[e + 2]), "=f"(bv[e + 3])
+                                         : "r"(pb + e * 4));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < TN; e += 2)
+                            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(bv[e]), "=f"(bv[e + 1]) : "r"(pb + e * 4));
+                    }
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+#pragma unroll
+                        for (int e = 0; e < TN; ++e) acc[m][e] = fmaf(av[m], bv[e], acc[m][e]);
+                }
+            } else {
+                // A[n][l] (64-byte rows, SWIZZLE_64B: 16-byte chunk u of row n at u ^ ((n >> 1) & 3)):
+                // rows wm*64 + ty + 8m; one float4 = 4 consecutive l of a row
+#pragma unroll
+                for (int qd = 0; qd < WS_BK / 4; ++qd) {
+                    float4 av[8];
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {
+                        const int n = wm * 64 + ty + 8 * m;
+                        const uint32_t addr = sa + n * 64 + ((qd ^ ((n >> 1) & 3)) << 4);
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(av[m].x), "=f"(av[m].y), "=f"(av[m].z), "=f"(av[m].w) : "r"(addr));
+                    }
+#pragma unroll
+                    for (int e4 = 0; e4 < 4; ++e4) {
+                        const int l = qd * 4 + e4;
+                        float bv[TN];
+                        const uint32_t pb = sb + l * BN * 4;
+                        if constexpr (TN % 4 == 0) {
+#pragma unroll
+                            for (int e = 0; e < TN; e += 4)
+                                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                             : "=f"(bv[e]), "=f"(bv[e + 1]), "=f"(bv[e + 2]), "=f"(bv[e + 3])
+                                             : "r"(pb + e * 4));
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < TN; e += 2)
+                                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(bv[e]), "=f"(bv[e + 1]) : "r"(pb + e * 4));
+                        }
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const float x = e4 == 0 ? av[m].x : e4 == 1 ? av[m].y : e4 == 2 ? av[m].z : av[m].w;
+#pragma unroll
+                            for (int e = 0; e < TN; ++e) acc[m][e] = fmaf(x, bv[e], acc[m][e]);
+                        }
+                    }
+                }
+            }
+            // generic reads of the slot done (fence: before the async-proxy refill);
+            // the last warp to get here refills the slot with chunk g + S
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                uint32_t old;
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(cnt0 + 4 * st)
+                             : "memory");
+                if (old == WS_CWARPS - 1) {
+                    asm volatile("st.shared.u32 [%0], 0;" ::"r"(cnt0 + 4 * st) : "memory");
+                    if (g + S < G) issue(g + S);
+                }
+            }
+        }
+
+        // ---- epilogue: each owned Y element written exactly once ----------------
+        if (bias) {                               // KSLinear bias (NEXT-2)
+#pragma unroll
+            for (int e = 0; e < TN; ++e) {
+                const float bq = __ldg(bias + (int64_t)i * b * d + (int64_t)(k0 + colB + e) * d + j);
+#pragma unroll
+                for (int m = 0; m < 8; ++m) acc[m][e] += bq;
+            }
+        }
+        if constexpr (LAYOUT == KS_LAYOUT_BSL) {
+            const int64_t nr = n0 + wm * 64 + ty * 4;
+#pragma unroll
+            for (int e = 0; e < TN; ++e) {
+                const int64_t r = (int64_t)i * b * d + (int64_t)(k0 + colB + e) * d + j;
+                float* yr = Y + r * B + nr;
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (nr + 32 * h < B)          // B % 4 == 0: a float4 of rows is all in or all out
+                        __stcs(reinterpret_cast<float4*>(yr + 32 * h),
+                               make_float4(acc[4 * h][e], acc[4 * h + 1][e], acc[4 * h + 2][e], acc[4 * h + 3][e]));
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int64_t n = n0 + wm * 64 + ty + 8 * m;
+                if (n >= B) continue;
+                float* yr = Y + n * M + (int64_t)i * b + k0 + colB;
+                if constexpr (TN % 4 == 0) {
+#pragma unroll
+                    for (int e = 0; e < TN; e += 4)
+                        __stcs(reinterpret_cast<float4*>(yr + e),
+                               make_float4(acc[m][e], acc[m][e + 1], acc[m][e + 2], acc[m][e + 3]));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < TN; e += 2)
+                        __stcs(reinterpret_cast<float2*>(yr + e), make_float2(acc[m][e], acc[m][e + 1]));
+                }
+            }
+        }
+    }
+}
+
+template <int LAYOUT, int BN>
+cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
+    using C = WsCfg<LAYOUT, BN>;
+    CUtensorMap xmap, kmap;
+    {
+        // k_tile: [(i*d + j)*c + l][k], b floats per row
+        const cuuint64_t kd[2] = {(cuuint64_t)h.b, (cuuint64_t)(h.a * h.d * h.c)};
+        const cuuint64_t ks[1] = {(cuuint64_t)h.b * 4};
+        const cuuint32_t kb[2] = {BN, WS_BK};
+        if (!encode(&kmap, h.k_tile, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    if (LAYOUT == KS_LAYOUT_BSL) {
+        const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
+        const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
+        const cuuint32_t xb[3] = {BM, 1, WS_BK};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    } else {
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
+        const cuuint32_t xb[2] = {WS_BK, BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_ffma_ws_kernel<LAYOUT, BN>;
+    static bool attr[64] = {false};
+    if (!attr[h.device & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr[h.device & 63] = true;
+    }
+    const int64_t ntiles = (h.b / BN) * ((call.B + BM - 1) / BM) * (h.a * h.d);
+    int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
+    if (max_grid() > 0) slots = max_grid();
+    const int64_t grid = ntiles < slots ? ntiles : slots;
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(WS_THREADS), C::SMEM, call.stream, xmap, kmap,
+                                         call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
+    ks::count_launch();
+    return e;
+}
+
+int pick_bn_ws(int64_t b) {
+    for (int bn : {128, 96, 64})
+        if (b % bn == 0) return bn;
+    return 0;
+}
+
+template <int LAYOUT>
+cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
+    switch (pick_bn_ws(h.b)) {
+        case 128: return launch_ws<LAYOUT, 128>(h, call);
+        case 96: return launch_ws<LAYOUT, 96>(h, call);
+        case 64: return launch_ws<LAYOUT, 64>(h, call);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+namespace ks {
+
+// BSL (any d) or BSF with d = 1; b a multiple of 64 or 96, c of 16; 16-byte
+// aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 disables (experiments).
+bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
+    static const bool enabled = [] {
+        const char* e = getenv("KS_FFMA_WS");
+        return !(e && atoi(e) == 0);
+    }();
+    if (!enabled || h.dtype != KS_DTYPE_F32) return false;
+    if (pick_bn_ws(h.b) == 0 || h.c % WS_BK != 0) return false;
+    if (call.layout != KS_LAYOUT_BSL && h.d != 1) return false;
+    if (h.a * h.d * h.c >= (int64_t(1) << 31) || call.B >= (int64_t(1) << 31)) return false;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
+    if (al & 15) return false;
+    if (call.layout == KS_LAYOUT_BSL && call.B % 4 != 0) return false;
+    return true;
+}
+
+cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call) {
+    if (call.layout == KS_LAYOUT_BSL) return launch_ws_layout<KS_LAYOUT_BSL>(h, call);
+    return launch_ws_layout<KS_LAYOUT_BSF>(h, call);
+}
+
+}  // namespace ks

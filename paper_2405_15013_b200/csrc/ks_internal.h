@@ -51,6 +51,10 @@ cudaError_t stream_launch(const ks_handle_s& h, const KsCall& call);
 
 bool ffma_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call);
+// warp-specialised TMA-fed FFMA kernel (ks_ffma_ws.cu): BSL, and BSF with d = 1;
+// ffma_launch routes there when it supports the call
+bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call);
 
 bool tf32_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);

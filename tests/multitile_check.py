@@ -11,6 +11,26 @@ import ksgen  # noqa: E402
 import oracle as O  # noqa: E402
 import paper_2405_15013_b200 as ksb  # noqa: E402
 
+if os.environ.get("KS_MULTITILE_MATH") == "fp32":
+    # warp-specialised FFMA kernel (persistent, slot refills by the last reader):
+    # bit-identical to the generic kernel with every CTA running several tiles
+    ok = True
+    for p, lay, B in [((1, 128, 128, 1), "bsf", 1000), ((1, 128, 128, 1), "bsl", 1000), ((6, 64, 64, 1), "bsf", 700),
+                      ((1, 64, 64, 4), "bsl", 1028), ((2, 96, 96, 3), "bsl", 516), ((3, 96, 48, 1), "bsf", 333)]:
+        M, N, _ = O.dims(p)
+        K4 = ksgen.k4_uniform(*p, seed=3)
+        X = ksgen.x_normal(B, N, seed=4)
+        f = ksb.Factor(*p, K4)
+        Xd = torch.from_numpy(X if lay == "bsf" else ksgen.to_bsl(X)).cuda()
+        f.set_kernel(ksb.KERNEL_FFMA)
+        Yf = ksb.matmul(f, Xd, layout=lay).cpu().numpy()
+        f.set_kernel(ksb.KERNEL_GENERIC)
+        Yg = ksb.matmul(f, Xd, layout=lay).cpu().numpy()
+        same = np.array_equal(Yf, Yg)
+        print(p, lay, B, "fp32 maxgrid", os.environ.get("KS_TF32_MAXGRID"), "bit-identical", same)
+        ok = ok and same
+    sys.exit(0 if ok else 1)
+
 if os.environ.get("KS_MULTITILE_MATH") == "f32x3":
     # 3xTF32 (FP32 contract, normwise <= 1e-5), BSL transposer and BSF splitter paths
     worst = 0.0

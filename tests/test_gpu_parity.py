@@ -279,6 +279,20 @@ def test_ffma_matches_oracle_and_generic(ksb, p, layout):
             assert np.array_equal(run(ksb, f, X[:B], layout), Yg[:B])
 
 
+@pytest.mark.parametrize("grid", [1, 3, 7])
+def test_ffma_ws_many_tiles_per_cta(grid):
+    """Warp-specialised FFMA kernel with a capped persistent grid (KS_TF32_MAXGRID):
+    every CTA runs several tiles, so the TMA ring and its last-reader refills wrap."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KS_TF32_MAXGRID=str(grid), KS_MULTITILE_MATH="fp32")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "multitile_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("p", [(1, 128, 128, 64), (16, 48, 48, 4), (1, 96, 96, 1), (4, 64, 64, 16)])
 @pytest.mark.parametrize("layout", ["bsf", "bsl"])
 def test_sweep_full_size_sampled_rows(ksb, p, layout):
