@@ -689,9 +689,13 @@ struct HalfJCfg {
     static constexpr int STG = BM * PITCH;
     static constexpr int BJ_BYTES = BN * BKH * 2;         // per j, BN * 32 B
     static constexpr int SLOT = J * (AH_BYTES + BJ_BYTES);
-    static constexpr int P = 2;
     static constexpr int EC = J > 4 ? 8 : 16;             // epilogue columns per TMEM load
     static constexpr int SCR = 4 * WarpStore<__half, J, EC>::BYTES;     // epilogue store scratch
+    // X staging ring sized for ~96 KB in flight (as Tf32JCfg), leaving 2 operand slots
+    static constexpr int P_WANT = (96 * 1024 + STG - 1) / STG;
+    static constexpr int P_ROOM = (212 * 1024 - 2 * SLOT - SCR) / STG;
+    static constexpr int P_MIN = P_WANT < P_ROOM ? P_WANT : P_ROOM;
+    static constexpr int P = P_MIN < 2 ? 2 : P_MIN > 8 ? 8 : P_MIN;
     static constexpr int S_FIT = (212 * 1024 - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 4 ? 4 : S_FIT;
     static constexpr int SCR_OFF = S * SLOT + P * STG;
@@ -699,6 +703,7 @@ struct HalfJCfg {
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
     static constexpr int TMEM_COLS = 2 * J * BN <= 256 ? 256 : 512;
     static_assert(J * BN <= 256 && BN % 16 == 0, "J accumulators, double-buffered");
+    static_assert((2 * S + 4 + 2 * P) * 8 + 4 <= 256, "barrier area");
     static_assert(S >= 2, "pipeline too shallow");
     static_assert(SMEM <= 227 * 1024, "shared memory");
 };
