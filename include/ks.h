@@ -123,8 +123,8 @@ ks_status_t ks_get_pattern(ks_handle_t h, int64_t out[4]);
  * contraction); otherwise KS_ERR_UNSUPPORTED and the math is unchanged.
  * KS_MATH_F32X3 allocates and packs the low halves rna_tf32(K - rna_tf32(K)) on the
  * handle's device the first time (synchronous).  Calls the F32X3 tensor-core
- * kernels cannot take (BSF with d > 1 and d % 4 != 0) run the FP32 CUDA-core
- * kernels.                                                                 */
+ * kernels cannot take (BSF with d > 4 and d % 4 != 0, c % 16 != 0) run the
+ * FP32 CUDA-core kernels.                                                  */
 ks_status_t ks_set_math(ks_handle_t h, ks_math_t m);
 
 /* Force a kernel family (tests / benchmarks).  KS_KERNEL_AUTO restores the
@@ -203,6 +203,30 @@ int ks_chain_fusion_eligible(const ks_handle_t* handles, int L, int64_t B, ks_la
  * ------------------------------------------------------------------------- */
 ks_status_t ks_chain_host(const ks_handle_t* handles, int L, const float* X_host,
                           float* Y_host, int64_t B, ks_layout_t layout, ks_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * CUDA-graph form of a chain ("optional CUDA-graph
+ * capture"): ks_chain_graph records exactly the launches ks_chain_any would
+ * make for (handles, L, X, Y, bias, B, layout) -- per-factor kernels with
+ * their programmatic-dependent-launch edges, or the one fused-chain kernel --
+ * into an executable CUDA graph; ks_graph_launch replays it on `stream` with a
+ * single cudaGraphLaunch (no per-launch host work).
+ *   X, Y, bias, B, layout: baked into the graph (same meaning, layout and
+ *            alignment rules as ks_chain_any); the caller keeps them alive and
+ *            may change their CONTENTS between launches.
+ *   handles: must outlive the graph; their math / kernel / fusion settings are
+ *            those at capture time.
+ * The graph owns its intermediate workspace (2 x B x max(M_l) elements,
+ * allocated at capture, freed by ks_graph_free).  ks_chain_graph is
+ * synchronous; returns NULL on error (see ks_last_error).  Replays are ordered
+ * on `stream` like any kernel launch; concurrent replays of ONE graph on
+ * different streams are not allowed (they share the workspace).            */
+typedef struct ks_graph_s* ks_graph_t;
+ks_graph_t  ks_chain_graph(const ks_handle_t* handles, int L, const void* X, void* Y, const void* bias,
+                           int64_t B, ks_layout_t layout);
+ks_status_t ks_graph_launch(ks_graph_t g, ks_stream_t stream);
+int         ks_graph_kernel_count(ks_graph_t g);          /* kernels one replay launches; -1 on NULL */
+void        ks_graph_free(ks_graph_t g);                   /* NULL is ignored; synchronises */
 
 /* Copy one packed variant of K back to host (tests check the index maps
  * bit-exactly).  variant 0: canonical a*b*c*d;  1: tile-contiguous K^T,

@@ -16,6 +16,7 @@ namespace {
 
 thread_local ks_status_t t_status = KS_OK;
 thread_local char t_msg[512] = "ok";
+thread_local bool t_capturing = false;   // inside ks_chain_graph's stream capture: no trace events
 
 std::atomic<uint64_t> g_launches{0};
 
@@ -154,7 +155,7 @@ ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, i
                     "B=%lld layout=%d", (int)h.forced, (long long)h.a, (long long)h.b,
                     (long long)h.c, (long long)h.d, (long long)B, layout);
     TraceRec rec{nullptr, nullptr, (int)k, 0.0};
-    const bool tracing = g_trace_on.load(std::memory_order_relaxed);
+    const bool tracing = g_trace_on.load(std::memory_order_relaxed) && !t_capturing;
     if (tracing) {
         std::lock_guard<std::mutex> lk(g_trace_mu);
         rec.start = trace_event();
@@ -209,7 +210,7 @@ bool fusion_ok(const ks_handle_t* hs, int L, const KsCall& call) {
 // Whole chain in one launch (validated arguments, fusion_ok true).
 ks_status_t run_fused(const ks_handle_t* hs, int L, const KsCall& call) {
     TraceRec rec{nullptr, nullptr, (int)KS_KERNEL_FUSED_CHAIN, 0.0};
-    const bool tracing = g_trace_on.load(std::memory_order_relaxed);
+    const bool tracing = g_trace_on.load(std::memory_order_relaxed) && !t_capturing;
     if (tracing) {
         std::lock_guard<std::mutex> lk(g_trace_mu);
         rec.start = trace_event();
@@ -230,27 +231,40 @@ ks_status_t run_fused(const ks_handle_t* hs, int L, const KsCall& call) {
     return KS_OK;
 }
 
-// Chain on device buffers; X, Y validated by the caller.
+// Workspace a per-factor chain needs: nbuf buffers of `bytes` each.
+void chain_workspace(const ks_handle_t* hs, int L, int64_t B, size_t* bytes, int* nbuf) {
+    int64_t maxdim = 0;
+    for (int l = 1; l < L; ++l) maxdim = hs[l]->M > maxdim ? hs[l]->M : maxdim;
+    *bytes = (size_t)hs[0]->esize() * (size_t)(B * maxdim);
+    *nbuf = L >= 3 ? 2 : (L == 2 ? 1 : 0);
+}
+
+// Chain on device buffers; X, Y validated by the caller.  `ws` (optional):
+// caller-owned intermediate buffers (ks_chain_graph), else stream-ordered
+// allocations from the device pool.
 ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
-                      int layout, cudaStream_t s, const float* bias = nullptr) {
+                      int layout, cudaStream_t s, const float* bias = nullptr, void* const* ws = nullptr) {
     if (L == 1) return run_one(*hs[0], X, Y, B, layout, s, bias);
     {
         KsCall call{X, Y, B, layout, s, bias};
         if (fusion_ok(hs, L, call)) return run_fused(hs, L, call);
     }
-    int64_t maxdim = 0;
-    for (int l = 1; l < L; ++l) maxdim = hs[l]->M > maxdim ? hs[l]->M : maxdim;
-    cudaMemPool_t pool;
-    cudaError_t e = get_pool(hs[0]->device, &pool);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
-    const size_t bytes = (size_t)hs[0]->esize() * (size_t)(B * maxdim);
+    size_t bytes;
+    int nbuf;
+    chain_workspace(hs, L, B, &bytes, &nbuf);
     void* buf[2] = {nullptr, nullptr};
-    const int nbuf = L >= 3 ? 2 : 1;
-    for (int i = 0; i < nbuf; ++i) {
-        e = cudaMallocFromPoolAsync(&buf[i], bytes, pool, s);
-        if (e != cudaSuccess) {
-            for (int k = 0; k < i; ++k) cudaFreeAsync(buf[k], s);
-            return fail_cuda(e, "chain workspace");
+    if (ws) {
+        for (int i = 0; i < nbuf; ++i) buf[i] = ws[i];
+    } else {
+        cudaMemPool_t pool;
+        cudaError_t e = get_pool(hs[0]->device, &pool);
+        if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
+        for (int i = 0; i < nbuf; ++i) {
+            e = cudaMallocFromPoolAsync(&buf[i], bytes, pool, s);
+            if (e != cudaSuccess) {
+                for (int k = 0; k < i; ++k) cudaFreeAsync(buf[k], s);
+                return fail_cuda(e, "chain workspace");
+            }
         }
     }
     ks_status_t st = KS_OK;
@@ -260,7 +274,8 @@ ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, in
         st = run_one(*hs[l], in, out, B, layout, s, l == 0 ? bias : nullptr);   // bias after the last hop
         in = out;
     }
-    for (int i = 0; i < nbuf; ++i) cudaFreeAsync(buf[i], s);
+    if (!ws)
+        for (int i = 0; i < nbuf; ++i) cudaFreeAsync(buf[i], s);
     return st;
 }
 
@@ -531,6 +546,92 @@ ks_status_t ks_chain_host(const ks_handle_t* hs, int L, const float* Xh, float* 
     cudaFreeAsync(dY, st);
     if (e != cudaSuccess) return fail_cuda(e, "host<->device copy");
     return s == KS_OK ? ok() : s;
+}
+
+}  // extern "C"
+
+struct ks_graph_s {
+    cudaGraphExec_t exec = nullptr;
+    void* ws[2] = {nullptr, nullptr};
+    int device = 0;
+    int kernels = 0;
+};
+
+extern "C" {
+
+ks_graph_t ks_chain_graph(const ks_handle_t* hs, int L, const void* X, void* Y, const void* bias, int64_t B,
+                          ks_layout_t layout) {
+    ks_status_t s = validate_chain(hs, L, B, (int)layout);
+    if (s != KS_OK) return nullptr;
+    if (B == 0 || !X || !Y) {
+        fail(KS_ERR_INVALID_ARG, "ks_chain_graph needs B > 0 and non-NULL X, Y");
+        return nullptr;
+    }
+    const int es = hs[0]->esize();
+    const uintptr_t amask = (uintptr_t)es - 1;
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(bias)) & amask) {
+        fail(KS_ERR_ALIGNMENT, "X, Y and bias must be element-aligned");
+        return nullptr;
+    }
+    if (overlap(X, B * hs[L - 1]->N * es, Y, B * hs[0]->M * es)) {
+        fail(KS_ERR_INVALID_ARG, "X and Y overlap");
+        return nullptr;
+    }
+    auto* g = new ks_graph_s();
+    g->device = hs[0]->device;
+    size_t bytes;
+    int nbuf;
+    chain_workspace(hs, L, B, &bytes, &nbuf);
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < nbuf && e == cudaSuccess; ++i) e = cudaMalloc(&g->ws[i], bytes);
+    cudaStream_t st = nullptr;
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaGraph_t graph = nullptr;
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        const int64_t l0 = g_launches.load();
+        t_capturing = true;
+        s = run_chain(hs, L, static_cast<const float*>(X), static_cast<float*>(Y), B, (int)layout, st,
+                      static_cast<const float*>(bias), g->ws);
+        t_capturing = false;
+        g->kernels = (int)(g_launches.load() - l0);
+        g_launches.fetch_sub(g->kernels);              // counted again at every replay
+        const cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+        if (s == KS_OK && e2 != cudaSuccess) e = e2;
+    }
+    if (e == cudaSuccess && s == KS_OK) e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (st) cudaStreamDestroy(st);
+    if (e != cudaSuccess || s != KS_OK) {
+        if (e != cudaSuccess) fail_cuda(e, "ks_chain_graph");
+        ks_graph_free(g);
+        return nullptr;
+    }
+    ok();
+    return g;
+}
+
+ks_status_t ks_graph_launch(ks_graph_t g, ks_stream_t stream) {
+    if (!g || !g->exec) return fail(KS_ERR_INVALID_ARG, "NULL graph");
+    const cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail_cuda(e, "cudaGraphLaunch");
+    g_launches.fetch_add(g->kernels, std::memory_order_relaxed);
+    return ok();
+}
+
+int ks_graph_kernel_count(ks_graph_t g) { return g ? g->kernels : -1; }
+
+void ks_graph_free(ks_graph_t g) {
+    if (!g) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g->device);
+    cudaDeviceSynchronize();
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    for (void* p : g->ws)
+        if (p) cudaFree(p);
+    cudaSetDevice(cur);
+    delete g;
 }
 
 ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst, int64_t count) {

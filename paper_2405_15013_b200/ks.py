@@ -34,7 +34,8 @@ EXPORTS = ["ks_pack_weights", "ks_pack_weights_ex", "ks_get_dtype", "ks_matmul_a
            "ks_chain_fusion_eligible", "ks_chain_host", "ks_read_packed",
            "ks_trace_enable", "ks_trace_read",
            "ks_last_error", "ks_last_error_message", "ks_status_string",
-           "ks_kernel_launch_count", "ks_abi_version"]
+           "ks_kernel_launch_count", "ks_abi_version",
+           "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free"]
 
 
 class KSError(RuntimeError):
@@ -108,6 +109,14 @@ def load_library(path: str = LIB_PATH):
     lib.ks_kernel_launch_count.restype = ctypes.c_uint64
     lib.ks_abi_version.argtypes = []
     lib.ks_abi_version.restype = ctypes.c_int
+    lib.ks_chain_graph.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, fp, i64, ctypes.c_int]
+    lib.ks_chain_graph.restype = vp
+    lib.ks_graph_launch.argtypes = [vp, vp]
+    lib.ks_graph_launch.restype = st
+    lib.ks_graph_kernel_count.argtypes = [vp]
+    lib.ks_graph_kernel_count.restype = ctypes.c_int
+    lib.ks_graph_free.argtypes = [vp]
+    lib.ks_graph_free.restype = None
     _lib = lib
     return lib
 
@@ -303,3 +312,36 @@ def chain_host(factors, X_host, Y_host, layout="bsf", stream=None):
     _check(_lib.ks_chain_host(_handles(factors), len(factors), ctypes.c_void_p(X_host.data_ptr()),
                               ctypes.c_void_p(Y_host.data_ptr()), int(B), lay, _stream_ptr(stream)))
     return Y_host
+
+
+class ChainGraph:
+    """ks_chain_graph: the launches of chain(factors, X, Y, layout, bias) captured
+    once into a CUDA graph; launch() replays them with one cudaGraphLaunch.  X, Y
+    and bias are bound at construction (their contents may change between
+    launches); the factors must outlive the graph."""
+
+    def __init__(self, factors, X, Y, layout="bsf", bias=None):
+        lay = _layout(layout)
+        lib = load_library()
+        B = X.shape[0] if lay == BSF else X.shape[1]
+        self._keep = (list(factors), X, Y, bias)
+        bp = _dev_ptr(bias, "bias") if bias is not None else None
+        h = lib.ks_chain_graph(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, int(B), lay)
+        if not h:
+            raise KSError(lib.ks_last_error(), lib.ks_last_error_message().decode())
+        self._g = ctypes.c_void_p(h)
+        self.kernels = int(lib.ks_graph_kernel_count(self._g))
+
+    def launch(self, stream=None):
+        _check(_lib.ks_graph_launch(self._g, _stream_ptr(stream)))
+
+    def free(self):
+        if getattr(self, "_g", None) is not None and _lib is not None:
+            _lib.ks_graph_free(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass

@@ -24,10 +24,10 @@ if [[ $STAGES == *sweep* ]]; then
 fi
 if [[ $STAGES == *ncu* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-      --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep --no-verify \
+      --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep --no-verify --no-baselines \
       > gpurun_out/ncu_launch_bench.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-ks_stream} -s ${NCU_SKIP:-12} -c ${NCU_COUNT:-3} \
-      -o gpurun_out/prof_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep --no-verify ${NCU_BENCH_ARGS} \
+      -o gpurun_out/prof_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep --no-verify --no-baselines ${NCU_BENCH_ARGS} \
       > gpurun_out/ncu_full.log 2>&1
 fi
 ls -la gpurun_out

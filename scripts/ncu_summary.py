@@ -28,7 +28,12 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__shared_mem_per_block_dynamic",
         "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
         "l1tex__m_l1tex2xbar_write_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
-        "smsp__cycles_active.avg"]
+        "smsp__cycles_active.avg", "gpc__cycles_elapsed.max",
+        # tensor pipe (tcgen05 UTCHMMA = the TF32 / F16 MMAs) and tensor memory
+        "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
 
 
 def launches(path):
@@ -55,8 +60,10 @@ def _rows(raw_text):
             continue
         d = {"kernel": row[hdr.index("Kernel Name")][:140]}
         for w in WANT:
-            if w in hdr:
-                d[w] = f"{row[hdr.index(w)]} {units[hdr.index(w)]}".strip()
+            # raw-page headers may carry a section prefix ("TPC.TriageCompute.<metric>")
+            idx = [k for k, h in enumerate(hdr) if h == w or h.endswith("." + w)]
+            if idx:
+                d[w] = f"{row[idx[0]]} {units[idx[0]]}".strip()
         try:
             rd = float(row[hdr.index("dram__bytes_read.sum")].replace(",", ""))
             wr = float(row[hdr.index("dram__bytes_write.sum")].replace(",", ""))

@@ -114,3 +114,44 @@ def test_fused_chain_host_and_trace(ksb):
     assert byts[0] == 4 * (100 * 1024 * 2 + sum(np.prod(p) for p in pats))
     Yf, Yu, _ = both(ksb, fs, X)
     assert np.array_equal(Yh.numpy(), Yu)
+
+
+# ------------------------------------------------------- CUDA-graph chains ----
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+def test_chain_graph_replays_bit_identical(ksb, fused, layout):
+    """ks_chain_graph: the captured launches replay to exactly
+    the direct chain's result, repeatedly, after the input changes, on another
+    stream; the replay's kernel count is credited to the launch counter."""
+    pats = configs.dyadic_patterns(8) if layout == "bsf" else configs.VIT_DOWN
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    N = configs.chain_dims(pats)[0]
+    B = 300
+    X = torch.from_numpy(ksgen.x_normal(B, N, seed=0)).cuda()
+    if layout == "bsl":
+        X = X.t().contiguous()
+    ksb.set_chain_fusion(fused)
+    try:
+        Yd = ksb.chain(fs, X, layout=layout)
+        Yg = torch.empty_like(Yd)
+        g = ksb.ChainGraph(fs, X, Yg, layout=layout)
+        assert g.kernels == (1 if (fused and ksb.chain_fusion_eligible(fs, B, layout)) else len(fs))
+        n0 = ksb.launch_count()
+        for _ in range(3):
+            g.launch()
+        torch.cuda.synchronize()
+        assert ksb.launch_count() - n0 == 3 * g.kernels
+        assert torch.equal(Yg, Yd)
+        X.mul_(-0.5)                                  # new contents, same buffer
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g.launch(s)
+        s.synchronize()
+        Yd2 = ksb.chain(fs, X, layout=layout)
+        torch.cuda.synchronize()
+        assert torch.equal(Yg, Yd2)
+        g.free()
+    finally:
+        ksb.set_chain_fusion(True)
