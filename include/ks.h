@@ -195,11 +195,18 @@ int ks_chain_fusion_eligible(const ks_handle_t* handles, int L, int64_t B, ks_la
 
 /* ---------------------------------------------------------------------------
  * ks_chain_host -- end-to-end form of ks_chain_ex for HOST buffers: X_host and
- * Y_host are host memory (pinned for full PCIe speed; pageable works but the
- * copies then serialise).  Enqueues host->device copy of X, the chain, and
- * device->host copy of Y on `stream`; device buffers come from the library's
- * stream-ordered pool.  Asynchronous: Y_host is valid after the caller
- * synchronises `stream`.  A single factor is L = 1.
+ * Y_host are host memory (pinned for full PCIe speed and copy/compute
+ * overlap; pageable works but the copies then serialise).  The batch is cut
+ * into chunks of ~16 MB of X + Y (at most 16) and pipelined over three
+ * library-internal streams: the host->device copy of chunk k+1 and the
+ * device->host copy of chunk k-1 overlap the chain on chunk k.  Ordered after
+ * prior work on `stream`, and later work on `stream` waits for all of it;
+ * device buffers come from the library's stream-ordered pool.  Asynchronous:
+ * Y_host is valid after the caller synchronises `stream`.  Each row equals
+ * ks_chain_ex's result bit for bit whenever the chunks run the same kernel
+ * families as the whole batch (always under KS_MATH_FP32, whose kernels are
+ * bit-identical; a ragged BSL chunk may move a TF32 call to FP32 FFMA).  A
+ * single factor is L = 1.
  * ------------------------------------------------------------------------- */
 ks_status_t ks_chain_host(const ks_handle_t* handles, int L, const float* X_host,
                           float* Y_host, int64_t B, ks_layout_t layout, ks_stream_t stream);

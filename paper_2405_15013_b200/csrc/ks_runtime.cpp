@@ -71,6 +71,31 @@ bool mul_ok(int64_t x, int64_t y, int64_t* out) {
 std::mutex g_pool_mu;
 std::vector<cudaMemPool_t> g_pools;
 
+// Per-device internal streams of ks_chain_host's copy / compute pipeline.
+struct HostStreams {
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+};
+std::mutex g_hs_mu;
+std::vector<HostStreams*> g_hs;
+
+cudaError_t host_streams(int dev, HostStreams** out) {
+    std::lock_guard<std::mutex> lk(g_hs_mu);
+    if ((int)g_hs.size() <= dev) g_hs.resize(dev + 1, nullptr);
+    if (!g_hs[dev]) {
+        auto* h = new HostStreams();
+        cudaError_t e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->comp, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete h;
+            return e;
+        }
+        g_hs[dev] = h;
+    }
+    *out = g_hs[dev];
+    return cudaSuccess;
+}
+
 cudaError_t get_pool(int dev, cudaMemPool_t* out) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1, nullptr);
@@ -525,26 +550,83 @@ ks_status_t ks_chain_host(const ks_handle_t* hs, int L, const float* Xh, float* 
     if (s != KS_OK) return s;
     if (B == 0) return ok();
     if (!Xh || !Yh) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int dev = hs[0]->device;
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    HostStreams* hsm = nullptr;
+    cudaError_t e = host_streams(dev, &hsm);
+    if (e != cudaSuccess) return fail_cuda(e, "internal streams");
     cudaMemPool_t pool;
-    cudaError_t e = get_pool(hs[0]->device, &pool);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
-    const size_t xbytes = (size_t)hs[0]->esize() * (size_t)(B * hs[L - 1]->N);
-    const size_t ybytes = (size_t)hs[0]->esize() * (size_t)(B * hs[0]->M);
+    if ((e = get_pool(dev, &pool)) != cudaSuccess) return fail_cuda(e, "cudaMemPoolCreate");
+    const int64_t es = hs[0]->esize();
+    const int64_t N = hs[L - 1]->N, M = hs[0]->M;
+    const size_t xbytes = (size_t)(es * B * N), ybytes = (size_t)(es * B * M);
+    // Batch chunks of ~16 MB of X + Y, pipelined over three streams: the H2D copy
+    // of chunk k+1 and the D2H copy of chunk k-1 overlap the chain on chunk k
+    // (PCIe is full duplex; rows are independent).  BSL chunks are column
+    // blocks (2-D copies into a contiguous N x Bc buffer), multiples of 4 columns.
+    const int64_t per_row = es * (N + M);
+    int64_t bc = (int64_t)(16 << 20) / (per_row > 0 ? per_row : 1);
+    if (bc < 1) bc = 1;
+    if (bc * 16 < B) bc = (B + 15) / 16;                 // at most 16 chunks
+    if (layout == KS_LAYOUT_BSL) bc = (bc + 3) / 4 * 4;
+    if (bc > B) bc = B;
+    const int64_t nch = (B + bc - 1) / bc;
     void *dX = nullptr, *dY = nullptr;
-    if ((e = cudaMallocFromPoolAsync(&dX, xbytes, pool, st)) != cudaSuccess) return fail_cuda(e, "staging X");
-    if ((e = cudaMallocFromPoolAsync(&dY, ybytes, pool, st)) != cudaSuccess) {
-        cudaFreeAsync(dX, st);
+    if ((e = cudaMallocFromPoolAsync(&dX, xbytes, pool, user)) != cudaSuccess) return fail_cuda(e, "staging X");
+    if ((e = cudaMallocFromPoolAsync(&dY, ybytes, pool, user)) != cudaSuccess) {
+        cudaFreeAsync(dX, user);
         return fail_cuda(e, "staging Y");
     }
-    e = cudaMemcpyAsync(dX, Xh, xbytes, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) {
-        s = run_chain(hs, L, static_cast<const float*>(dX), static_cast<float*>(dY), B, (int)layout, st);
-        if (s == KS_OK) e = cudaMemcpyAsync(Yh, dY, ybytes, cudaMemcpyDeviceToHost, st);
+    std::vector<cudaEvent_t> evs;
+    auto event = [&](cudaEvent_t* ev) {
+        cudaError_t r = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (r == cudaSuccess) evs.push_back(*ev);
+        return r;
+    };
+    cudaEvent_t ev_start;
+    if ((e = event(&ev_start)) == cudaSuccess) e = cudaEventRecord(ev_start, user);
+    for (cudaStream_t t : {hsm->h2d, hsm->comp, hsm->d2h})
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(t, ev_start, 0);
+    for (int64_t k = 0; k < nch && e == cudaSuccess && s == KS_OK; ++k) {
+        const int64_t n0 = k * bc, nb = (B - n0) < bc ? (B - n0) : bc;
+        // device chunk buffers: B x N / B x M (BSF) or N x nb / M x nb (BSL), contiguous
+        char* xk = static_cast<char*>(dX) + es * n0 * N;
+        char* yk = static_cast<char*>(dY) + es * n0 * M;
+        // H2D of chunk k
+        if (layout == KS_LAYOUT_BSF)
+            e = cudaMemcpyAsync(xk, reinterpret_cast<const char*>(Xh) + es * n0 * N, (size_t)(es * nb * N),
+                                cudaMemcpyHostToDevice, hsm->h2d);
+        else   // column block [n0, n0 + nb) of the N x B host matrix -> contiguous N x nb
+            e = cudaMemcpy2DAsync(xk, (size_t)(es * nb), reinterpret_cast<const char*>(Xh) + es * n0, (size_t)(es * B),
+                                  (size_t)(es * nb), (size_t)N, cudaMemcpyHostToDevice, hsm->h2d);
+        cudaEvent_t ev_in, ev_comp;
+        if (e == cudaSuccess) e = event(&ev_in);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in, hsm->h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(hsm->comp, ev_in, 0);
+        if (e != cudaSuccess) break;
+        s = run_chain(hs, L, reinterpret_cast<const float*>(xk), reinterpret_cast<float*>(yk), nb, (int)layout,
+                      hsm->comp);
+        if (s != KS_OK) break;
+        if ((e = event(&ev_comp)) == cudaSuccess) e = cudaEventRecord(ev_comp, hsm->comp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(hsm->d2h, ev_comp, 0);
+        if (e != cudaSuccess) break;
+        // D2H of chunk k
+        if (layout == KS_LAYOUT_BSF)
+            e = cudaMemcpyAsync(reinterpret_cast<char*>(Yh) + es * n0 * M, yk, (size_t)(es * nb * M),
+                                cudaMemcpyDeviceToHost, hsm->d2h);
+        else
+            e = cudaMemcpy2DAsync(reinterpret_cast<char*>(Yh) + es * n0, (size_t)(es * B), yk, (size_t)(es * nb),
+                                  (size_t)(es * nb), (size_t)M, cudaMemcpyDeviceToHost, hsm->d2h);
     }
-    cudaFreeAsync(dX, st);
-    cudaFreeAsync(dY, st);
-    if (e != cudaSuccess) return fail_cuda(e, "host<->device copy");
+    // join: the caller's stream waits for every internal stream (also on error paths)
+    for (cudaStream_t t : {hsm->h2d, hsm->comp, hsm->d2h}) {
+        cudaEvent_t ev_j;
+        if (event(&ev_j) == cudaSuccess && cudaEventRecord(ev_j, t) == cudaSuccess) cudaStreamWaitEvent(user, ev_j, 0);
+    }
+    cudaFreeAsync(dX, user);
+    cudaFreeAsync(dY, user);
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);    // released once complete
+    if (e != cudaSuccess) return fail_cuda(e, "host<->device pipeline");
     return s == KS_OK ? ok() : s;
 }
 

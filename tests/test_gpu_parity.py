@@ -197,6 +197,36 @@ def test_chain_host_equals_device(ksb):
     assert np.array_equal(Yh.numpy(), Yd.cpu().numpy())
 
 
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_chain_host_pipelined_chunks(ksb, layout, pinned):
+    """ks_chain_host cuts big batches into ~16 MB chunks pipelined over three
+    internal streams (H2D / chain / D2H): several chunks with a ragged last one,
+    both layouts (BSL chunks are 2-D column-block copies), pinned and pageable
+    host memory, a non-default caller stream -> bit-identical to the device chain."""
+    pats = [(6, 64, 64, 1), (1, 128, 128, 3)]            # configs[3] DOWN shapes, FFMA (FP32)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    N, M = configs.chain_dims(pats)[0], fs[0].M
+    B = 9002                                              # 3 KB per row -> 4 chunks of 5462 / ... ragged
+    X = ksgen.x_normal(B, N, seed=0)
+    Xl = X if layout == "bsf" else ksgen.to_bsl(X)
+    Xh = torch.from_numpy(np.ascontiguousarray(Xl))
+    Yh = torch.empty((B, M) if layout == "bsf" else (M, B), dtype=torch.float32)
+    if pinned:
+        Xh, Yh = Xh.pin_memory(), Yh.pin_memory()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ksb.chain_host(fs, Xh, Yh, layout=layout, stream=s)
+    s.synchronize()
+    Yd = ksb.chain(fs, to_dev(Xl), layout=layout)
+    torch.cuda.synchronize()
+    assert np.array_equal(Yh.numpy(), Yd.cpu().numpy())
+    rows = np.array([0, 1, 5461, 5462, B - 1])
+    Yr = Yh.numpy() if layout == "bsf" else Yh.numpy().T
+    assert O.normwise_error(Yr[rows], O.chain(pats, K4s, X, rows=rows)) <= 1e-5
+
+
 def test_deterministic_and_misaligned(ksb):
     p = (4, 2, 2, 16)
     M, N, _ = O.dims(p)
