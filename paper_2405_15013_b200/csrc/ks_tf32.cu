@@ -683,10 +683,17 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 constexpr int BKH = 16;                        // l per stage (one UMMA k-step of 32 B)
 constexpr int AH_BYTES = BM * BKH * 2;         // 4 KB per j
 
-template <int J, int BN>
+// JB = j extent of the X box: J, or 8 for J = 4 when d % 8 != 0.  A 4-half
+// box row would be 8 bytes (TMA's minimum is 16) and a 3-D view needs the l
+// stride d * 2 bytes to be a multiple of 16, so that case ("per-l boxes") loads
+// 16 2-D boxes {8 halves, 128 n} per stage, one per l, stacked [l][n][8]
+// (the transposers use the first 4 of the 8 j; the rest is the next j-group's,
+// served from L2).
+template <int J, int BN, int JB = J>
 struct HalfJCfg {
-    static constexpr int PITCH = 32 * J + 16;             // staged row: [16 l][J] halves + 16 B
-    static constexpr int STG = BM * PITCH;
+    static constexpr bool PER_L = JB != J;
+    static constexpr int PITCH = PER_L ? 16 : 32 * JB + 16;   // staged row: [16 l][JB] halves + 16 B
+    static constexpr int STG = PER_L ? BKH * BM * 16 : BM * PITCH;
     static constexpr int BJ_BYTES = BN * BKH * 2;         // per j, BN * 32 B
     static constexpr int SLOT = J * (AH_BYTES + BJ_BYTES);
     static constexpr int EC = J > 4 ? 8 : 16;             // epilogue columns per TMEM load
@@ -708,12 +715,12 @@ struct HalfJCfg {
     static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-template <typename T, int J, int BN>
+template <typename T, int J, int BN, int JB = J>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
                     int64_t ntiles) {
-    using C = HalfJCfg<J, BN>;
+    using C = HalfJCfg<J, BN, JB>;
     constexpr int S = C::S;
     constexpr int P = C::P;
     extern __shared__ uint8_t smem_raw[];
@@ -779,10 +786,16 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 const int p = (int)(gx % P);
                 if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
                 mbar_expect_tx(sfull0 + 8 * p, C::STG);
-                if (contig)
+                if constexpr (C::PER_L) {
+#pragma unroll 1
+                    for (int l = 0; l < BKH; ++l)
+                        tma_2d(stg0 + p * C::STG + l * (BM * 16), &xmap, ((tc.i * c + l0 + l) * d + tc.j0) & ~7,
+                               tc.n0, sfull0 + 8 * p);   // 16-byte aligned start (required)
+                } else if (contig) {
                     tma_2d(stg0 + p * C::STG, &xmap, (tc.i * c + l0) * d, tc.n0, sfull0 + 8 * p);
-                else
+                } else {
                     tma_3d(stg0 + p * C::STG, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
+                }
             };
             for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
             for (int64_t g = 0; g < G; ++g) {
@@ -805,15 +818,34 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         for (int64_t g = 0; g < G; ++g) {
             const int p = (int)(g % P);
             mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
-            uint32_t w[8 * J];
+            uint32_t w[8 * JB];
             const uint32_t src = stg0 + p * C::STG + r * C::PITCH;
+            // 16-byte unit q of the virtual row [16 l][JB]: contiguous, or (per-l boxes) l = q at l * 2 KB
+            constexpr uint32_t QSTRIDE = C::PER_L ? BM * 16 : 16;
 #pragma unroll
-            for (int q = 0; q < 2 * J; ++q)
+            for (int q = 0; q < 2 * JB; ++q)
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(w[4 * q]), "=r"(w[4 * q + 1]), "=r"(w[4 * q + 2]), "=r"(w[4 * q + 3])
-                             : "r"(src + q * 16));
+                             : "r"(src + q * QSTRIDE));
             fence_proxy_async();          // generic reads before the TMA (async proxy) refill
             mbar_arrive(sempty0 + 8 * p);
+            // virtual row [16 l][J] halves, as 32-bit words
+            uint32_t wv[8 * J];
+            if constexpr (C::PER_L) {
+                // box l starts at the 16-byte-aligned column below (i c + l0 + l) d + j0; the
+                // 4 wanted halves sit at offset 0 or 4 (d, j0 multiples of 4): words 0-1 or 2-3
+                const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
+                const int col0 = (tc.i * c + (int)(g % nk) * BKH) * d + tc.j0;
+#pragma unroll
+                for (int l = 0; l < BKH; ++l) {
+                    const bool hi4 = ((col0 + l * d) & 4) != 0;
+                    wv[2 * l] = hi4 ? w[4 * l + 2] : w[4 * l];
+                    wv[2 * l + 1] = hi4 ? w[4 * l + 3] : w[4 * l + 1];
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8 * J; ++q) wv[q] = w[q];
+            }
             const int st = (int)(g % S);
             if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
             const uint32_t sa = slot0 + st * C::SLOT + rowoff;
@@ -824,7 +856,7 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 for (int q = 0; q < 8; ++q) {         // halves l = 2q, 2q+1 of column jj
                     const int e0 = (2 * q) * J + jj, e1 = (2 * q + 1) * J + jj;
                     const uint32_t sel = (e0 & 1 ? 0x32u : 0x10u) | ((e1 & 1 ? 0x76u : 0x54u) << 8);
-                    o[q] = __byte_perm(w[e0 >> 1], w[e1 >> 1], sel);
+                    o[q] = __byte_perm(wv[e0 >> 1], wv[e1 >> 1], sel);
                 }
                 sts128(sa + jj * AH_BYTES + ((0 ^ sw) * 16), __uint_as_float(o[0]), __uint_as_float(o[1]),
                        __uint_as_float(o[2]), __uint_as_float(o[3]));
@@ -885,8 +917,28 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
                         for (int jj = 0; jj < J; ++jj) v[jj][e] += ElemTraits<T>::to_f(bias[r0 + (int64_t)e * d + jj]);
                 }
-                warp_store_rows<T, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<T, J, EC>::BYTES, v, Y,
-                                          (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                if constexpr (JB != J) {
+                    // J = 4 of an 8-wide box (d % 8 != 0): the 4 outputs of one k are one
+                    // 8-byte run, the next k is d away -- per-row stores (units of the
+                    // coalescing store would straddle runs)
+                    const int64_t n = (int64_t)tc.n0 + lq * 32 + lane;
+                    if (n < B) {
+#pragma unroll
+                        for (int e = 0; e < EC; ++e) {
+                            uint32_t w[2];
+#pragma unroll
+                            for (int x = 0; x < 2; ++x) {
+                                const T lo = ElemTraits<T>::from_f(v[2 * x][e]), hi = ElemTraits<T>::from_f(v[2 * x + 1][e]);
+                                w[x] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
+                                       ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
+                            }
+                            __stcs(reinterpret_cast<uint2*>(Y + n * M + r0 + (int64_t)e * d), make_uint2(w[0], w[1]));
+                        }
+                    }
+                } else {
+                    warp_store_rows<T, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<T, J, EC>::BYTES, v, Y,
+                                              (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                }
             }
             tc_fence_before();
             mbar_arrive(acce0 + 8 * ab);
@@ -1082,9 +1134,11 @@ cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
 bool bsfj_ok(const ks_handle_s& h) { return pick_bsfj(h).J != 0; }
 
 // Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
+// d % 4 == 0 but not 8 (d = 12, 20, ...): J = 4 from an 8-wide box.
 int pick_j_half(int64_t d) {
     if (d == 2 || d == 3 || d == 4 || d == 6 || d == 8) return (int)d;
-    return d % 8 == 0 ? 8 : 0;
+    if (d % 8 == 0) return 8;
+    return d % 4 == 0 ? 4 : 0;
 }
 int pick_bn_half(int64_t b, int J) {
     for (int bn : {128, 96, 64, 48, 32, 16})
@@ -1092,9 +1146,9 @@ int pick_bn_half(int64_t b, int J) {
     return 0;
 }
 
-template <typename T, int J, int BN>
+template <typename T, int J, int BN, int JB = J>
 cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
-    using C = HalfJCfg<J, BN>;
+    using C = HalfJCfg<J, BN, JB>;
     const CUtensorMapDataType dt = ElemTraits<T>::tma;
     CUtensorMap xmap, kmap;
     {
@@ -1103,7 +1157,12 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t kb[2] = {BKH, BN};
         if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_32B, dt)) return cudaErrorInvalidValue;
     }
-    if (J == h.d) {
+    if (C::PER_L) {
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 2};
+        const cuuint32_t xb[2] = {(cuuint32_t)JB, BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
+    } else if (J == h.d) {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * 2};
         const cuuint32_t xb[2] = {(cuuint32_t)(BKH * J + 8), BM};
@@ -1111,10 +1170,10 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
     } else {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 2, (cuuint64_t)h.N * 2};
-        const cuuint32_t xb[3] = {8, BKH + 1, BM};
+        const cuuint32_t xb[3] = {(cuuint32_t)JB, BKH + 1, BM};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_half_bsfj_kernel<T, J, BN>;
+    auto kern = ks_half_bsfj_kernel<T, J, BN, JB>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1132,15 +1191,15 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
-template <typename T, int J>
+template <typename T, int J, int JB = J>
 cudaError_t launch_halfj_bn(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn_half(h.b, J)) {
-        case 128: if constexpr (J * 128 <= 256) return launch_halfj<T, J, 128>(h, call); break;
-        case 96: if constexpr (J * 96 <= 256) return launch_halfj<T, J, 96>(h, call); break;
-        case 64: if constexpr (J * 64 <= 256) return launch_halfj<T, J, 64>(h, call); break;
-        case 48: if constexpr (J * 48 <= 256) return launch_halfj<T, J, 48>(h, call); break;
-        case 32: if constexpr (J * 32 <= 256) return launch_halfj<T, J, 32>(h, call); break;
-        case 16: return launch_halfj<T, J, 16>(h, call);
+        case 128: if constexpr (J * 128 <= 256) return launch_halfj<T, J, 128, JB>(h, call); break;
+        case 96: if constexpr (J * 96 <= 256) return launch_halfj<T, J, 96, JB>(h, call); break;
+        case 64: if constexpr (J * 64 <= 256) return launch_halfj<T, J, 64, JB>(h, call); break;
+        case 48: if constexpr (J * 48 <= 256) return launch_halfj<T, J, 48, JB>(h, call); break;
+        case 32: if constexpr (J * 32 <= 256) return launch_halfj<T, J, 32, JB>(h, call); break;
+        case 16: return launch_halfj<T, J, 16, JB>(h, call);
     }
     return cudaErrorInvalidValue;
 }
@@ -1150,7 +1209,7 @@ cudaError_t launch_halfj_any(const ks_handle_s& h, const KsCall& call) {
     switch (pick_j_half(h.d)) {
         case 2: return launch_halfj_bn<T, 2>(h, call);
         case 3: return launch_halfj_bn<T, 3>(h, call);
-        case 4: return launch_halfj_bn<T, 4>(h, call);
+        case 4: return h.d == 4 ? launch_halfj_bn<T, 4>(h, call) : launch_halfj_bn<T, 4, 8>(h, call);
         case 6: return launch_halfj_bn<T, 6>(h, call);
         case 8: return launch_halfj_bn<T, 8>(h, call);
     }

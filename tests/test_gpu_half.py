@@ -49,7 +49,9 @@ CASES = [((1, 64, 64, 1), "bsf"), ((6, 64, 256, 1), "bsf"), ((2, 128, 128, 1), "
          ((1, 768, 192, 2), "bsl"), ((3, 96, 96, 3), "bsl"), ((2, 16, 32, 2), "bsl"),
          # BSF d > 1: J-column gather, J = d (2-D box) or J = 8 (3-D box)
          ((2, 128, 64, 2), "bsf"), ((1, 48, 48, 3), "bsf"), ((3, 64, 64, 4), "bsf"), ((1, 96, 96, 6), "bsf"),
-         ((1, 64, 64, 8), "bsf"), ((1, 32, 48, 16), "bsf"), ((2, 16, 16, 24), "bsf")]
+         ((1, 64, 64, 8), "bsf"), ((1, 32, 48, 16), "bsf"), ((2, 16, 16, 24), "bsf"),
+         # d % 4 == 0, d % 8 != 0: J = 4 out of an 8-wide box, per-row 8-byte stores
+         ((1, 48, 64, 12), "bsf"), ((2, 64, 64, 12), "bsf"), ((1, 32, 32, 20), "bsf")]
 
 
 @pytest.mark.parametrize("name", ["bf16", "f16"])
@@ -68,7 +70,7 @@ def test_half_tensor_core(ksb, name, p, layout):
 
 
 @pytest.mark.parametrize("name", ["bf16", "f16"])
-@pytest.mark.parametrize("p,layout", [((2, 4, 4, 2), "bsf"), ((1, 64, 64, 5), "bsf"), ((1, 48, 64, 12), "bsf"),
+@pytest.mark.parametrize("p,layout", [((2, 4, 4, 2), "bsf"), ((1, 64, 64, 5), "bsf"), ((1, 48, 64, 10), "bsf"),
                                       ((2, 3, 5, 7), "bsl")])
 def test_half_generic(ksb, name, p, layout):
     B = 33
@@ -82,6 +84,7 @@ def test_half_generic(ksb, name, p, layout):
 
 @pytest.mark.parametrize("name", ["bf16", "f16"])
 @pytest.mark.parametrize("p,layout", [((2, 64, 64, 1), "bsf"), ((1, 32, 32, 8), "bsf"), ((2, 48, 48, 3), "bsf"),
+                                      ((1, 64, 32, 12), "bsf"),
                                       ((2, 32, 32, 4), "bsl")])
 def test_half_integer_exact_and_bias(ksb, name, p, layout):
     M, N, _ = O.dims(p)
