@@ -18,6 +18,8 @@ def summarize(path):
     mix = {}
     iexec = hdr.index("Instructions Executed")
     for r in data:
+        if len(r) < len(hdr):
+            continue
         for i in cols:
             try:
                 tot[hdr[i]] += int(r[i])
