@@ -35,16 +35,22 @@ constexpr int WS_BK = 16;              // l per chunk
 constexpr int WS_CWARPS = 8;           // warps per CTA, all compute
 constexpr int WS_THREADS = 32 * WS_CWARPS;
 
+// Warps split 2 x 4 (rows x outputs) for BN in {96, 128}: tile 128 rows, TN =
+// BN/16; BN = 64 uses 4 x 2 warps: tile 256 rows, TN = 8 (a 128 x 64 tile would
+// leave TN = 4: 3 shared loads per 32 FFMA instead of 4 per 64).
 template <int LAYOUT, int BN>
 struct WsCfg {
-    static constexpr int TN = BN / 16;                     // outputs per thread
-    static constexpr int A_BYTES = WS_BK * BM * 4;         // 8 KB
+    static constexpr int WM = BN == 64 ? 4 : 2;            // warps along the batch rows
+    static constexpr int WN = 8 / WM;                      // warps along the outputs
+    static constexpr int BMW = 64 * WM;                    // batch rows per tile
+    static constexpr int TN = BN / (4 * WN);               // outputs per thread
+    static constexpr int A_BYTES = WS_BK * BMW * 4;        // 8 or 16 KB
     static constexpr int B_BYTES = WS_BK * BN * 4;
     static constexpr int SLOT = A_BYTES + B_BYTES;         // multiple of 1 KB (A stays 1 KB aligned)
     static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
     static constexpr int BAR_OFF = S * SLOT;
     static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;     // full barriers, counters, align pad
-    static_assert(BN == 64 || BN == 96 || BN == 128, "TN in {4, 6, 8}");
+    static_assert(BN == 64 || BN == 96 || BN == 128, "TN in {6, 8}");
     static_assert(SLOT % 1024 == 0, "slot alignment (SWIZZLE_64B A tiles)");
     static_assert(S >= 3, "ring depth");
 };
@@ -67,7 +73,8 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nkc = b / BN;
-    const int64_t nnb = (B + BM - 1) / BM;
+    constexpr int BMW = C::BMW;
+    const int64_t nnb = (B + BMW - 1) / BMW;
     const int nk = c / WS_BK;
     const int64_t M = (int64_t)a * b * d;
 
@@ -75,7 +82,7 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
     auto decode = [&](int64_t tile, int& q, int& k0, int64_t& n0) {
         k0 = (int)(tile % nkc) * BN;
         tile /= nkc;
-        n0 = (tile % nnb) * BM;
+        n0 = (tile % nnb) * BMW;
         q = (int)(tile / nnb);
     };
     const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
@@ -111,9 +118,9 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
     if (tid == 0)
         for (int64_t gx = 0; gx < S && gx < G; ++gx) issue(gx);
 
-    const int wm = warp >> 2, wn = warp & 3;      // 2 x 4 warps: 64 rows x BN/4 outputs each
+    const int wm = warp / C::WN, wn = warp % C::WN;   // WM x WN warps: 64 rows x BN/WN outputs each
     const int ty = lane >> 2, tx = lane & 3;
-    const int colB = wn * (BN / 4) + tx * TN;
+    const int colB = wn * (BN / C::WN) + tx * TN;
     int64_t g = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int q, k0;
@@ -138,9 +145,9 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                 for (int l = 0; l < WS_BK; ++l) {
                     float av[8], bv[TN];
                     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(av[0]), "=f"(av[1]), "=f"(av[2]), "=f"(av[3]) : "r"(pa + l * BM * 4));
+                                 : "=f"(av[0]), "=f"(av[1]), "=f"(av[2]), "=f"(av[3]) : "r"(pa + l * BMW * 4));
                     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(av[4]), "=f"(av[5]), "=f"(av[6]), "=f"(av[7]) : "r"(pa + l * BM * 4 + 128));
+                                 : "=f"(av[4]), "=f"(av[5]), "=f"(av[6]), "=f"(av[7]) : "r"(pa + l * BMW * 4 + 128));
                     const uint32_t pb = sb + l * BN * 4;
                     if constexpr (TN % 4 == 0) {
 #pragma unroll
@@ -267,12 +274,12 @@ cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
     if (LAYOUT == KS_LAYOUT_BSL) {
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
         const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
-        const cuuint32_t xb[3] = {BM, 1, WS_BK};
+        const cuuint32_t xb[3] = {(cuuint32_t)C::BMW, 1, WS_BK};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     } else {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
-        const cuuint32_t xb[2] = {WS_BK, BM};
+        const cuuint32_t xb[2] = {WS_BK, (cuuint32_t)C::BMW};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
     }
     auto kern = ks_ffma_ws_kernel<LAYOUT, BN>;
@@ -282,7 +289,7 @@ cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
         if (e != cudaSuccess) return e;
         attr[h.device & 63] = true;
     }
-    const int64_t ntiles = (h.b / BN) * ((call.B + BM - 1) / BM) * (h.a * h.d);
+    const int64_t ntiles = (h.b / BN) * ((call.B + C::BMW - 1) / C::BMW) * (h.a * h.d);
     int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
