@@ -352,3 +352,30 @@ def test_model_chain_full_size_sampled_rows(ksb, name):
     rows = np.array([0, 1, B // 2, B - 1])
     Yref = O.chain(pats, K4s, X, rows=rows)
     assert O.normwise_error(Y.cpu().numpy()[rows], Yref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("math", ["tf32", "f32x3"])
+@pytest.mark.parametrize("name", ["VIT_UP", "VIT_DOWN", "GPT2_DOWN", "GPT2_UP"])
+def test_model_chain_full_size_tensor_core_sampled_rows(ksb, name, math):
+    """configs[3]/[4] at the bench's sizes and launch configuration (BSF, per-factor
+    launches) in TF32 (normwise 5e-3) and 3xTF32 (FP32 contract 1e-5), sampled rows
+    against the FP64 oracle, and the CUDA-graph replay bit-identical to it."""
+    pats = getattr(configs, name)
+    B = configs.VIT_BATCH if name.startswith("VIT") else configs.GPT2_BATCH
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    N = configs.chain_dims(pats)[0]
+    X = ksgen.x_normal(B, N, seed=0)
+    fs = [ksb.Factor(*p, k).set_math(ksb.MATH_TF32 if math == "tf32" else ksb.MATH_F32X3)
+          for p, k in zip(pats, K4s)]
+    assert all(f.plan(B, "bsf") == "tf32" for f in fs)
+    Xd = to_dev(X)
+    Y = ksb.chain(fs, Xd)
+    Yg = torch.empty_like(Y)
+    g = ksb.ChainGraph(fs, Xd, Yg)
+    g.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(Yg, Y)
+    g.free()
+    rows = np.array([0, 1, 127, 128, B // 2, B - 1])
+    Yref = O.chain(pats, K4s, X, rows=rows)
+    assert O.normwise_error(Y.cpu().numpy()[rows], Yref) <= (5e-3 if math == "tf32" else FP32_TOL)
