@@ -36,11 +36,11 @@ constexpr int WS_CWARPS = 8;           // warps per CTA, all compute
 constexpr int WS_THREADS = 32 * WS_CWARPS;
 
 // Warps split 2 x 4 (rows x outputs) for BN in {96, 128}: tile 128 rows, TN =
-// BN/16; BN = 64 uses 4 x 2 warps: tile 256 rows, TN = 8 (a 128 x 64 tile would
-// leave TN = 4: 3 shared loads per 32 FFMA instead of 4 per 64).
+// BN/16; BN in {48, 64} uses 4 x 2 warps: tile 256 rows, TN = 6 / 8 (a 128-row
+// tile would leave TN = 3 / 4: 3 shared loads per 32 FFMA instead of 4 per 64).
 template <int LAYOUT, int BN>
 struct WsCfg {
-    static constexpr int WM = BN == 64 ? 4 : 2;            // warps along the batch rows
+    static constexpr int WM = BN <= 64 ? 4 : 2;            // warps along the batch rows
     static constexpr int WN = 8 / WM;                      // warps along the outputs
     static constexpr int BMW = 64 * WM;                    // batch rows per tile
     static constexpr int TN = BN / (4 * WN);               // outputs per thread
@@ -50,7 +50,7 @@ struct WsCfg {
     static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
     static constexpr int BAR_OFF = S * SLOT;
     static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;     // full barriers, counters, align pad
-    static_assert(BN == 64 || BN == 96 || BN == 128, "TN in {6, 8}");
+    static_assert(BN == 48 || BN == 64 || BN == 96 || BN == 128, "TN in {6, 8}");
     static_assert(SLOT % 1024 == 0, "slot alignment (SWIZZLE_64B A tiles)");
     static_assert(S >= 3, "ring depth");
 };
@@ -300,7 +300,7 @@ cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
 }
 
 int pick_bn_ws(int64_t b) {
-    for (int bn : {128, 96, 64})
+    for (int bn : {128, 96, 64, 48})
         if (b % bn == 0) return bn;
     return 0;
 }
@@ -311,6 +311,7 @@ cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
         case 128: return launch_ws<LAYOUT, 128>(h, call);
         case 96: return launch_ws<LAYOUT, 96>(h, call);
         case 64: return launch_ws<LAYOUT, 64>(h, call);
+        case 48: return launch_ws<LAYOUT, 48>(h, call);
     }
     return cudaErrorInvalidValue;
 }
@@ -319,7 +320,7 @@ cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
 
 namespace ks {
 
-// BSL (any d) or BSF with d = 1; b a multiple of 64 or 96, c of 16; 16-byte
+// BSL (any d) or BSF with d = 1; b a multiple of 48 or 64, c of 16; 16-byte
 // aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 disables (experiments).
 bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
     static const bool enabled = [] {

@@ -25,7 +25,9 @@ class KSLinear(torch.nn.Module):
     def __init__(self, patterns, weights=None, bias: bool | torch.Tensor = True, layout: str = "bsf",
                  math_mode: str = "fp32", device="cuda", generator: torch.Generator | None = None):
         """patterns: [(a,b,c,d), ...] in product order K_1..K_L (a_l c_l d_l ==
-        a_{l+1} b_{l+1} d_{l+1}).  weights: matching list of
+        a_{l+1} b_{l+1} d_{l+1}).  math_mode: "fp32" (CUDA cores),
+        "tf32" or "f32x3" (FP32-accurate 3xTF32) on the tensor cores for factors
+        with b, c >= 16.  weights: matching list of
         canonical (a,b,c,d) float32 tensors/arrays, or None for the paper's
         initialisation U[-1/sqrt(c), 1/sqrt(c)]."""
         super().__init__()
@@ -47,8 +49,8 @@ class KSLinear(torch.nn.Module):
         for p, w in zip(patterns, weights):
             t = torch.as_tensor(w, dtype=torch.float32).contiguous().to(dev)
             f = ks.Factor(*p, t)
-            if math_mode == "tf32" and p[1] >= 16 and p[2] >= 16:
-                f.set_math(ks.MATH_TF32)
+            if math_mode in ("tf32", "f32x3") and p[1] >= 16 and p[2] >= 16:
+                f.set_math(ks.MATH_TF32 if math_mode == "tf32" else ks.MATH_F32X3)
             self.factors.append(f)
         if isinstance(bias, torch.Tensor):
             self.bias = torch.nn.Parameter(bias.detach().to(dev, torch.float32).contiguous(), requires_grad=False)
