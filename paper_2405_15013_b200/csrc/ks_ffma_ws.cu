@@ -260,6 +260,230 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
     }
 }
 
+// ---- BSF, d % 4 == 0: four consecutive j per tile, all four in every thread --
+// One TMA box {4 j, 17 l, 64 n} of X viewed as [B][a c][d] per chunk of 16 l
+// brings the d-strided columns of 4 KS blocks as 16-byte vectors (the 17th l is
+// padding: a staged row is 17 units of 16 bytes, so the 8 consecutive rows a
+// warp reads fall on 8 different bank groups).  Instead of transposing the
+// staged [n][l][j] chunk, every thread computes all 4 j for its rows: per l it
+// reads one float4 (4 j) per row and one K^T vector per j -- 8 shared loads per
+// 64 FFMA, no transposer, no extra shared-memory pass (a per-j variant that read
+// A element-wise needed 10 loads per 64 FFMA and was slower than the
+// register-staged kernel, profiles/r01_exp_ffma_wsj_negative.txt).
+// Tile: 64 batch rows x BN outputs x 4 j; warps 2 (rows) x 4 (outputs); thread
+// micro-tile 4 rows (ty + 8r) x 4 j x TK outputs, TK = BN / 16.
+constexpr int WSG_BM = 64;
+
+template <int TK>
+struct WsgCfg {
+    static constexpr int BN = 16 * TK;
+    static constexpr int PITCH = (WS_BK + 1) * 16;        // staged row: 17 l x 4 j floats
+    static constexpr int A_BYTES = WSG_BM * PITCH;         // 17 KB
+    static constexpr int BJ_BYTES = WS_BK * BN * 4;        // per j
+    static constexpr int SLOT0 = A_BYTES + 4 * BJ_BYTES;
+    static constexpr int SLOT = (SLOT0 + 1023) / 1024 * 1024;
+    static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
+    static constexpr int BAR_OFF = S * SLOT;
+    static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;
+    static_assert(TK == 2 || TK == 3 || TK == 4, "TK");
+    static_assert(S >= 3, "ring depth");
+};
+
+template <int TK>
+__global__ void __launch_bounds__(WS_THREADS, 2)
+ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                   float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                   int64_t ntiles) {
+    using C = WsgCfg<TK>;
+    constexpr int S = C::S;
+    constexpr int BN = C::BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t slot0 = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    const uint32_t full0 = smem_u32(&bars[0]);
+    const uint32_t cnt0 = smem_u32(&bars[8]);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nkc = b / BN;
+    const int njg = d / 4;
+    const int64_t nnb = (B + WSG_BM - 1) / WSG_BM;
+    const int nk = c / WS_BK;
+    const int64_t M = (int64_t)a * b * d;
+
+    // tile -> (k-chunk fastest, j-group, n-block, i): the k-chunks and j-groups of
+    // one X tile run on neighbouring CTAs at the same time and share it in L2
+    auto decode = [&](int64_t tile, int& i, int& j0, int& k0, int64_t& n0) {
+        k0 = (int)(tile % nkc) * BN;
+        tile /= nkc;
+        j0 = (int)(tile % njg) * 4;
+        tile /= njg;
+        n0 = (tile % nnb) * WSG_BM;
+        i = (int)(tile / nnb);
+    };
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t G = my_tiles * nk;
+    auto issue = [&](int64_t gx) {
+        int i, j0, k0;
+        int64_t n0;
+        decode(blockIdx.x + (gx / nk) * gridDim.x, i, j0, k0, n0);
+        const int st = (int)(gx % S);
+        const int l0 = (int)(gx % nk) * WS_BK;
+        const uint32_t sa = slot0 + st * C::SLOT;
+        mbar_expect_tx(full0 + 8 * st, C::A_BYTES + 4 * C::BJ_BYTES);
+        tma_3d(sa, &xmap, j0, i * c + l0, (int)n0, full0 + 8 * st);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+            tma_2d(sa + C::A_BYTES + jj * C::BJ_BYTES, &kmap, k0, (i * d + j0 + jj) * c + l0, full0 + 8 * st);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            asm volatile("st.shared.u32 [%0], 0;" ::"r"(cnt0 + 4 * s) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_launch_dependents();
+    if (tid == 0)
+        for (int64_t gx = 0; gx < S && gx < G; ++gx) issue(gx);
+
+    const int wm = warp >> 2, wn = warp & 3;
+    const int ty = lane >> 2, tx = lane & 3;
+    const int colB = wn * (4 * TK) + tx * TK;          // first of the thread's TK outputs
+    int64_t g = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int i, j0, k0;
+        int64_t n0;
+        decode(tile, i, j0, k0, n0);
+        float acc[4][4][TK];                              // [row r][j][output e]
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int e = 0; e < TK; ++e) acc[r][jj][e] = 0.f;
+        for (int t = 0; t < nk; ++t, ++g) {
+            const int st = (int)(g % S);
+            mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+            const uint32_t sa = slot0 + st * C::SLOT;
+            const uint32_t pa = sa + (wm * 32 + ty) * C::PITCH;        // rows wm*32 + ty + 8r
+            const uint32_t pb = sa + C::A_BYTES + colB * 4;
+#pragma unroll
+            for (int l = 0; l < WS_BK; ++l) {
+                float4 av[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(av[r].x), "=f"(av[r].y), "=f"(av[r].z), "=f"(av[r].w)
+                                 : "r"(pa + r * 8 * C::PITCH + l * 16));
+                float bv[4][TK];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const uint32_t q = pb + jj * C::BJ_BYTES + l * BN * 4;
+                    if constexpr (TK == 4) {
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(bv[jj][0]), "=f"(bv[jj][1]), "=f"(bv[jj][2]), "=f"(bv[jj][3]) : "r"(q));
+                    } else if constexpr (TK == 2) {
+                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(bv[jj][0]), "=f"(bv[jj][1]) : "r"(q));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < TK; ++e) bv[jj][e] = lds32(q + e * 4);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float x[4] = {av[r].x, av[r].y, av[r].z, av[r].w};
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                        for (int e = 0; e < TK; ++e) acc[r][jj][e] = fmaf(x[jj], bv[jj][e], acc[r][jj][e]);
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                uint32_t old;
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(cnt0 + 4 * st)
+                             : "memory");
+                if (old == WS_CWARPS - 1) {
+                    asm volatile("st.shared.u32 [%0], 0;" ::"r"(cnt0 + 4 * st) : "memory");
+                    if (g + S < G) issue(g + S);
+                }
+            }
+        }
+        // epilogue: the 4 j of one (row, output k) are one 16-byte run of Y
+        const int64_t rbase = (int64_t)i * b * d + (int64_t)(k0 + colB) * d + j0;
+        if (bias) {
+#pragma unroll
+            for (int e = 0; e < TK; ++e) {
+                const float4 bq = __ldg(reinterpret_cast<const float4*>(bias + rbase + (int64_t)e * d));
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    acc[r][0][e] += bq.x; acc[r][1][e] += bq.y; acc[r][2][e] += bq.z; acc[r][3][e] += bq.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t n = n0 + wm * 32 + ty + 8 * r;
+            if (n >= B) continue;
+            float* yr = Y + n * M + rbase;
+#pragma unroll
+            for (int e = 0; e < TK; ++e)
+                __stcs(reinterpret_cast<float4*>(yr + (int64_t)e * d),
+                       make_float4(acc[r][0][e], acc[r][1][e], acc[r][2][e], acc[r][3][e]));
+        }
+    }
+}
+
+template <int TK>
+cudaError_t launch_wsg(const ks_handle_s& h, const KsCall& call) {
+    using C = WsgCfg<TK>;
+    constexpr int BN = C::BN;
+    CUtensorMap xmap, kmap;
+    {
+        const cuuint64_t kd[2] = {(cuuint64_t)h.b, (cuuint64_t)(h.a * h.d * h.c)};
+        const cuuint64_t ks[1] = {(cuuint64_t)h.b * 4};
+        const cuuint32_t kb[2] = {BN, WS_BK};
+        if (!encode(&kmap, h.k_tile, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
+        const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
+        const cuuint32_t xb[3] = {4, WS_BK + 1, WSG_BM};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_ffma_wsg_kernel<TK>;
+    static bool attr[64] = {false};
+    if (!attr[h.device & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr[h.device & 63] = true;
+    }
+    const int64_t ntiles = (h.b / BN) * (h.d / 4) * ((call.B + WSG_BM - 1) / WSG_BM) * h.a;
+    int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
+    if (max_grid() > 0) slots = max_grid();
+    const int64_t grid = ntiles < slots ? ntiles : slots;
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(WS_THREADS), C::SMEM, call.stream, xmap, kmap,
+                                         call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
+    ks::count_launch();
+    return e;
+}
+
+// TK (outputs per thread per j) for the 4-j kernel: the widest of 4, 3, 2 with
+// 16 TK dividing b; 0 = unsupported.
+int pick_tk_wsg(int64_t b) {
+    for (int tk : {4, 3, 2})
+        if (b % (16 * tk) == 0) return tk;
+    return 0;
+}
+
 template <int LAYOUT, int BN>
 cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
     using C = WsCfg<LAYOUT, BN>;
@@ -320,16 +544,26 @@ cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
 
 namespace ks {
 
-// BSL (any d) or BSF with d = 1; b a multiple of 48 or 64, c of 16; 16-byte
-// aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 disables (experiments).
+// BSL (any d) or BSF with d = 1: b a multiple of 48 or 64.  BSF with d % 4 == 0:
+// b a multiple of 32 or 48 (four-j kernel), 16-byte aligned bias.  c a multiple
+// of 16; 16-byte aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 /
+// KS_FFMA_WSG=0 disable (experiments).
 bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
     static const bool enabled = [] {
         const char* e = getenv("KS_FFMA_WS");
         return !(e && atoi(e) == 0);
     }();
     if (!enabled || h.dtype != KS_DTYPE_F32) return false;
-    if (pick_bn_ws(h.b) == 0 || h.c % WS_BK != 0) return false;
-    if (call.layout != KS_LAYOUT_BSL && h.d != 1) return false;
+    if (call.layout == KS_LAYOUT_BSF && h.d > 1) {            // four-j kernel (d % 4 == 0)
+        static const bool gather_on = [] {
+            const char* e = getenv("KS_FFMA_WSG");
+            return !(e && atoi(e) == 0);
+        }();
+        if (!gather_on || h.d % 4 != 0 || pick_tk_wsg(h.b) == 0 || h.c % WS_BK != 0) return false;
+        if ((reinterpret_cast<uintptr_t>(call.bias) & 15) != 0) return false;
+    } else if (pick_bn_ws(h.b) == 0 || h.c % WS_BK != 0) {
+        return false;
+    }
     if (h.a * h.d * h.c >= (int64_t(1) << 31) || call.B >= (int64_t(1) << 31)) return false;
     const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
     if (al & 15) return false;
@@ -339,6 +573,14 @@ bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
 
 cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call) {
     if (call.layout == KS_LAYOUT_BSL) return launch_ws_layout<KS_LAYOUT_BSL>(h, call);
+    if (h.d > 1) {
+        switch (pick_tk_wsg(h.b)) {
+            case 4: return launch_wsg<4>(h, call);
+            case 3: return launch_wsg<3>(h, call);
+            case 2: return launch_wsg<2>(h, call);
+        }
+        return cudaErrorInvalidValue;
+    }
     return launch_ws_layout<KS_LAYOUT_BSF>(h, call);
 }
 
