@@ -23,6 +23,7 @@ def to_dev(a):
 
 
 FAMILIES = [((2, 3, 2, 3), "generic", "fp32"), ((4, 2, 2, 8), "stream", "fp32"), ((2, 64, 48, 4), "ffma", "fp32"),
+            ((1, 64, 48, 2), "ffma", "fp32"), ((3, 48, 64, 1), "ffma", "fp32"), ((1, 96, 64, 3), "ffma", "fp32"),
             ((1, 64, 64, 1), "tf32", "tf32"), ((2, 48, 48, 8), "tf32", "tf32"), ((1, 128, 128, 3), "tf32", "tf32"),
             ((1, 64, 48, 16), "tf32", "tf32"), ((1, 128, 128, 12), "tf32", "tf32")]
 
