@@ -484,36 +484,45 @@ int pick_tk_wsg(int64_t b) {
     return 0;
 }
 
-// ---- BSF, d = 2: both j per tile, every thread computes both -----------------
-// The 16 l x 2 j values of a chunk are one contiguous run of an X row: 2-D box
-// {36 floats, 128 n} (4 floats of padding: 9 16-byte units per staged row, so 8
-// consecutive rows fall on 8 bank groups).  A float4 of a staged row is
-// (l, j0), (l, j1), (l+1, j0), (l+1, j1): one shared load per row feeds two l
-// steps -- 12 shared loads per 128 FFMA for TK = 4.  Tile 128 rows x BN
-// outputs x 2 j; warps 2 (rows) x 4 (outputs); thread 8 rows (ty + 8r) x 2 j x TK.
-template <int TK>
-struct Ws2Cfg {
+// ---- BSF, d in {2, 3}: all d j per tile, every thread computes all of them ---
+// The 16 l x d j values of a chunk are one contiguous run of an X row: 2-D box
+// {16 d + 4 floats, RW n} (4 floats of padding: 4d + 1 16-byte units per staged
+// row, an odd number, so 8 consecutive rows fall on 8 bank groups).  Per group
+// of 4 l a row holds 4d floats = d float4s (element l' * d + j); a thread
+// loads them for each of its R rows plus one K^T vector per (l', j), and does
+// R x d x TK x 4 FFMA: 12 shared loads per 128 FFMA for d = 2 (R = 8) and 24
+// per 192 for d = 3 (R = 4).  Tile RW = 16 R rows x BN outputs x d j; warps 2
+// (rows) x 4 (outputs); thread rows ty + 8r (r < R).  The epilogue writes the
+// d TK consecutive outputs of a row as float4s.
+template <int D, int TK>
+struct WscCfg {
+    static constexpr int R = D == 2 ? 8 : 4;               // rows per thread
+    static constexpr int RW = 16 * R;                      // rows per tile
     static constexpr int BN = 16 * TK;
-    static constexpr int PITCH = (2 * WS_BK + 4) * 4;      // 144 B
-    static constexpr int A_BYTES = BM * PITCH;             // 18 KB
+    static constexpr int PITCH = (WS_BK * D + 4) * 4;
+    static constexpr int A_BYTES = RW * PITCH;
     static constexpr int BJ_BYTES = WS_BK * BN * 4;
-    static constexpr int SLOT0 = A_BYTES + 2 * BJ_BYTES;
+    static constexpr int SLOT0 = A_BYTES + D * BJ_BYTES;
     static constexpr int SLOT = (SLOT0 + 1023) / 1024 * 1024;
     static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
     static constexpr int BAR_OFF = S * SLOT;
     static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;
+    static_assert(D == 2 || D == 3, "D");
     static_assert(TK == 2 || TK == 3 || TK == 4, "TK");
+    static_assert((D * TK) % 2 == 0, "float2 epilogue units");
     static_assert(S >= 3, "ring depth");
 };
 
-template <int TK>
+template <int D, int TK>
 __global__ void __launch_bounds__(WS_THREADS, 2)
-ks_ffma_ws2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+ks_ffma_wsc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                    float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c,
                    int64_t ntiles) {
-    using C = Ws2Cfg<TK>;
+    using C = WscCfg<D, TK>;
     constexpr int S = C::S;
     constexpr int BN = C::BN;
+    constexpr int R = C::R;
+    constexpr int RW = C::RW;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t slot0 = smem_u32(smem);
@@ -524,14 +533,14 @@ ks_ffma_ws2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nkc = b / BN;
-    const int64_t nnb = (B + BM - 1) / BM;
+    const int64_t nnb = (B + RW - 1) / RW;
     const int nk = c / WS_BK;
-    const int64_t M = (int64_t)a * b * 2;
+    const int64_t M = (int64_t)a * b * D;
 
     auto decode = [&](int64_t tile, int& i, int& k0, int64_t& n0) {   // k-chunk fastest, n-block, i
         k0 = (int)(tile % nkc) * BN;
         tile /= nkc;
-        n0 = (tile % nnb) * BM;
+        n0 = (tile % nnb) * RW;
         i = (int)(tile / nnb);
     };
     const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
@@ -543,11 +552,11 @@ ks_ffma_ws2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         const int st = (int)(gx % S);
         const int l0 = (int)(gx % nk) * WS_BK;
         const uint32_t sa = slot0 + st * C::SLOT;
-        mbar_expect_tx(full0 + 8 * st, C::A_BYTES + 2 * C::BJ_BYTES);
-        tma_2d(sa, &xmap, (i * c + l0) * 2, (int)n0, full0 + 8 * st);
+        mbar_expect_tx(full0 + 8 * st, C::A_BYTES + D * C::BJ_BYTES);
+        tma_2d(sa, &xmap, (i * c + l0) * D, (int)n0, full0 + 8 * st);
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj)
-            tma_2d(sa + C::A_BYTES + jj * C::BJ_BYTES, &kmap, k0, (i * 2 + jj) * c + l0, full0 + 8 * st);
+        for (int jj = 0; jj < D; ++jj)
+            tma_2d(sa + C::A_BYTES + jj * C::BJ_BYTES, &kmap, k0, (i * D + jj) * c + l0, full0 + 8 * st);
     };
 
     if (tid == 0) {
@@ -573,27 +582,27 @@ ks_ffma_ws2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         int i, k0;
         int64_t n0;
         decode(tile, i, k0, n0);
-        float acc[8][2][TK];
+        float acc[R][D][TK];
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
+            for (int jj = 0; jj < D; ++jj)
 #pragma unroll
                 for (int e = 0; e < TK; ++e) acc[r][jj][e] = 0.f;
         for (int t = 0; t < nk; ++t, ++g) {
             const int st = (int)(g % S);
             mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
             const uint32_t sa = slot0 + st * C::SLOT;
-            const uint32_t pa = sa + (wm * 64 + ty) * C::PITCH;        // rows wm*64 + ty + 8r
+            const uint32_t pa = sa + (wm * (8 * R) + ty) * C::PITCH;       // rows wm*8R + ty + 8r
             const uint32_t pb = sa + C::A_BYTES + colB * 4;
 #pragma unroll
-            for (int lp = 0; lp < WS_BK / 2; ++lp) {
-                float bv[2][2][TK];                       // [l of the pair][j][e]
+            for (int lq = 0; lq < WS_BK / 4; ++lq) {
+                float bv[4][D][TK];                       // [l' of the quad][j][e]
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+                for (int h = 0; h < 4; ++h)
 #pragma unroll
-                    for (int jj = 0; jj < 2; ++jj) {
-                        const uint32_t q = pb + jj * C::BJ_BYTES + (2 * lp + h) * BN * 4;
+                    for (int jj = 0; jj < D; ++jj) {
+                        const uint32_t q = pb + jj * C::BJ_BYTES + (4 * lq + h) * BN * 4;
                         if constexpr (TK == 4) {
                             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                          : "=f"(bv[h][jj][0]), "=f"(bv[h][jj][1]), "=f"(bv[h][jj][2]), "=f"(bv[h][jj][3])
@@ -606,17 +615,20 @@ ks_ffma_ws2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                         }
                     }
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    float4 av;
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(av.x), "=f"(av.y), "=f"(av.z), "=f"(av.w) : "r"(pa + r * 8 * C::PITCH + lp * 16));
-                    const float x[2][2] = {{av.x, av.y}, {av.z, av.w}};      // [l of the pair][j]
+                for (int r = 0; r < R; ++r) {
+                    float x[4 * D];                       // x[l' * D + j]
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
+                    for (int u = 0; u < D; ++u)
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(x[4 * u]), "=f"(x[4 * u + 1]), "=f"(x[4 * u + 2]), "=f"(x[4 * u + 3])
+                                     : "r"(pa + r * 8 * C::PITCH + (lq * D + u) * 16));
 #pragma unroll
-                        for (int jj = 0; jj < 2; ++jj)
+                    for (int h = 0; h < 4; ++h)
 #pragma unroll
-                            for (int e = 0; e < TK; ++e) acc[r][jj][e] = fmaf(x[h][jj], bv[h][jj][e], acc[r][jj][e]);
+                        for (int jj = 0; jj < D; ++jj)
+#pragma unroll
+                            for (int e = 0; e < TK; ++e)
+                                acc[r][jj][e] = fmaf(x[h * D + jj], bv[h][jj][e], acc[r][jj][e]);
                 }
             }
             fence_proxy_async();
@@ -631,33 +643,37 @@ ks_ffma_ws2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                 }
             }
         }
-        // epilogue: outputs (k, j) for k in [k0+colB, +TK), j in {0, 1} are 2 TK consecutive floats
-        const int64_t rbase = (int64_t)i * b * 2 + (int64_t)(k0 + colB) * 2;
+        // epilogue: outputs (k, j), k in [k0+colB, +TK), j < D, are D TK consecutive floats
+        const int64_t rbase = (int64_t)i * b * D + (int64_t)(k0 + colB) * D;
         if (bias) {
 #pragma unroll
             for (int e = 0; e < TK; ++e)
 #pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    const float bq = __ldg(bias + rbase + 2 * e + jj);
+                for (int jj = 0; jj < D; ++jj) {
+                    const float bq = __ldg(bias + rbase + D * e + jj);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) acc[r][jj][e] += bq;
+                    for (int r = 0; r < R; ++r) acc[r][jj][e] += bq;
                 }
         }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int64_t n = n0 + wm * 64 + ty + 8 * r;
+        for (int r = 0; r < R; ++r) {
+            const int64_t n = n0 + wm * (8 * R) + ty + 8 * r;
             if (n >= B) continue;
             float* yr = Y + n * M + rbase;
+            float o[D * TK];
 #pragma unroll
             for (int e = 0; e < TK; ++e)
-                __stcs(reinterpret_cast<float2*>(yr + 2 * e), make_float2(acc[r][0][e], acc[r][1][e]));
+#pragma unroll
+                for (int jj = 0; jj < D; ++jj) o[D * e + jj] = acc[r][jj][e];
+#pragma unroll
+            for (int u = 0; u < D * TK; u += 2) __stcs(reinterpret_cast<float2*>(yr + u), make_float2(o[u], o[u + 1]));
         }
     }
 }
 
-template <int TK>
-cudaError_t launch_ws2(const ks_handle_s& h, const KsCall& call) {
-    using C = Ws2Cfg<TK>;
+template <int D, int TK>
+cudaError_t launch_wsc(const ks_handle_s& h, const KsCall& call) {
+    using C = WscCfg<D, TK>;
     constexpr int BN = C::BN;
     CUtensorMap xmap, kmap;
     {
@@ -669,17 +685,17 @@ cudaError_t launch_ws2(const ks_handle_s& h, const KsCall& call) {
     {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
-        const cuuint32_t xb[2] = {2 * WS_BK + 4, BM};
+        const cuuint32_t xb[2] = {(cuuint32_t)(WS_BK * D + 4), (cuuint32_t)C::RW};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_ffma_ws2_kernel<TK>;
+    auto kern = ks_ffma_wsc_kernel<D, TK>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         attr[h.device & 63] = true;
     }
-    const int64_t ntiles = (h.b / BN) * ((call.B + BM - 1) / BM) * h.a;
+    const int64_t ntiles = (h.b / BN) * ((call.B + C::RW - 1) / C::RW) * h.a;
     int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
@@ -687,6 +703,23 @@ cudaError_t launch_ws2(const ks_handle_s& h, const KsCall& call) {
                                          call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, ntiles);
     ks::count_launch();
     return e;
+}
+
+// TK for the all-j kernel: as pick_tk_wsg, but d TK even (float2 epilogue units).
+int pick_tk_wsc(int64_t b, int64_t d) {
+    for (int tk : {4, 3, 2})
+        if (b % (16 * tk) == 0 && (d * tk) % 2 == 0) return tk;
+    return 0;
+}
+
+template <int D>
+cudaError_t launch_wsc_tk(const ks_handle_s& h, const KsCall& call) {
+    switch (pick_tk_wsc(h.b, D)) {
+        case 4: return launch_wsc<D, 4>(h, call);
+        case 3: if constexpr ((D * 3) % 2 == 0) return launch_wsc<D, 3>(h, call); break;
+        case 2: return launch_wsc<D, 2>(h, call);
+    }
+    return cudaErrorInvalidValue;
 }
 
 template <int LAYOUT, int BN>
@@ -750,8 +783,8 @@ cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
 namespace ks {
 
 // BSL (any d) or BSF with d = 1: b a multiple of 48 or 64.  BSF with d % 4 == 0
-// (four-j kernel, 16-byte aligned bias) or d = 2 (two-j kernel): b a multiple of
-// 32 or 48.  c a multiple
+// (four-j kernel, 16-byte aligned bias) or d in {2, 3} (all-j contiguous kernel):
+// b a multiple of 32 or 48 (d = 3: of 32).  c a multiple
 // of 16; 16-byte aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 /
 // KS_FFMA_WSG=0 disable (experiments).
 bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
@@ -765,7 +798,8 @@ bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
             const char* e = getenv("KS_FFMA_WSG");
             return !(e && atoi(e) == 0);
         }();
-        if (!gather_on || (h.d % 4 != 0 && h.d != 2) || pick_tk_wsg(h.b) == 0 || h.c % WS_BK != 0) return false;
+        if (!gather_on || h.c % WS_BK != 0) return false;
+        if (h.d % 4 == 0 ? pick_tk_wsg(h.b) == 0 : (h.d > 3 || pick_tk_wsc(h.b, h.d) == 0)) return false;
         if (h.d % 4 == 0 && (reinterpret_cast<uintptr_t>(call.bias) & 15) != 0) return false;
     } else if (pick_bn_ws(h.b) == 0 || h.c % WS_BK != 0) {
         return false;
@@ -779,14 +813,8 @@ bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
 
 cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call) {
     if (call.layout == KS_LAYOUT_BSL) return launch_ws_layout<KS_LAYOUT_BSL>(h, call);
-    if (h.d == 2) {                                         // both j per thread
-        switch (pick_tk_wsg(h.b)) {
-            case 4: return launch_ws2<4>(h, call);
-            case 3: return launch_ws2<3>(h, call);
-            case 2: return launch_ws2<2>(h, call);
-        }
-        return cudaErrorInvalidValue;
-    }
+    if (h.d == 2) return launch_wsc_tk<2>(h, call);        // all d j per thread
+    if (h.d == 3) return launch_wsc_tk<3>(h, call);
     if (h.d > 1) {
         switch (pick_tk_wsg(h.b)) {
             case 4: return launch_wsg<4>(h, call);
