@@ -680,8 +680,9 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 // of J accumulators (2 x J x BN <= 512 TMEM columns); the epilogue stores
 // through warp_store_rows (coalesced 16-byte units).
 // ==========================================================================
-constexpr int BKH = 16;                        // l per stage (one UMMA k-step of 32 B)
-constexpr int AH_BYTES = BM * BKH * 2;         // 4 KB per j
+// HK = l per stage: 16 (32-byte SWIZZLE_32B operand rows, one K = 16 MMA) or
+// 32 (64-byte SWIZZLE_64B rows, two MMAs) -- 32 halves the per-stage barrier /
+// transposer / TMA-issue overhead per byte and is used when c % 32 == 0 and J <= 4.
 
 // JB = j extent of the X box: J, or 8 for J = 4 when d % 8 != 0.  A 4-half
 // box row would be 8 bytes (TMA's minimum is 16) and a 3-D view needs the l
@@ -689,12 +690,14 @@ constexpr int AH_BYTES = BM * BKH * 2;         // 4 KB per j
 // 16 2-D boxes {8 halves, 128 n} per stage, one per l, stacked [l][n][8]
 // (the transposers use the first 4 of the 8 j; the rest is the next j-group's,
 // served from L2).
-template <int J, int BN, int JB = J>
+template <int J, int BN, int JB = J, int HK = 16>
 struct HalfJCfg {
     static constexpr bool PER_L = JB != J;
-    static constexpr int PITCH = PER_L ? 16 : 32 * JB + 16;   // staged row: [16 l][JB] halves + 16 B
-    static constexpr int STG = PER_L ? BKH * BM * 16 : BM * PITCH;
-    static constexpr int BJ_BYTES = BN * BKH * 2;         // per j, BN * 32 B
+    static constexpr int RB = 2 * HK;                     // operand row bytes
+    static constexpr int AH_BYTES = BM * RB;              // A tile per j
+    static constexpr int PITCH = PER_L ? 16 : RB * JB + 16;   // staged row: [HK l][JB] halves + 16 B
+    static constexpr int STG = PER_L ? HK * BM * 16 : BM * PITCH;
+    static constexpr int BJ_BYTES = BN * RB;              // per j
     static constexpr int SLOT = J * (AH_BYTES + BJ_BYTES);
     static constexpr int EC = J > 4 ? 8 : 16;             // epilogue columns per TMEM load
     static constexpr int SCR = 4 * WarpStore<__half, J, EC>::BYTES;     // epilogue store scratch
@@ -713,14 +716,17 @@ struct HalfJCfg {
     static_assert((2 * S + 4 + 2 * P) * 8 + 4 <= 256, "barrier area");
     static_assert(S >= 2, "pipeline too shallow");
     static_assert(SMEM <= 227 * 1024, "shared memory");
+    static_assert(HK == 16 || (HK == 32 && !PER_L && J <= 4), "HK = 32: contiguous / gather boxes, J <= 4");
 };
 
-template <typename T, int J, int BN, int JB = J>
+template <typename T, int J, int BN, int JB = J, int HK = 16>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
                     int64_t ntiles) {
-    using C = HalfJCfg<J, BN, JB>;
+    using C = HalfJCfg<J, BN, JB, HK>;
+    constexpr int AH_BYTES = C::AH_BYTES;
+    constexpr int RB = C::RB;
     constexpr int S = C::S;
     constexpr int P = C::P;
     extern __shared__ uint8_t smem_raw[];
@@ -745,7 +751,7 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     const bool contig = (J == d);                 // 2-D box over X rows, else 3-D {8 j, 17 l, n}
     const int64_t nnb = (B + BM - 1) / BM;
     const int64_t M = (int64_t)a * b * d;
-    const int nk = c / BKH;                       // c % 16 == 0
+    const int nk = c / HK;                        // c % HK == 0
     const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t G = my_tiles * nk;
 
@@ -782,13 +788,13 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         if (lane == 0) {
             auto issue_x = [&](int64_t gx) {
                 const TileJ tc = decode_j(blockIdx.x + (gx / nk) * gridDim.x, nkc, njg, nnb, BN, J);
-                const int l0 = (int)(gx % nk) * BKH;
+                const int l0 = (int)(gx % nk) * HK;
                 const int p = (int)(gx % P);
                 if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
                 mbar_expect_tx(sfull0 + 8 * p, C::STG);
                 if constexpr (C::PER_L) {
 #pragma unroll 1
-                    for (int l = 0; l < BKH; ++l)
+                    for (int l = 0; l < HK; ++l)
                         tma_2d(stg0 + p * C::STG + l * (BM * 16), &xmap, ((tc.i * c + l0 + l) * d + tc.j0) & ~7,
                                tc.n0, sfull0 + 8 * p);   // 16-byte aligned start (required)
                 } else if (contig) {
@@ -801,7 +807,7 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             for (int64_t g = 0; g < G; ++g) {
                 if (g + P - 1 < G) issue_x(g + P - 1);
                 const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
-                const int l0 = (int)(g % nk) * BKH;
+                const int l0 = (int)(g % nk) * HK;
                 const int st = (int)(g % S);
                 if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
                 mbar_expect_tx(full0 + 8 * st, J * C::BJ_BYTES);
@@ -813,55 +819,55 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     } else if (warp <= 4) {
         // staging row r: [16 l][J] halves -> J K-major SW32 A rows of 16 halves
         const int r = tid - 32;
-        const uint32_t rowoff = (uint32_t)((r / 8) * 256 + (r % 8) * 32);
-        const int sw = (r % 8) / 4;
+        const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
+        const int sw = RB == 64 ? (r % 8) / 2 : (r % 8) / 4;     // SW64 / SW32 chunk XOR
         for (int64_t g = 0; g < G; ++g) {
             const int p = (int)(g % P);
             mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
-            uint32_t w[8 * JB];
+            uint32_t w[HK / 2 * JB];
             const uint32_t src = stg0 + p * C::STG + r * C::PITCH;
-            // 16-byte unit q of the virtual row [16 l][JB]: contiguous, or (per-l boxes) l = q at l * 2 KB
+            // 16-byte unit q of the virtual row [HK l][JB]: contiguous, or (per-l boxes) l = q at l * 2 KB
             constexpr uint32_t QSTRIDE = C::PER_L ? BM * 16 : 16;
 #pragma unroll
-            for (int q = 0; q < 2 * JB; ++q)
+            for (int q = 0; q < HK / 8 * JB; ++q)
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(w[4 * q]), "=r"(w[4 * q + 1]), "=r"(w[4 * q + 2]), "=r"(w[4 * q + 3])
                              : "r"(src + q * QSTRIDE));
             fence_proxy_async();          // generic reads before the TMA (async proxy) refill
             mbar_arrive(sempty0 + 8 * p);
-            // virtual row [16 l][J] halves, as 32-bit words
-            uint32_t wv[8 * J];
+            // virtual row [HK l][J] halves, as 32-bit words
+            uint32_t wv[HK / 2 * J];
             if constexpr (C::PER_L) {
                 // box l starts at the 16-byte-aligned column below (i c + l0 + l) d + j0; the
                 // 4 wanted halves sit at offset 0 or 4 (d, j0 multiples of 4): words 0-1 or 2-3
                 const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
-                const int col0 = (tc.i * c + (int)(g % nk) * BKH) * d + tc.j0;
+                const int col0 = (tc.i * c + (int)(g % nk) * HK) * d + tc.j0;
 #pragma unroll
-                for (int l = 0; l < BKH; ++l) {
+                for (int l = 0; l < HK; ++l) {
                     const bool hi4 = ((col0 + l * d) & 4) != 0;
                     wv[2 * l] = hi4 ? w[4 * l + 2] : w[4 * l];
                     wv[2 * l + 1] = hi4 ? w[4 * l + 3] : w[4 * l + 1];
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < 8 * J; ++q) wv[q] = w[q];
+                for (int q = 0; q < HK / 2 * J; ++q) wv[q] = w[q];
             }
             const int st = (int)(g % S);
             if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
             const uint32_t sa = slot0 + st * C::SLOT + rowoff;
 #pragma unroll
             for (int jj = 0; jj < J; ++jj) {
-                uint32_t o[8];
+                uint32_t o[HK / 2];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {         // halves l = 2q, 2q+1 of column jj
+                for (int q = 0; q < HK / 2; ++q) {    // halves l = 2q, 2q+1 of column jj
                     const int e0 = (2 * q) * J + jj, e1 = (2 * q + 1) * J + jj;
                     const uint32_t sel = (e0 & 1 ? 0x32u : 0x10u) | ((e1 & 1 ? 0x76u : 0x54u) << 8);
                     o[q] = __byte_perm(wv[e0 >> 1], wv[e1 >> 1], sel);
                 }
-                sts128(sa + jj * AH_BYTES + ((0 ^ sw) * 16), __uint_as_float(o[0]), __uint_as_float(o[1]),
-                       __uint_as_float(o[2]), __uint_as_float(o[3]));
-                sts128(sa + jj * AH_BYTES + ((1 ^ sw) * 16), __uint_as_float(o[4]), __uint_as_float(o[5]),
-                       __uint_as_float(o[6]), __uint_as_float(o[7]));
+#pragma unroll
+                for (int ch = 0; ch < HK / 8; ++ch)
+                    sts128(sa + jj * AH_BYTES + ((ch ^ sw) * 16), __uint_as_float(o[4 * ch]),
+                           __uint_as_float(o[4 * ch + 1]), __uint_as_float(o[4 * ch + 2]), __uint_as_float(o[4 * ch + 3]));
             }
             fence_proxy_async();
             mbar_arrive(full0 + 8 * st);
@@ -882,8 +888,16 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     const uint32_t sb = sa + J * AH_BYTES;
 #pragma unroll
                     for (int jj = 0; jj < J; ++jj)
-                        mma_f16(tmem + (uint32_t)((ab * J + jj) * BN), sw32_desc(sa + jj * AH_BYTES),
-                                sw32_desc(sb + jj * C::BJ_BYTES), idesc, t > 0 ? 1u : 0u);
+#pragma unroll
+                        for (int s = 0; s < HK / 16; ++s) {   // K = 16 halves = 32 B per MMA
+                            const uint32_t ah = sa + jj * AH_BYTES + 32 * s, bh = sb + jj * C::BJ_BYTES + 32 * s;
+                            if constexpr (HK == 32)
+                                mma_f16(tmem + (uint32_t)((ab * J + jj) * BN), sw64_desc(ah), sw64_desc(bh), idesc,
+                                        (t > 0 || s > 0) ? 1u : 0u);
+                            else
+                                mma_f16(tmem + (uint32_t)((ab * J + jj) * BN), sw32_desc(ah), sw32_desc(bh), idesc,
+                                        t > 0 ? 1u : 0u);
+                        }
                     mma_commit(empty0 + 8 * st);
                 }
                 mma_commit(accf0 + 8 * ab);
@@ -1146,16 +1160,17 @@ int pick_bn_half(int64_t b, int J) {
     return 0;
 }
 
-template <typename T, int J, int BN, int JB = J>
+template <typename T, int J, int BN, int JB = J, int HK = 16>
 cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
-    using C = HalfJCfg<J, BN, JB>;
+    using C = HalfJCfg<J, BN, JB, HK>;
+    constexpr CUtensorMapSwizzle SWH = HK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     const CUtensorMapDataType dt = ElemTraits<T>::tma;
     CUtensorMap xmap, kmap;
     {
         const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
         const cuuint64_t ks[1] = {(cuuint64_t)h.c * 2};
-        const cuuint32_t kb[2] = {BKH, BN};
-        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_32B, dt)) return cudaErrorInvalidValue;
+        const cuuint32_t kb[2] = {HK, BN};
+        if (!encode(&kmap, h.k_tf32, 2, kd, ks, kb, SWH, dt)) return cudaErrorInvalidValue;
     }
     if (C::PER_L) {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
@@ -1165,15 +1180,15 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
     } else if (J == h.d) {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * 2};
-        const cuuint32_t xb[2] = {(cuuint32_t)(BKH * J + 8), BM};
+        const cuuint32_t xb[2] = {(cuuint32_t)(HK * J + 8), BM};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
     } else {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 2, (cuuint64_t)h.N * 2};
-        const cuuint32_t xb[3] = {(cuuint32_t)JB, BKH + 1, BM};
+        const cuuint32_t xb[3] = {(cuuint32_t)JB, HK + 1, BM};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_half_bsfj_kernel<T, J, BN, JB>;
+    auto kern = ks_half_bsfj_kernel<T, J, BN, JB, HK>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1191,17 +1206,26 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
-template <typename T, int J, int JB = J>
-cudaError_t launch_halfj_bn(const ks_handle_s& h, const KsCall& call) {
+template <typename T, int J, int JB, int HK>
+cudaError_t launch_halfj_bn_hk(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn_half(h.b, J)) {
-        case 128: if constexpr (J * 128 <= 256) return launch_halfj<T, J, 128, JB>(h, call); break;
-        case 96: if constexpr (J * 96 <= 256) return launch_halfj<T, J, 96, JB>(h, call); break;
-        case 64: if constexpr (J * 64 <= 256) return launch_halfj<T, J, 64, JB>(h, call); break;
-        case 48: if constexpr (J * 48 <= 256) return launch_halfj<T, J, 48, JB>(h, call); break;
-        case 32: if constexpr (J * 32 <= 256) return launch_halfj<T, J, 32, JB>(h, call); break;
-        case 16: return launch_halfj<T, J, 16, JB>(h, call);
+        case 128: if constexpr (J * 128 <= 256) return launch_halfj<T, J, 128, JB, HK>(h, call); break;
+        case 96: if constexpr (J * 96 <= 256) return launch_halfj<T, J, 96, JB, HK>(h, call); break;
+        case 64: if constexpr (J * 64 <= 256) return launch_halfj<T, J, 64, JB, HK>(h, call); break;
+        case 48: if constexpr (J * 48 <= 256) return launch_halfj<T, J, 48, JB, HK>(h, call); break;
+        case 32: if constexpr (J * 32 <= 256) return launch_halfj<T, J, 32, JB, HK>(h, call); break;
+        case 16: return launch_halfj<T, J, 16, JB, HK>(h, call);
     }
     return cudaErrorInvalidValue;
+}
+
+// 32 l per stage when c allows it and the staging row stays small (J <= 4, no per-l boxes)
+template <typename T, int J, int JB = J>
+cudaError_t launch_halfj_bn(const ks_handle_s& h, const KsCall& call) {
+    if constexpr (J <= 4 && JB == J) {
+        if (h.c % 32 == 0) return launch_halfj_bn_hk<T, J, JB, 32>(h, call);
+    }
+    return launch_halfj_bn_hk<T, J, JB, 16>(h, call);
 }
 
 template <typename T>

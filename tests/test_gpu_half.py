@@ -51,7 +51,9 @@ CASES = [((1, 64, 64, 1), "bsf"), ((6, 64, 256, 1), "bsf"), ((2, 128, 128, 1), "
          ((2, 128, 64, 2), "bsf"), ((1, 48, 48, 3), "bsf"), ((3, 64, 64, 4), "bsf"), ((1, 96, 96, 6), "bsf"),
          ((1, 64, 64, 8), "bsf"), ((1, 32, 48, 16), "bsf"), ((2, 16, 16, 24), "bsf"),
          # d % 4 == 0, d % 8 != 0: J = 4 out of an 8-wide box, per-row 8-byte stores
-         ((1, 48, 64, 12), "bsf"), ((2, 64, 64, 12), "bsf"), ((1, 32, 32, 20), "bsf")]
+         ((1, 48, 64, 12), "bsf"), ((2, 64, 64, 12), "bsf"), ((1, 32, 32, 20), "bsf"),
+         # c % 32 == 0, J <= 4: 32 l per stage (SWIZZLE_64B operand rows)
+         ((2, 64, 96, 3), "bsf"), ((1, 96, 64, 2), "bsf"), ((2, 128, 128, 4), "bsf"), ((1, 32, 64, 4), "bsf")]
 
 
 @pytest.mark.parametrize("name", ["bf16", "f16"])
