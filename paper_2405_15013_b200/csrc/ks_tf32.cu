@@ -1047,6 +1047,16 @@ BsfjPlan pick_bsfj(const ks_handle_s& h) {
     } else {
         return p;
     }
+    // BN = 256 (UMMA N maximum) only for wide blocks with J = 2 (b = 768 in ViT-S UP):
+    // it halves the L2 re-reads of X across output chunks; KS_BSFJ_BN256=0 disables
+    static const bool bn256 = [] {
+        const char* e = getenv("KS_BSFJ_BN256");
+        return !(e && atoi(e) == 0);
+    }();
+    if (bn256 && !x3 && p.J == 2 && h.b > 128 && h.b % 256 == 0) {
+        p.BN = 256;
+        return p;
+    }
     for (int bn : {128, 96, 64, 48, 32, 16})
         if (h.b % bn == 0 && p.J * bn <= 512) {
             p.BN = bn;
@@ -1114,6 +1124,7 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
 template <int J, bool X3, bool GATHER>
 cudaError_t launch_bsfj_bn(const ks_handle_s& h, const KsCall& call, int BN) {
     switch (BN) {
+        case 256: if constexpr (J == 2 && !X3 && !GATHER) return launch_bsfj<J, 256, X3, GATHER>(h, call); break;
         case 128: if constexpr (J * 128 <= 512) return launch_bsfj<J, 128, X3, GATHER>(h, call); break;
         case 96: if constexpr (J * 96 <= 512) return launch_bsfj<J, 96, X3, GATHER>(h, call); break;
         case 64: return launch_bsfj<J, 64, X3, GATHER>(h, call);
