@@ -35,43 +35,42 @@ struct FusedFactor {
 struct FusedParams {
     FusedFactor f[MAXF];   // application order (K_L first)
     int pass_len[MAXF];    // number of factors in each pass (1..3), passes in order
+    int pass_first[MAXF];  // index in f of each pass's first factor
     int npass;
     int N;                 // row length (all dims equal)
+    int resident;          // number of radix-8 passes whose weights live in TMEM (0..2)
+    int res_pass[2];       // which passes (the TMEM slot is the index in this list)
 };
 
-// One radix-2^T pass over all rows of the tile, T consecutive dyadic factors
-// (b = c = 2) with d, 2d, 4d.
+// Weights of one radix-2^T item (T consecutive dyadic factors, b = c = 2, with
+// d0, 2 d0, 4 d0): kw[t][p][kl] = K4[i][k][l][jt] of factor t, pair p (bit t of
+// the element index m cleared), kl = 2k + l.
 template <int T>
-__device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const FusedFactor* F) {
+__device__ __forceinline__ void dyadic_load(const FusedFactor* F, int it, float (&kw)[T][(1 << T) / 2][4]) {
     constexpr int E = 1 << T;
     const int d0 = F[0].d;
-    const int nitem = N / E;                      // (super-block of the last factor, j) pairs
-    for (int it = threadIdx.x; it < nitem; it += THREADS) {
-        const int j = it % d0;
-        const int blk = it / d0;                  // super-block of size E*d0
-        const int base = blk * (E * d0) + j;
-        // weights: for factor t, pair p (bit t of m = 0), K4[i][k][l][jt]
-        float kw[T][E / 2][4];
-        if (d0 == 1) {
-            // the item's weights of factor t are one 2^(T+1)-float run starting at
-            // blk * 2^(T+1): vector loads; offset of (pair p, k, l) inside the run is
-            // (p >> t) * 4 * 2^t + (2k + l) * 2^t + (p mod 2^t)
+    const int j = it % d0;
+    const int blk = it / d0;                      // super-block of size E*d0
+    if (d0 == 1) {
+        // the item's weights of factor t are one 2^(T+1)-float run starting at
+        // blk * 2^(T+1): vector loads; offset of (pair p, k, l) inside the run is
+        // (p >> t) * 4 * 2^t + (2k + l) * 2^t + (p mod 2^t)
 #pragma unroll
-            for (int t = 0; t < T; ++t) {
-                float kk[2 * E];
-                const float4* src = reinterpret_cast<const float4*>(F[t].k + (int64_t)blk * (2 * E));
+        for (int t = 0; t < T; ++t) {
+            float kk[2 * E];
+            const float4* src = reinterpret_cast<const float4*>(F[t].k + (int64_t)blk * (2 * E));
 #pragma unroll
-                for (int q = 0; q < E / 2; ++q) {
-                    const float4 w = __ldg(src + q);
-                    kk[4 * q] = w.x; kk[4 * q + 1] = w.y; kk[4 * q + 2] = w.z; kk[4 * q + 3] = w.w;
-                }
-#pragma unroll
-                for (int p = 0; p < E / 2; ++p)
-#pragma unroll
-                    for (int kl = 0; kl < 4; ++kl)
-                        kw[t][p][kl] = kk[(p >> t) * 4 * (1 << t) + kl * (1 << t) + (p & ((1 << t) - 1))];
+            for (int q = 0; q < E / 2; ++q) {
+                const float4 w = __ldg(src + q);
+                kk[4 * q] = w.x; kk[4 * q + 1] = w.y; kk[4 * q + 2] = w.z; kk[4 * q + 3] = w.w;
             }
-        } else
+#pragma unroll
+            for (int p = 0; p < E / 2; ++p)
+#pragma unroll
+                for (int kl = 0; kl < 4; ++kl)
+                    kw[t][p][kl] = kk[(p >> t) * 4 * (1 << t) + kl * (1 << t) + (p & ((1 << t) - 1))];
+        }
+    } else {
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             const int dt = d0 << t;
@@ -91,41 +90,101 @@ __device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const Fu
                 kw[t][p][3] = __ldg(kp + 3 * dt);     // k=1,l=1
             }
         }
-        for (int r = 0; r < rows; ++r) {
-            float* row = sm + (size_t)r * N + base;
-            float v[E];
-            if (d0 == 1) {                         // E consecutive floats: vector shared loads
+    }
+}
+
+// Apply an item's T factors to its E elements {base + m*d0} of every row.
+template <int T>
+__device__ __forceinline__ void dyadic_apply(float* sm, int rows, int N, int d0, int it,
+                                             const float (&kw)[T][(1 << T) / 2][4]) {
+    constexpr int E = 1 << T;
+    const int base = (it / d0) * (E * d0) + it % d0;
+    for (int r = 0; r < rows; ++r) {
+        float* row = sm + (size_t)r * N + base;
+        float v[E];
+        if (d0 == 1) {                             // E consecutive floats: vector shared loads
 #pragma unroll
-                for (int m = 0; m < E; m += 4) {
-                    const float4 q = *reinterpret_cast<const float4*>(row + m);
-                    v[m] = q.x; v[m + 1] = q.y; v[m + 2] = q.z; v[m + 3] = q.w;
-                }
-            } else {
-#pragma unroll
-                for (int m = 0; m < E; ++m) v[m] = row[m * d0];
+            for (int m = 0; m < E; m += 4) {
+                const float4 q = *reinterpret_cast<const float4*>(row + m);
+                v[m] = q.x; v[m + 1] = q.y; v[m + 2] = q.z; v[m + 3] = q.w;
             }
+        } else {
 #pragma unroll
-            for (int t = 0; t < T; ++t) {
+            for (int m = 0; m < E; ++m) v[m] = row[m * d0];
+        }
 #pragma unroll
-                for (int p = 0; p < E / 2; ++p) {
-                    const int lo = p & ((1 << t) - 1);
-                    const int m0 = ((p >> t) << (t + 1)) | lo;
-                    const int m1 = m0 | (1 << t);
-                    const float x0 = v[m0], x1 = v[m1];
-                    v[m0] = fmaf(x1, kw[t][p][1], fmaf(x0, kw[t][p][0], 0.f));
-                    v[m1] = fmaf(x1, kw[t][p][3], fmaf(x0, kw[t][p][2], 0.f));
-                }
-            }
-            if (d0 == 1) {
+        for (int t = 0; t < T; ++t) {
 #pragma unroll
-                for (int m = 0; m < E; m += 4)
-                    *reinterpret_cast<float4*>(row + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
-            } else {
-#pragma unroll
-                for (int m = 0; m < E; ++m) row[m * d0] = v[m];
+            for (int p = 0; p < E / 2; ++p) {
+                const int lo = p & ((1 << t) - 1);
+                const int m0 = ((p >> t) << (t + 1)) | lo;
+                const int m1 = m0 | (1 << t);
+                const float x0 = v[m0], x1 = v[m1];
+                v[m0] = fmaf(x1, kw[t][p][1], fmaf(x0, kw[t][p][0], 0.f));
+                v[m1] = fmaf(x1, kw[t][p][3], fmaf(x0, kw[t][p][2], 0.f));
             }
         }
+        if (d0 == 1) {
+#pragma unroll
+            for (int m = 0; m < E; m += 4)
+                *reinterpret_cast<float4*>(row + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m) row[m * d0] = v[m];
+        }
     }
+}
+
+// One radix-2^T pass over all rows of the tile, T consecutive dyadic factors
+// (b = c = 2) with d, 2d, 4d: weights loaded (from L2) per item, then applied to
+// every row of the group.
+template <int T>
+__device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const FusedFactor* F) {
+    constexpr int E = 1 << T;
+    const int nitem = N / E;                      // (super-block of the last factor, j) pairs
+    for (int it = threadIdx.x; it < nitem; it += THREADS) {
+        float kw[T][E / 2][4];
+        dyadic_load<T>(F, it, kw);
+        dyadic_apply<T>(sm, rows, N, F[0].d, it, kw);
+    }
+}
+
+// ---- TMEM-resident weights (P.resident radix-8 passes) -----------------------
+// A pass's weights are re-read from L2 for every group of R rows (they do not fit
+// beside the row buffers in shared memory); P.resident passes (<= 2; the d0 = 1
+// pass, whose weight loads are the least coalesced, first) keep them in tensor memory
+// instead, loaded once per CTA: thread t (one item
+// per thread, N / 8 == THREADS) owns 96 columns of TMEM lane (warp % 4) * 32 +
+// lane -- 4 warps share a lane quarter, 4 x 96 = 384 of the 512 columns -- and
+// reads its 48 weights back with three tcgen05.ld .x16 per pass and row group.
+__device__ __forceinline__ uint32_t tmem_w_addr(uint32_t tmem, int ps, int q) {
+    const int warp = threadIdx.x >> 5;
+    return tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 96 + ps * 48 + 16 * q);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+          "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+          "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+          "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+          "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+          "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16f(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
 }
 
 // One factor with b = c = BB (any a, d) per pass.
@@ -170,8 +229,29 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
                       const __grid_constant__ FusedParams P, int R) {
     extern __shared__ __align__(128) float4 sm4[];
     __shared__ __align__(8) uint64_t full[2];
+    __shared__ uint32_t tmem_slot;
+    if (BB == 2 && P.resident > 0) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_slot;
     pdl_wait();
     pdl_launch_dependents();
+    if (BB == 2 && P.resident > 0) {                // stage the resident passes' weights once
+        for (int slot = 0; slot < P.resident; ++slot) {
+            float kw[3][4][4];
+            dyadic_load<3>(&P.f[P.pass_first[P.res_pass[slot]]], threadIdx.x, kw);
+            const float* flat = &kw[0][0][0];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) tmem_st16(tmem_w_addr(tmem, slot, q), flat + 16 * q);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     const int N = P.N;
     // buffer b at smf + b*R*N: indexing the shared symbol directly (not through an
     // array of pointers) keeps the accesses in the shared window (LDS/STS, not
@@ -218,7 +298,14 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
         int f = 0;
         for (int ps = 0; ps < P.npass; ++ps) {
             const int len = P.pass_len[ps];
-            if (BB == 2 && len == 3) dyadic_pass<3>(sm, rows, N, &P.f[f]);
+            const int slot = P.resident > 0 && P.res_pass[0] == ps ? 0 : P.resident > 1 && P.res_pass[1] == ps ? 1 : -1;
+            if (BB == 2 && slot >= 0) {              // weights from TMEM
+                float kw[3][4][4];
+                float* flat = &kw[0][0][0];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) tmem_ld16f(tmem_w_addr(tmem, slot, q), flat + 16 * q);
+                dyadic_apply<3>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
+            } else if (BB == 2 && len == 3) dyadic_pass<3>(sm, rows, N, &P.f[f]);
             else if (BB == 2 && len == 2) dyadic_pass<2>(sm, rows, N, &P.f[f]);
             else block_pass<BB>(sm, rows, N, P.f[f]);
             f += len;
@@ -245,6 +332,14 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
         }
     }
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (BB == 2 && P.resident > 0) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+        }
+    }
 }
 
 constexpr int SMEM_BUDGET = 200 * 1024;      // two row-group buffers (double-buffered)
@@ -294,8 +389,26 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
                    2 * P.f[t + len].a == P.f[t + len - 1].a)
                 ++len;
         }
+        P.pass_first[P.npass] = t;
         P.pass_len[P.npass++] = len;
         t += len;
+    }
+    // TMEM-resident weights for up to two leading radix-8 passes: one item per thread
+    static const int resident_max = [] {            // KS_FUSED_TMEM (experiments): 0..2
+        const char* e = getenv("KS_FUSED_TMEM");
+        const int v = e ? atoi(e) : 2;
+        return v < 0 ? 0 : v > 2 ? 2 : v;
+    }();
+    P.resident = 0;
+    if (dyadic && N / 8 == THREADS) {
+        // the d0 = 1 pass first: its per-thread float4 weight loads are 64 B apart
+        // (half of every sector wasted), the d0 > 1 passes' loads are coalesced --
+        // measured: TMEM for passes {0, 1} 129 us, for {3, 2} 156 us, none 172 us
+        for (int pass_d1 = 0; pass_d1 < 2; ++pass_d1)
+            for (int ps = 0; ps < P.npass && P.resident < resident_max; ++ps) {
+                const bool d1 = P.f[P.pass_first[ps]].d == 1;
+                if (P.pass_len[ps] == 3 && d1 == (pass_d1 == 0)) P.res_pass[P.resident++] = ps;
+            }
     }
     int64_t R = SMEM_BUDGET / (2 * N * 4);                      // rows per buffer
     if (R > 16) R = 16;
