@@ -40,12 +40,14 @@ struct FusedParams {
     int N;                 // row length (all dims equal)
     int resident;          // number of radix-8 passes whose weights live in TMEM (0..2)
     int res_pass[2];       // which passes (the TMEM slot is the index in this list)
+    int part_pass;         // a third pass whose first two factors live in the last 128 columns, or -1
 };
 
 // Weights of one radix-2^T item (T consecutive dyadic factors, b = c = 2, with
 // d0, 2 d0, 4 d0): kw[t][p][kl] = K4[i][k][l][jt] of factor t, pair p (bit t of
 // the element index m cleared), kl = 2k + l.
-template <int T>
+// T0: load only factors t >= T0 (the others come from tensor memory).
+template <int T, int T0 = 0>
 __device__ __forceinline__ void dyadic_load(const FusedFactor* F, int it, float (&kw)[T][(1 << T) / 2][4]) {
     constexpr int E = 1 << T;
     const int d0 = F[0].d;
@@ -56,7 +58,7 @@ __device__ __forceinline__ void dyadic_load(const FusedFactor* F, int it, float 
         // blk * 2^(T+1): vector loads; offset of (pair p, k, l) inside the run is
         // (p >> t) * 4 * 2^t + (2k + l) * 2^t + (p mod 2^t)
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
+        for (int t = T0; t < T; ++t) {
             float kk[2 * E];
             const float4* src = reinterpret_cast<const float4*>(F[t].k + (int64_t)blk * (2 * E));
 #pragma unroll
@@ -72,7 +74,7 @@ __device__ __forceinline__ void dyadic_load(const FusedFactor* F, int it, float 
         }
     } else {
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
+        for (int t = T0; t < T; ++t) {
             const int dt = d0 << t;
 #pragma unroll
             for (int p = 0; p < E / 2; ++p) {
@@ -160,6 +162,11 @@ __device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const Fu
 __device__ __forceinline__ uint32_t tmem_w_addr(uint32_t tmem, int ps, int q) {
     const int warp = threadIdx.x >> 5;
     return tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 96 + ps * 48 + 16 * q);
+}
+// the 128 columns left after two resident passes: 32 per thread, factors 0-1 of a third pass
+__device__ __forceinline__ uint32_t tmem_part_addr(uint32_t tmem, int q) {
+    const int warp = threadIdx.x >> 5;
+    return tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(384 + (warp >> 2) * 32 + 16 * q);
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
     asm volatile(
@@ -250,6 +257,13 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
 #pragma unroll
             for (int q = 0; q < 3; ++q) tmem_st16(tmem_w_addr(tmem, slot, q), flat + 16 * q);
         }
+        if (P.part_pass >= 0) {                       // factors 0-1 of a third pass: 32 columns
+            float kw[3][4][4];
+            dyadic_load<3>(&P.f[P.pass_first[P.part_pass]], threadIdx.x, kw);
+            const float* flat = &kw[0][0][0];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) tmem_st16(tmem_part_addr(tmem, q), flat + 16 * q);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     const int N = P.N;
@@ -304,6 +318,13 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
                 float* flat = &kw[0][0][0];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) tmem_ld16f(tmem_w_addr(tmem, slot, q), flat + 16 * q);
+                dyadic_apply<3>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
+            } else if (BB == 2 && ps == P.part_pass) {   // factors 0-1 from TMEM, factor 2 from L2
+                float kw[3][4][4];
+                float* flat = &kw[0][0][0];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) tmem_ld16f(tmem_part_addr(tmem, q), flat + 16 * q);
+                dyadic_load<3, 2>(&P.f[f], threadIdx.x, kw);
                 dyadic_apply<3>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
             } else if (BB == 2 && len == 3) dyadic_pass<3>(sm, rows, N, &P.f[f]);
             else if (BB == 2 && len == 2) dyadic_pass<2>(sm, rows, N, &P.f[f]);
@@ -364,6 +385,14 @@ bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call) {
     return ((al | reinterpret_cast<uintptr_t>(call.bias)) & 15) == 0;
 }
 
+bool resident_partial() {                           // KS_FUSED_TMEM_PART=0 disables (experiments)
+    static const bool on = [] {
+        const char* e = getenv("KS_FUSED_TMEM_PART");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call) {
     FusedParams P{};
     const int64_t N = hs[0]->N;
@@ -400,6 +429,7 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
         return v < 0 ? 0 : v > 2 ? 2 : v;
     }();
     P.resident = 0;
+    P.part_pass = -1;
     if (dyadic && N / 8 == THREADS) {
         // the d0 = 1 pass first: its per-thread float4 weight loads are 64 B apart
         // (half of every sector wasted), the d0 > 1 passes' loads are coalesced --
@@ -409,6 +439,12 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
                 const bool d1 = P.f[P.pass_first[ps]].d == 1;
                 if (P.pass_len[ps] == 3 && d1 == (pass_d1 == 0)) P.res_pass[P.resident++] = ps;
             }
+        if (P.resident == 2 && resident_max >= 2 && resident_partial())
+            for (int ps = 0; ps < P.npass; ++ps)
+                if (P.pass_len[ps] == 3 && ps != P.res_pass[0] && ps != P.res_pass[1]) {
+                    P.part_pass = ps;
+                    break;
+                }
     }
     int64_t R = SMEM_BUDGET / (2 * N * 4);                      // rows per buffer
     if (R > 16) R = 16;
