@@ -38,29 +38,31 @@ constexpr int WS_THREADS = 32 * WS_CWARPS;
 // Warps split 2 x 4 (rows x outputs) for BN in {96, 128}: tile 128 rows, TN =
 // BN/16; BN in {48, 64} uses 4 x 2 warps: tile 256 rows, TN = 6 / 8 (a 128-row
 // tile would leave TN = 3 / 4: 3 shared loads per 32 FFMA instead of 4 per 64).
-template <int LAYOUT, int BN>
+// KB = l per chunk: 32 when c allows (half the ring waits / refills per FFMA; the
+// BSF A rows become 128 bytes, SWIZZLE_128B), else 16.
+template <int LAYOUT, int BN, int KB = WS_BK>
 struct WsCfg {
     static constexpr int WM = BN <= 64 ? 4 : 2;            // warps along the batch rows
     static constexpr int WN = 8 / WM;                      // warps along the outputs
     static constexpr int BMW = 64 * WM;                    // batch rows per tile
     static constexpr int TN = BN / (4 * WN);               // outputs per thread
-    static constexpr int A_BYTES = WS_BK * BMW * 4;        // 8 or 16 KB
-    static constexpr int B_BYTES = WS_BK * BN * 4;
+    static constexpr int A_BYTES = KB * BMW * 4;
+    static constexpr int B_BYTES = KB * BN * 4;
     static constexpr int SLOT = A_BYTES + B_BYTES;         // multiple of 1 KB (A stays 1 KB aligned)
     static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
     static constexpr int BAR_OFF = S * SLOT;
     static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;     // full barriers, counters, align pad
     static_assert(BN == 48 || BN == 64 || BN == 96 || BN == 128, "TN in {6, 8}");
     static_assert(SLOT % 1024 == 0, "slot alignment (SWIZZLE_64B A tiles)");
-    static_assert(S >= 3, "ring depth");
+    static_assert(S * KB >= 64, "ring depth (l in flight)");
 };
 
-template <int LAYOUT, int BN>
+template <int LAYOUT, int BN, int KB = WS_BK>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                   float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
                   int64_t ntiles) {
-    using C = WsCfg<LAYOUT, BN>;
+    using C = WsCfg<LAYOUT, BN, KB>;
     constexpr int S = C::S;
     constexpr int TN = C::TN;
     extern __shared__ uint8_t smem_raw[];
@@ -75,7 +77,7 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
     const int nkc = b / BN;
     constexpr int BMW = C::BMW;
     const int64_t nnb = (B + BMW - 1) / BMW;
-    const int nk = c / WS_BK;
+    const int nk = c / KB;
     const int64_t M = (int64_t)a * b * d;
 
     // tile -> (k-chunk fastest, n-block, block q = i*d + j)
@@ -93,7 +95,7 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
         decode(blockIdx.x + (gx / nk) * gridDim.x, q, k0, n0);
         const int i = q / d, j = q % d;
         const int st = (int)(gx % S);
-        const int l0 = (int)(gx % nk) * WS_BK;
+        const int l0 = (int)(gx % nk) * KB;
         const uint32_t sa = slot0 + st * C::SLOT;
         mbar_expect_tx(full0 + 8 * st, C::SLOT);
         if constexpr (LAYOUT == KS_LAYOUT_BSL)
@@ -142,7 +144,7 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                 // A[l][n]: rows wm*64 + ty*4 + {0..3} and +32
                 const uint32_t pa = sa + (wm * 64 + ty * 4) * 4;
 #pragma unroll
-                for (int l = 0; l < WS_BK; ++l) {
+                for (int l = 0; l < KB; ++l) {
                     float av[8], bv[TN];
                     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                  : "=f"(av[0]), "=f"(av[1]), "=f"(av[2]), "=f"(av[3]) : "r"(pa + l * BMW * 4));
@@ -169,12 +171,13 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                 // A[n][l] (64-byte rows, SWIZZLE_64B: 16-byte chunk u of row n at u ^ ((n >> 1) & 3)):
                 // rows wm*64 + ty + 8m; one float4 = 4 consecutive l of a row
 #pragma unroll
-                for (int qd = 0; qd < WS_BK / 4; ++qd) {
+                for (int qd = 0; qd < KB / 4; ++qd) {
                     float4 av[8];
 #pragma unroll
                     for (int m = 0; m < 8; ++m) {
                         const int n = wm * 64 + ty + 8 * m;
-                        const uint32_t addr = sa + n * 64 + ((qd ^ ((n >> 1) & 3)) << 4);
+                        const int sw = KB == 16 ? (n >> 1) & 3 : n & 7;        // SWIZZLE_64B / 128B
+                        const uint32_t addr = sa + n * (KB * 4) + ((qd ^ sw) << 4);
                         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                      : "=f"(av[m].x), "=f"(av[m].y), "=f"(av[m].z), "=f"(av[m].w) : "r"(addr));
                     }
@@ -722,29 +725,30 @@ cudaError_t launch_wsc_tk(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
-template <int LAYOUT, int BN>
+template <int LAYOUT, int BN, int KB = WS_BK>
 cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
-    using C = WsCfg<LAYOUT, BN>;
+    using C = WsCfg<LAYOUT, BN, KB>;
     CUtensorMap xmap, kmap;
     {
         // k_tile: [(i*d + j)*c + l][k], b floats per row
         const cuuint64_t kd[2] = {(cuuint64_t)h.b, (cuuint64_t)(h.a * h.d * h.c)};
         const cuuint64_t ks[1] = {(cuuint64_t)h.b * 4};
-        const cuuint32_t kb[2] = {BN, WS_BK};
+        const cuuint32_t kb[2] = {BN, KB};
         if (!encode(&kmap, h.k_tile, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
     if (LAYOUT == KS_LAYOUT_BSL) {
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
         const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
-        const cuuint32_t xb[3] = {(cuuint32_t)C::BMW, 1, WS_BK};
+        const cuuint32_t xb[3] = {(cuuint32_t)C::BMW, 1, KB};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     } else {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
-        const cuuint32_t xb[2] = {WS_BK, (cuuint32_t)C::BMW};
-        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+        const cuuint32_t xb[2] = {KB, (cuuint32_t)C::BMW};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, KB == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
     }
-    auto kern = ks_ffma_ws_kernel<LAYOUT, BN>;
+    auto kern = ks_ffma_ws_kernel<LAYOUT, BN, KB>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -767,15 +771,28 @@ int pick_bn_ws(int64_t b) {
     return 0;
 }
 
-template <int LAYOUT>
-cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
+template <int LAYOUT, int KB>
+cudaError_t launch_ws_kb(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn_ws(h.b)) {
-        case 128: return launch_ws<LAYOUT, 128>(h, call);
-        case 96: return launch_ws<LAYOUT, 96>(h, call);
-        case 64: return launch_ws<LAYOUT, 64>(h, call);
-        case 48: return launch_ws<LAYOUT, 48>(h, call);
+        case 128: return launch_ws<LAYOUT, 128, KB>(h, call);
+        case 96: return launch_ws<LAYOUT, 96, KB>(h, call);
+        case 64: return launch_ws<LAYOUT, 64, KB>(h, call);
+        case 48: return launch_ws<LAYOUT, 48, KB>(h, call);
     }
     return cudaErrorInvalidValue;
+}
+
+template <int LAYOUT>
+cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
+    // 32 l per staged chunk pays only for BSL with b = 96 tiles (2,96,96,16: 365 -> 327 us);
+    // elsewhere it is 0-10 % slower (profiles/r01_ffma_kb32_negative.txt).  KS_FFMA_KB32=0 disables.
+    static const bool kb32 = [] {
+        const char* e = getenv("KS_FFMA_KB32");
+        return !(e && atoi(e) == 0);
+    }();
+    if (LAYOUT == KS_LAYOUT_BSL && kb32 && h.c % 32 == 0 && pick_bn_ws(h.b) == 96)
+        return launch_ws<LAYOUT, 96, 32>(h, call);
+    return launch_ws_kb<LAYOUT, WS_BK>(h, call);
 }
 
 }  // namespace
