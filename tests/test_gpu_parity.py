@@ -324,7 +324,7 @@ def test_ffma_ws_many_tiles_per_cta(grid):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("p", [(1, 128, 128, 64), (16, 48, 48, 4), (1, 96, 96, 1), (4, 64, 64, 16)])
+@pytest.mark.parametrize("p", [(1, 128, 128, 64), (16, 48, 48, 4), (1, 96, 96, 1), (4, 64, 64, 16), (1, 128, 128, 1), (1, 64, 64, 2)])
 @pytest.mark.parametrize("layout", ["bsf", "bsl"])
 def test_sweep_full_size_sampled_rows(ksb, p, layout):
     """configs[2] at B = 25088 in bench's launch configuration (auto plan):
