@@ -45,8 +45,10 @@ def test_random_pattern_matches_oracle(ksb, p, B, layout, math):
     f = ksb.Factor(*p, K4)
     tol = 1e-5
     if math != "fp32":
-        if p[1] < 16 or p[2] < 16:
-            pytest.skip("tensor-core math needs b, c >= 16")
+        if p[1] < 16 or p[2] < 16:             # tensor-core math needs b, c >= 16 (include/ks.h)
+            with pytest.raises(ksb.KSError, match="KS_ERR_UNSUPPORTED"):
+                f.set_math(ksb.MATH_TF32 if math == "tf32" else ksb.MATH_F32X3)
+            return
         f.set_math(ksb.MATH_TF32 if math == "tf32" else ksb.MATH_F32X3)
         tol = 5e-3 if math == "tf32" else 1e-5
     Xd = torch.from_numpy(np.ascontiguousarray(X if layout == "bsf" else ksgen.to_bsl(X))).cuda()
