@@ -564,10 +564,18 @@ ks_status_t ks_chain_host(const ks_handle_t* hs, int L, const float* Xh, float* 
     // of chunk k+1 and the D2H copy of chunk k-1 overlap the chain on chunk k
     // (PCIe is full duplex; rows are independent).  BSL chunks are column
     // blocks (2-D copies into a contiguous N x Bc buffer), multiples of 4 columns.
+    static const int64_t chunk_mb = [] {                 // KS_HOST_CHUNK_MB (experiments)
+        const char* v = getenv("KS_HOST_CHUNK_MB");
+        return (int64_t)(v && atoi(v) > 0 ? atoi(v) : 16);
+    }();
+    static const int64_t max_chunks = [] {               // KS_HOST_MAX_CHUNKS (experiments)
+        const char* v = getenv("KS_HOST_MAX_CHUNKS");
+        return (int64_t)(v && atoi(v) > 0 ? atoi(v) : 16);
+    }();
     const int64_t per_row = es * (N + M);
-    int64_t bc = (int64_t)(16 << 20) / (per_row > 0 ? per_row : 1);
+    int64_t bc = (chunk_mb << 20) / (per_row > 0 ? per_row : 1);
     if (bc < 1) bc = 1;
-    if (bc * 16 < B) bc = (B + 15) / 16;                 // at most 16 chunks
+    if (bc * max_chunks < B) bc = (B + max_chunks - 1) / max_chunks;
     if (layout == KS_LAYOUT_BSL) bc = (bc + 3) / 4 * 4;
     if (bc > B) bc = B;
     const int64_t nch = (B + bc - 1) / bc;
