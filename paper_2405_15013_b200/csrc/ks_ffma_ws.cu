@@ -784,13 +784,14 @@ cudaError_t launch_ws_kb(const ks_handle_s& h, const KsCall& call) {
 
 template <int LAYOUT>
 cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
-    // 32 l per staged chunk pays only for BSL with b = 96 tiles (2,96,96,16: 365 -> 327 us);
-    // elsewhere it is 0-10 % slower (profiles/r01_ffma_kb32_negative.txt).  KS_FFMA_KB32=0 disables.
+    // 32 l per staged chunk pays only for b = 96 tiles (9-12 %: BSL (2,96,96,16) 365 -> 327 us,
+    // BSF (64,96,96,1) 839 -> 745 us); elsewhere it is 0-10 % slower
+    // (profiles/r01_ffma_kb32_negative.txt).  KS_FFMA_KB32=0 disables.
     static const bool kb32 = [] {
         const char* e = getenv("KS_FFMA_KB32");
         return !(e && atoi(e) == 0);
     }();
-    if (LAYOUT == KS_LAYOUT_BSL && kb32 && h.c % 32 == 0 && pick_bn_ws(h.b) == 96)
+    if (kb32 && h.c % 32 == 0 && pick_bn_ws(h.b) == 96)
         return launch_ws<LAYOUT, 96, 32>(h, call);
     return launch_ws_kb<LAYOUT, WS_BK>(h, call);
 }
