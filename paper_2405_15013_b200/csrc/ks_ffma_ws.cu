@@ -38,8 +38,8 @@ constexpr int WS_THREADS = 32 * WS_CWARPS;
 // Warps split 2 x 4 (rows x outputs) for BN in {96, 128}: tile 128 rows, TN =
 // BN/16; BN in {48, 64} uses 4 x 2 warps: tile 256 rows, TN = 6 / 8 (a 128-row
 // tile would leave TN = 3 / 4: 3 shared loads per 32 FFMA instead of 4 per 64).
-// KB = l per chunk: 32 when c allows (half the ring waits / refills per FFMA; the
-// BSF A rows become 128 bytes, SWIZZLE_128B), else 16.
+// KB = l per chunk: 16, or 32 for BN = 96 tiles when c % 32 == 0 (half the ring
+// waits / refills per FFMA; the BSF A rows become 128 bytes, SWIZZLE_128B).
 template <int LAYOUT, int BN, int KB = WS_BK>
 struct WsCfg {
     static constexpr int WM = BN <= 64 ? 4 : 2;            // warps along the batch rows
