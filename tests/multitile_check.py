@@ -19,7 +19,7 @@ if os.environ.get("KS_MULTITILE_MATH") == "fp32":
                       ((1, 64, 64, 4), "bsl", 1028), ((2, 96, 96, 3), "bsl", 516), ((3, 96, 48, 1), "bsf", 333),
                       ((1, 64, 64, 4), "bsf", 1000), ((2, 48, 48, 8), "bsf", 700), ((1, 128, 64, 2), "bsf", 900),
                       ((2, 48, 48, 1), "bsf", 600), ((1, 48, 64, 4), "bsl", 520), ((1, 128, 64, 3), "bsf", 700),
-                      ((2, 96, 32, 3), "bsf", 333), ((1, 96, 64, 5), "bsl", 776), ((2, 96, 64, 1), "bsf", 555)]:
+                      ((2, 96, 32, 3), "bsf", 333), ((1, 96, 64, 5), "bsl", 776), ((2, 96, 64, 1), "bsf", 555), ((1, 64, 48, 6), "bsf", 333)]:
         M, N, _ = O.dims(p)
         K4 = ksgen.k4_uniform(*p, seed=3)
         X = ksgen.x_normal(B, N, seed=4)

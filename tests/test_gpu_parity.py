@@ -283,7 +283,7 @@ def test_plan_table(ksb):
 GEMMLIKE = [(1, 48, 48, 1), (1, 64, 64, 2), (2, 96, 96, 4), (1, 128, 128, 3), (3, 64, 64, 16),
             (1, 48, 48, 64), (6, 64, 64, 1), (1, 768, 192, 2), (6, 64, 256, 1), (64, 64, 64, 1),
             (1, 64, 256, 16), (1, 256, 64, 16), (2, 32, 16, 4), (1, 24, 8, 5), (2, 192, 48, 2),
-            (2, 96, 64, 3), (1, 64, 48, 3), (3, 32, 32, 2), (1, 48, 48, 3), (4, 96, 96, 1), (1, 96, 160, 1)]
+            (2, 96, 64, 3), (1, 64, 48, 3), (3, 32, 32, 2), (1, 48, 48, 3), (4, 96, 96, 1), (1, 96, 160, 1), (1, 64, 64, 6), (2, 96, 32, 6)]
 
 
 @pytest.mark.parametrize("p", GEMMLIKE)
@@ -324,7 +324,7 @@ def test_ffma_ws_many_tiles_per_cta(grid):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("p", [(1, 128, 128, 64), (16, 48, 48, 4), (1, 96, 96, 1), (4, 64, 64, 16), (1, 128, 128, 1), (1, 64, 64, 2)])
+@pytest.mark.parametrize("p", [(1, 128, 128, 64), (16, 48, 48, 4), (1, 96, 96, 1), (4, 64, 64, 16), (1, 128, 128, 1), (1, 64, 64, 2), (1, 128, 128, 6)])
 @pytest.mark.parametrize("layout", ["bsf", "bsl"])
 def test_sweep_full_size_sampled_rows(ksb, p, layout):
     """configs[2] at B = 25088 in bench's launch configuration (auto plan):
