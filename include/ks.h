@@ -265,6 +265,15 @@ const char* ks_status_string(ks_status_t s);
 uint64_t    ks_kernel_launch_count(void);       /* kernels launched so far   */
 int         ks_abi_version(void);               /* KS_ABI_VERSION            */
 
+/* Measurement aid (not on the KS path): the FP32 FFMA throughput of the
+ * current device, measured by an FFMA-loop kernel (8 independent chains per
+ * thread, 2 x 512 threads per SM, best of 5 event-timed launches on `stream`;
+ * synchronous).  The "alu" roofline denominator of the FP32 CUDA-core kernels
+ * (SURVEY.md §8d "Peaks": "an FFMA loop for FP32").  *tflops receives TFLOP/s
+ * (2 flops per FMA).  KS_ERR_INVALID_ARG if tflops is NULL; KS_ERR_CUDA /
+ * KS_ERR_OOM on CUDA failures. */
+ks_status_t ks_peak_ffma(ks_stream_t stream, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

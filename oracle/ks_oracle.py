@@ -10,8 +10,11 @@ in SURVEY.md §8(c) and DESIGN.md "Readings of the paper".
 Pins (tests/test_oracle_pins.py) tie each function to something other than
 itself: brute-force Kronecker products, numpy/scipy routines (FFT, Hadamard,
 matmul), hand-worked examples printed in the paper/spec (tests/golden/), and
-exact integer identities.  Every function below is pinned; none is
-"parity unpinned".
+exact integer identities.  Every arithmetic function below is pinned,
+including the contract metric normwise_error (hand-computed real and complex
+values) and envelope_delta (hand values + real FP32/TF32 dot products); none
+is "parity unpinned".  (Round 1 claimed this while normwise_error dropped
+imaginary parts; fixed in round 2.)
 """
 from __future__ import annotations
 
@@ -381,10 +384,23 @@ def model_flops(p, B: int) -> int:
 
 def normwise_error(Y_hat, Y_ref) -> float:
     """max |Y_hat - Y| / max |Y| over the tensor (§8c-10 reading of the
-    north-star 'max relative error')."""
-    Y_ref = np.asarray(Y_ref, dtype=np.float64)
-    den = float(np.max(np.abs(Y_ref))) if Y_ref.size else 0.0
-    num = float(np.max(np.abs(np.asarray(Y_hat, np.float64) - Y_ref))) if Y_ref.size else 0.0
+    north-star 'max relative error').  |.| is the modulus, so complex inputs
+    (the Fig. 1 DFT check) compare real AND imaginary parts: both
+    sides are promoted to complex128 when either is complex, else float64.
+    The shapes must match exactly (no broadcasting)."""
+    Y_hat = np.asarray(Y_hat)
+    Y_ref = np.asarray(Y_ref)
+    if Y_hat.shape != Y_ref.shape:
+        raise ValueError(f"shape mismatch: {Y_hat.shape} vs {Y_ref.shape}")
+    wide = np.complex128 if (np.iscomplexobj(Y_hat) or np.iscomplexobj(Y_ref)) else np.float64
+    Y_hat = Y_hat.astype(wide)
+    Y_ref = Y_ref.astype(wide)
+    if Y_ref.size == 0:
+        return 0.0
+    den = float(np.max(np.abs(Y_ref)))
+    num = float(np.max(np.abs(Y_hat - Y_ref)))
+    if not (np.isfinite(num) and np.isfinite(den)):
+        return float("inf")
     if den == 0.0:
         return 0.0 if num == 0.0 else float("inf")
     return num / den

@@ -58,6 +58,10 @@ cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call);
 
 bool tf32_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);
+// round-2 TF32 kernel (ks_tf32_v2.cu): BSL and BSF d = 1, MN-major A by TMA,
+// resident weights, TMA-store epilogue; tf32_launch routes there when it applies
+bool tf32v2_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t tf32v2_launch(const ks_handle_s& h, const KsCall& call);
 
 // half precision handles (NEXT-3): tcgen05 kind::f16 kernel and a generic one
 bool half_supports(const ks_handle_s& h, const KsCall& call);

@@ -1031,6 +1031,18 @@ struct BsfjPlan {
     int J = 0, BN = 0;
     bool gather = false;
 };
+// J = 8 (32-byte gather runs) also for b > 64: TMA boxes with 16-byte inner runs
+// (J = 4) read X at <= 3-4 TB/s, 32-byte runs at 4.6-5.1 TB/s
+// (scripts/probe_tma_gather.cu); BN then halves (J x BN <= 512 TMEM columns) and the
+// b / BN output chunks of one X tile run on adjacent CTAs at the same time (L2 hits).
+bool j8_wide() {
+    static const bool on = [] {
+        const char* e = getenv("KS_BSFJ_J8");
+        return e && atoi(e) == 1;
+    }();
+    return on;
+}
+
 // 3xTF32 doubles every operand tile: J <= 4 there (d = 6 runs FFMA).
 BsfjPlan pick_bsfj(const ks_handle_s& h) {
     BsfjPlan p;
@@ -1038,7 +1050,7 @@ BsfjPlan pick_bsfj(const ks_handle_s& h) {
     if (h.c % 16 != 0) return p;
     if (h.d >= 2 && h.d <= (x3 ? 4 : 8) && h.d != 5 && h.d != 7) {
         p.J = (int)h.d;
-    } else if (!x3 && h.d > 8 && h.d % 8 == 0 && h.b <= 64) {
+    } else if (!x3 && h.d > 8 && h.d % 8 == 0 && (h.b <= 64 || j8_wide())) {
         p.J = 8;
         p.gather = true;
     } else if (h.d > (x3 ? 4 : 8) && h.d % 4 == 0) {
@@ -1271,6 +1283,7 @@ cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
 namespace ks {
 
 bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
+    if (tf32v2_supports(h, call)) return true;
     if (h.b < 16 || h.c < 16 || h.c % 8 != 0 || pick_bn(h.b) == 0) return false;
     if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31)) return false;
     if (call.B >= (int64_t(1) << 31)) return false;
@@ -1290,6 +1303,7 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
         if (h.d == 1) return launch_layout<KS_LAYOUT_BSF, float, true>(h, call);
         return launch_bsfj_any<true>(h, call);
     }
+    if (tf32v2_supports(h, call)) return tf32v2_launch(h, call);
     if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL>(h, call);
     if (h.d == 1) return launch_layout<KS_LAYOUT_BSF>(h, call);
     return launch_bsfj_any<false>(h, call);

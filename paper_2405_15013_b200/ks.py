@@ -35,7 +35,7 @@ EXPORTS = ["ks_pack_weights", "ks_pack_weights_ex", "ks_get_dtype", "ks_matmul_a
            "ks_trace_enable", "ks_trace_read",
            "ks_last_error", "ks_last_error_message", "ks_status_string",
            "ks_kernel_launch_count", "ks_abi_version",
-           "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free"]
+           "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free", "ks_peak_ffma"]
 
 
 class KSError(RuntimeError):
@@ -117,6 +117,8 @@ def load_library(path: str = LIB_PATH):
     lib.ks_graph_kernel_count.restype = ctypes.c_int
     lib.ks_graph_free.argtypes = [vp]
     lib.ks_graph_free.restype = None
+    lib.ks_peak_ffma.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+    lib.ks_peak_ffma.restype = st
     _lib = lib
     return lib
 
@@ -143,6 +145,13 @@ def _stream_ptr(stream):
 
 def launch_count() -> int:
     return int(load_library().ks_kernel_launch_count())
+
+
+def peak_ffma_tflops(stream=None) -> float:
+    """Measured FP32 FFMA TFLOP/s of the current device (ks_peak_ffma)."""
+    out = ctypes.c_double(0.0)
+    _check(load_library().ks_peak_ffma(_stream_ptr(stream), ctypes.byref(out)))
+    return float(out.value)
 
 
 def trace_enable(on: bool = True):
@@ -245,15 +254,45 @@ def _dev_ptr(t, what):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _torch_dtype(dtype_id):
+    import torch
+    return {DTYPE_F32: torch.float32, DTYPE_BF16: torch.bfloat16, DTYPE_F16: torch.float16}[dtype_id]
+
+
+def _check_io(dtype_id, n_in, n_out, X, Y, B, lay, bias=None):
+    """Reject, before the C ABI sees them, arguments that would make a kernel
+    read or write out of bounds: element type, shapes against (B, N) / (B, M)
+    in the given layout, bias length, and device.  Raises ValueError/TypeError."""
+    want = _torch_dtype(dtype_id)
+    if B < 0:
+        raise ValueError(f"B must be >= 0, got {B}")
+    for t, what, n in ((X, "X", n_in), (Y, "Y", n_out)):
+        if t.dtype != want:
+            raise TypeError(f"{what} has dtype {t.dtype}, the factor computes in {want}")
+        exp = (B, n) if lay == BSF else (n, B)
+        if tuple(t.shape) != exp:
+            raise ValueError(f"{what} must have shape {exp} ({'BSF' if lay == BSF else 'BSL'}), got {tuple(t.shape)}")
+    if X.device != Y.device:
+        raise ValueError(f"X is on {X.device}, Y on {Y.device}")
+    if bias is not None:
+        if bias.dtype != want:
+            raise TypeError(f"bias has dtype {bias.dtype}, expected {want}")
+        if bias.numel() != n_out:
+            raise ValueError(f"bias must have M = {n_out} values, got {bias.numel()}")
+        if bias.device != X.device:
+            raise ValueError(f"bias is on {bias.device}, X on {X.device}")
+
+
 def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None, bias=None):
-    """Y = X K^T (+ bias) through ks_matmul / ks_matmul_bias.  X: CUDA float32,
-    (B, N) for BSF or (N, B) for BSL; bias: CUDA float32 (M,) or None."""
+    """Y = X K^T (+ bias) through ks_matmul / ks_matmul_bias.  X: CUDA tensor of
+    the factor's element type, (B, N) for BSF or (N, B) for BSL; bias: (M,) or None."""
     import torch
     lay = _layout(layout)
     if B is None:
         B = X.shape[0] if lay == BSF else X.shape[1]
     if Y is None:
-        Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=X.dtype)
+        Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=_torch_dtype(f.dtype))
+    _check_io(f.dtype, f.N, f.M, X, Y, int(B), lay, bias)
     if f.dtype != DTYPE_F32:
         bp = _dev_ptr(bias, "bias") if bias is not None else None
         _check(_lib.ks_matmul_any(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, int(B), lay,
@@ -276,10 +315,15 @@ def chain(factors, X, Y=None, layout="bsf", stream=None, bias=None):
     in paper order K_1..K_L."""
     import torch
     lay = _layout(layout)
+    if not factors:
+        raise ValueError("a chain needs at least one factor")
     B = X.shape[0] if lay == BSF else X.shape[1]
     M = factors[0].M
     if Y is None:
-        Y = torch.empty((B, M) if lay == BSF else (M, B), device=X.device, dtype=X.dtype)
+        Y = torch.empty((B, M) if lay == BSF else (M, B), device=X.device, dtype=_torch_dtype(factors[0].dtype))
+    if any(f.dtype != factors[0].dtype for f in factors):
+        raise TypeError("all factors of a chain must have the same element type")
+    _check_io(factors[0].dtype, factors[-1].N, M, X, Y, int(B), lay, bias)
     if factors[0].dtype != DTYPE_F32:
         bp = _dev_ptr(bias, "bias") if bias is not None else None
         _check(_lib.ks_chain_any(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp,
@@ -309,6 +353,9 @@ def chain_host(factors, X_host, Y_host, layout="bsf", stream=None):
     for t, w in ((X_host, "X_host"), (Y_host, "Y_host")):
         if t.is_cuda or not t.is_contiguous():
             raise ValueError(f"{w} must be a contiguous host tensor")
+    if factors[0].dtype != DTYPE_F32:
+        raise TypeError("ks_chain_host takes F32 factors")
+    _check_io(DTYPE_F32, factors[-1].N, factors[0].M, X_host, Y_host, int(B), lay)
     _check(_lib.ks_chain_host(_handles(factors), len(factors), ctypes.c_void_p(X_host.data_ptr()),
                               ctypes.c_void_p(Y_host.data_ptr()), int(B), lay, _stream_ptr(stream)))
     return Y_host
@@ -324,6 +371,7 @@ class ChainGraph:
         lay = _layout(layout)
         lib = load_library()
         B = X.shape[0] if lay == BSF else X.shape[1]
+        _check_io(factors[0].dtype, factors[-1].N, factors[0].M, X, Y, int(B), lay, bias)
         self._keep = (list(factors), X, Y, bias)
         bp = _dev_ptr(bias, "bias") if bias is not None else None
         h = lib.ks_chain_graph(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, int(B), lay)

@@ -53,6 +53,8 @@ class KSLinear(torch.nn.Module):
                 f.set_math(ks.MATH_TF32 if math_mode == "tf32" else ks.MATH_F32X3)
             self.factors.append(f)
         if isinstance(bias, torch.Tensor):
+            if bias.numel() != self.out_features:
+                raise ValueError(f"bias must have out_features = {self.out_features} values, got {bias.numel()}")
             self.bias = torch.nn.Parameter(bias.detach().to(dev, torch.float32).contiguous(), requires_grad=False)
         elif bias:
             bound = 1.0 / math.sqrt(self.in_features)

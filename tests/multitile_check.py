@@ -57,7 +57,11 @@ worst = 0.0
 for p, lay, B in [((1, 64, 64, 4), "bsf", 1024), ((1, 64, 64, 4), "bsl", 1024), ((1, 64, 64, 1), "bsf", 1024),
                   ((2, 48, 48, 8), "bsf", 512), ((1, 128, 128, 8), "bsf", 512), ((2, 96, 96, 1), "bsl", 772),
                   ((1, 256, 64, 16), "bsf", 300), ((1, 128, 128, 3), "bsf", 700), ((1, 128, 128, 12), "bsf", 600),
-                  ((2, 64, 64, 16), "bsf", 520), ((1, 96, 96, 6), "bsf", 400), ((1, 768, 192, 2), "bsf", 300)]:
+                  ((2, 64, 64, 16), "bsf", 520), ((1, 96, 96, 6), "bsf", 400), ((1, 768, 192, 2), "bsf", 300),
+                  # round-2 TF32 kernel (ks_tf32_v2.cu): resident-weight segments, nkc > 1, SW64 store boxes
+                  ((2, 64, 64, 4), "bsl", 1024), ((3, 48, 48, 1), "bsf", 900), ((1, 768, 192, 2), "bsl", 300),
+                  ((4, 128, 128, 2), "bsl", 516), ((6, 64, 256, 1), "bsf", 700), ((2, 16, 24, 3), "bsl", 388),
+                  ((1, 320, 40, 2), "bsl", 260), ((5, 112, 64, 1), "bsf", 600)]:
     M, N, _ = O.dims(p)
     K4 = ksgen.k4_uniform(*p, seed=3)
     X = ksgen.x_normal(B, N, seed=4)

@@ -164,7 +164,11 @@ def test_dft_chain_real_imag_split_matches_numpy_fft(ksb):
     torch.cuda.synchronize()
     Zh = Z.cpu().numpy().astype(np.float64)
     got = Zh[:B] + 1j * Zh[B:]
+    # complex moduli: real AND imaginary parts are compared (normwise_error
+    # promotes to complex128); each half is also checked on its own
     assert O.normwise_error(got, ref) < 1e-5
+    assert O.normwise_error(Zh[:B], ref.real) < 1e-5 * np.abs(ref).max() / np.abs(ref.real).max()
+    assert O.normwise_error(Zh[B:], ref.imag) < 1e-5 * np.abs(ref).max() / np.abs(ref.imag).max()
 
 
 @pytest.mark.parametrize("name", ["VIT_UP", "VIT_DOWN", "GPT2_DOWN", "GPT2_UP"])

@@ -368,3 +368,102 @@ def test_truncate_tf32():
     t = O.truncate_tf32(r)
     assert np.all(np.abs(t) <= np.abs(r))
     assert np.all(np.abs(t.astype(np.float64) - r) < 2.0 ** -10 * np.abs(r))
+
+
+# ------------------------------------------- the contract metric (R9, c-10) --
+def test_normwise_error_hand_values_real():
+    """max|Y_hat - Y| / max|Y| worked by hand."""
+    ref = np.array([[3.0, -4.0], [0.0, 2.0]])
+    got = np.array([[3.0, -3.0], [0.5, 2.0]])
+    assert O.normwise_error(got, ref) == 0.25            # max diff 1.0 / max |ref| 4.0
+    assert O.normwise_error(ref, ref) == 0.0
+    assert O.normwise_error(np.zeros(3), np.zeros(3)) == 0.0
+    assert O.normwise_error(np.array([0.0, 1e-30]), np.zeros(2)) == float("inf")
+    assert O.normwise_error(np.array([np.nan, 0.0]), np.array([1.0, 0.0])) == float("inf")
+    # max, not mean: one bad element among many good ones decides
+    ref = np.ones(1000)
+    got = ref.copy()
+    got[517] = 1.5
+    assert O.normwise_error(got, ref) == 0.5
+    # float32 inputs are widened, not compared in float32
+    assert O.normwise_error(np.float32([1 + 2 ** -23]), np.float64([1.0])) == 2.0 ** -23
+    with pytest.raises(ValueError):
+        O.normwise_error(np.zeros((2, 3)), np.zeros((3, 2)))
+
+
+def test_normwise_error_hand_values_complex():
+    """Complex moduli (the Fig. 1 DFT check): ref=[3+4j, 0],
+    got=[3+4j, 1j] -> |1j| / |3+4j| = 1/5."""
+    assert O.normwise_error(np.array([3 + 4j, 1j]), np.array([3 + 4j, 0])) == pytest.approx(0.2, abs=0)
+    # an error only in the imaginary part is seen
+    assert O.normwise_error(np.array([1 + 100j, 2 - 50j]), np.array([1 + 1j, 2 + 5j])) == \
+        pytest.approx(99 / np.hypot(2, 5), rel=1e-15)
+    # real got vs complex ref: the missing imaginary part counts
+    assert O.normwise_error(np.array([1.0, 0.0]), np.array([1 + 1j, 0])) == pytest.approx(1 / np.sqrt(2))
+
+
+def test_normwise_error_catches_corrupted_imaginary_half():
+    """The GPU DFT test's recombination: a corrupted imaginary half of the
+    stacked [Re; Im] batch must fail the 1e-5 contract."""
+    L, B = 6, 4
+    N = 2 ** L
+    Zr = ksgen.x_normal(B, N, seed=30).astype(np.float64)
+    Zi = ksgen.x_normal(B, N, seed=31).astype(np.float64)
+    ref = np.fft.fft((Zr + 1j * Zi)[:, O.bitrev(L)], axis=1)
+    good = ref.real + 1j * ref.imag
+    assert O.normwise_error(good, ref) == 0.0
+    bad_im = ref.real + 1j * (ref.imag + 1e-3 * np.abs(ref).max() * (np.arange(N) == 7))
+    assert O.normwise_error(bad_im, ref) > 1e-5
+    bad_sign = ref.real - 1j * ref.imag                  # conjugated output (a sign slip)
+    assert O.normwise_error(bad_sign, ref) > 1e-2
+
+
+def test_envelope_delta_hand_values():
+    """delta = 2 u_in + u_in^2 + gamma_{2c}, gamma_n = n u / (1 - n u)."""
+    assert O.envelope_delta(2, 0.1, u=0.01) == pytest.approx(0.2 + 0.01 + 0.04 / 0.96, rel=1e-15)
+    assert O.envelope_delta(1, 0.0, u=0.25) == pytest.approx(0.5 / 0.5, rel=1e-15)
+    u = 2.0 ** -24
+    assert O.envelope_delta(64, 0.0) == pytest.approx(128 * u / (1 - 128 * u), rel=1e-15)
+    assert O.envelope_delta(64, 2.0 ** -10) == pytest.approx(2 ** -9 + 2 ** -20 + 128 * u / (1 - 128 * u),
+                                                             rel=1e-15)
+
+
+def test_envelope_delta_covers_worst_observed_fp32_and_tf32_dots():
+    """The bound holds for real FP32 sequential-FMA dot products (Higham's
+    gamma_c is the textbook bound; the envelope uses 2c) and for TF32-truncated
+    operands with u_in = 2^-10, on adversarially scaled data; and it is not
+    vacuous: it is within 2^9 of the worst observed error."""
+    rng = np.random.default_rng(7)
+    worst_ratio = 0.0
+    for c in (2, 16, 48, 128):
+        x = rng.standard_normal((4000, c)).astype(np.float32)
+        k = rng.uniform(-1, 1, (c,)).astype(np.float32)
+        x[:, 0] *= 1e4                                  # large first term, cancellations later
+        exact = x.astype(np.float64) @ k.astype(np.float64)
+        env = np.abs(x).astype(np.float64) @ np.abs(k).astype(np.float64)
+        acc = np.zeros(4000, np.float32)
+        for l in range(c):                              # one rounding per add, ascending l
+            acc = (acc + x[:, l] * k[l]).astype(np.float32)
+        err = np.abs(acc.astype(np.float64) - exact)
+        assert np.all(err <= O.envelope_delta(c, 0.0) * env)
+        worst_ratio = max(worst_ratio, float(np.max(err / (O.envelope_delta(c, 0.0) * env))))
+        xt = O.truncate_tf32(x).astype(np.float64)
+        kt = O.round_tf32_rna(k).astype(np.float64)
+        err_t = np.abs(xt @ kt - exact)
+        assert np.all(err_t <= O.envelope_delta(c, 2.0 ** -10) * env)
+    assert worst_ratio > 2.0 ** -9
+
+
+def test_model_bytes_and_pattern_check_hand_values():
+    """Byte model: 4 (B N + abcd + B M) bytes; FFT factor of
+    configs[1]: (2^{l-1},2,2,2^{12-l}), B = 8192 -> 4 (2 * 8192 * 4096 + 8192)
+    = 268,468,224 bytes (the per-launch figure in DESIGN §5.1 / BENCH_r01)."""
+    assert O.model_bytes((1, 2, 2, 2048), 8192) == 268_468_224
+    assert O.model_bytes((2048, 2, 2, 1), 8192) == 268_468_224
+    # (2,4,4,2), B = 8 (configs[0]): N = M = 16, nnz = 64 -> 4 (128 + 64 + 128)
+    assert O.model_bytes((2, 4, 4, 2), 8) == 1280
+    assert O.model_bytes((1, 3, 5, 1), 2, elem_bytes=2) == 2 * (10 + 15 + 6)
+    for bad in ((0, 1, 1, 1), (1, -2, 1, 1), (1, 1, 1, 0)):
+        with pytest.raises(ValueError):
+            O.check_pattern(bad)
+    assert O.check_pattern((2, 3, 4, 5)) == (2, 3, 4, 5)
