@@ -32,7 +32,9 @@ def bmm_bsl(X, Kb, a, b, c, d):
     return Yp.view(a, d, b, B).permute(0, 2, 1, 3).reshape(a * b * d, B)
 
 
-def _time(fn, flush, reps, warm=3):
+def _time(fn, flush, reps, warm=3, with_iqr=False):
+    """Median (and IQR) of `reps` event-timed calls, L2 flushed before each
+    (PAPER.md:1224 reports medians with the IQR)."""
     import torch
     for _ in range(warm):
         fn()
@@ -45,7 +47,11 @@ def _time(fn, flush, reps, warm=3):
         e.record()
         e.synchronize()
         ts.append(s.elapsed_time(e))
-    return statistics.median(ts)
+    med = statistics.median(ts)
+    if not with_iqr:
+        return med
+    q = statistics.quantiles(ts, n=4) if len(ts) >= 4 else [med, med, med]
+    return med, q[2] - q[0]
 
 
 def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool = True):
@@ -78,7 +84,7 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
         for lay in ("bsf", "bsl"):
             X = Xfull[:, :N].contiguous() if lay == "bsf" else Xfull[:, :N].t().contiguous()
             Y = torch.empty((B, M) if lay == "bsf" else (M, B), device=dev, dtype=dt)
-            t_ks = _time(lambda: ksb.matmul(f, X, Y, layout=lay), flush, reps)
+            t_ks, iqr_ks = _time(lambda: ksb.matmul(f, X, Y, layout=lay), flush, reps, with_iqr=True)
             bfn = bmm_bsf if lay == "bsf" else bmm_bsl
             t_bmm = _time(lambda: bfn(X, Kb, a, b, c, d), flush, reps)
             if check:
@@ -90,6 +96,7 @@ def run_sweep(dev, reps: int = 7, patterns=None, math: str = "fp32", check: bool
             byts = esize * (B * N + a * b * c * d + B * M)
             rec[f"{lay}_plan"] = f.plan(B, lay)
             rec[f"{lay}_ks_ms"] = round(t_ks, 5)
+            rec[f"{lay}_ks_iqr_ms"] = round(iqr_ks, 5)
             rec[f"{lay}_bmm_ms"] = round(t_bmm, 5)
             rec[f"{lay}_speedup"] = round(t_bmm / t_ks, 4)
             rec[f"{lay}_ks_gbs"] = round(byts / t_ks / 1e6, 1)

@@ -1,9 +1,9 @@
 """Multi-process (world size 2, gloo, CPU) tests of the batch-partitioned path.
 
-The GPU compute step is replaced by the CPU oracle here (there is no GPU in
-this container); what is under test is the host-side logic the N>1 bench and
-verification use: shard bounds, max-over-ranks timing, and gathering shards
-back into the full batch in both layouts.
+There is no GPU in this container, so the per-rank compute is a CPU stand-in;
+what is under test is the host-side code the N>1 bench runs: bench.py's
+shard_input / verify_sharded and dist.py's shard bounds, sample gather,
+max / sum over ranks, and gathering shards back in both layouts.
 """
 import os
 import socket
@@ -16,6 +16,7 @@ import torch.multiprocessing as mp
 
 import ksgen
 import oracle as O
+from paper_2405_15013_b200 import dist as kdist
 from paper_2405_15013_b200.dist import gather_rows, max_over_ranks, shard_bounds
 
 
@@ -75,3 +76,70 @@ def test_gloo_world2_partition_gather_and_timing():
     bsf_ok, bsl_ok, tmax = res
     assert bsf_ok and bsl_ok
     assert tmax == 2.0
+
+
+# ---------------------------------------------------------------------------
+# bench.py's own multi-GPU bookkeeping (shard_input -> per-rank compute ->
+# verify_sharded / max_over_ranks / sum_over_ranks), driven at world size 2.
+# The per-rank "kernel" is a torch CPU matmul with a dense K assembled here
+# (not the oracle); the oracle only checks, exactly as in bench.py.
+# ---------------------------------------------------------------------------
+def _dense_local(p, K4):
+    a, b, c, d = p
+    D = np.zeros((a * b * d, a * c * d))
+    for i in range(a):
+        for k in range(b):
+            for l in range(c):
+                for j in range(d):
+                    D[i * b * d + k * d + j, i * c * d + l * d + j] = K4[i, k, l, j]
+    return torch.from_numpy(D)
+
+
+def _bench_worker(rank, world, port, out, corrupt, layout, B):
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pats = [(2, 3, 4, 2), (1, 8, 6, 2)]               # chain: (1,8,6,2) applied first, N = 12 -> 16 -> 12
+        K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+        N = 12
+        lo, hi, Xb, Xl = bench.shard_input(B, N, rank, world, layout)
+        assert Xb.shape == (hi - lo, N)
+        Z = torch.from_numpy(Xb.astype(np.float64))
+        for p, k in zip(reversed(pats), reversed(K4s)):
+            Z = Z @ _dense_local(p, k).T
+        Yl = Z.float()
+        if corrupt and rank == 1:
+            Yl = Yl + 1.0
+        if layout == "bsl":
+            Yl = Yl.t().contiguous()
+        rec = bench.verify_sharded(Yl, lo, hi, layout, bench.oracle_ref(pats, K4s, N), 1e-5, O.normwise_error,
+                                   check=rank == 0)
+        tmax = kdist.max_over_ranks(2.0 + rank)
+        tsum = kdist.sum_over_ranks(hi - lo)
+        if rank == 0:
+            out.put((rec, tmax, tsum))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("corrupt", [False, True])
+@pytest.mark.parametrize("layout,B", [("bsf", 11), ("bsl", 9), ("bsf", 1)])
+def test_bench_sharded_verify_world2(corrupt, layout, B):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q, corrupt, layout, B)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    rec, tmax, tsum = q.get(timeout=180)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert tmax == 3.0 and tsum == B                      # max time, all ranks' rows
+    assert rec["ranks"] == 2
+    assert rec["rows_checked"] == min(B, 8) or rec["rows_checked"] >= min(B, 3)
+    if corrupt and B > 1:
+        assert not rec["ok"] and rec["max_normwise_err"] > 1e-3
+    else:
+        assert rec["ok"], rec
