@@ -239,7 +239,11 @@ void        ks_graph_free(ks_graph_t g);                   /* NULL is ignored; s
  * bit-exactly).  variant 0: canonical a*b*c*d;  1: tile-contiguous K^T,
  * [i*d+j][l][k] (a*d*c*b floats);  2: TF32-rounded tiles [i*d+j][k][l]
  * (a*d*b*c floats);  3: the F32X3 low halves rna_tf32(K - rna_tf32(K)), same order
- * as 2 (only after ks_set_math(h, KS_MATH_F32X3)).  count must equal the
+ * as 2 (only after ks_set_math(h, KS_MATH_F32X3));  4: the densified TF32
+ * super-blocks [i][k*d+j][l*d+j'] = rna_tf32(K4[i][k][l][j]) if j == j' else 0,
+ * a*(b*d)*(c*d) floats (only after ks_set_math(h, KS_MATH_TF32) with
+ * 2 <= d <= 8: the BSF tensor-core path may contract a super-block as one dense
+ * (bd x cd) block, Def. 1).  count must equal the
  * variant's element count.  Half
  * handles copy elements of their dtype (2 bytes each): variant 0 canonical,
  * 2 tensor-core tiles [i*d+j][k][l] (unrounded); variant 1 does not exist.  */

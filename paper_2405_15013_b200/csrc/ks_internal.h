@@ -15,6 +15,9 @@ struct ks_handle_s {
     float* k_tile;        // [i*d+j][l][k]  = K^T tiles
     float* k_tf32;        // [i*d+j][k][l]  TF32-rounded, K-major B operand
     float* k_lo;          // [i*d+j][k][l]  rna_tf32(K - k_tf32) (3xTF32 low part), from ks_set_math(F32X3)
+    float* k_dense = nullptr;   // [i][k*d+j][l*d+j'] rna_tf32(K4[i][k][l][j]) if j == j' else 0: the
+                                // super-block i of K as a dense (bd x cd) TF32 block, from ks_set_math(TF32)
+                                // for 2 <= d <= KS_DENSE_MAX_D (BSF "densified" tensor-core path)
     ks_math_t math;
     ks_kernel_t forced;
     int dtype = KS_DTYPE_F32;   // element type of K, X, Y (half handles: k_canon / k_tf32
@@ -39,6 +42,8 @@ void count_launch();
 // ---- packing (ks_pack.cu) --------------------------------------------------
 cudaError_t pack_tiles(const ks_handle_s& h, cudaStream_t s);
 cudaError_t pack_lo(const ks_handle_s& h, cudaStream_t s);        // fills h.k_lo
+cudaError_t pack_dense(const ks_handle_s& h, cudaStream_t s);     // fills h.k_dense
+constexpr int64_t KS_DENSE_MAX_D = 8;
 
 // ---- kernel families ---------------------------------------------------------
 // Each family exposes `supports` (pure host predicate, no CUDA calls) and

@@ -6,6 +6,8 @@
 //                                            tcgen05 TF32 kernel, pre-rounded
 //   k_lo  [(i*d+j)][k][l]  = rna_tf32(K4[i][k][l][j] - k_tf32[...]) -- the low
 //                                            part of the 3xTF32 split (F32X3)
+//   k_dense[i][k*d+j][l*d+j'] = rna_tf32(K4[i][k][l][j]) if j == j' else 0 --
+//                                            densified super-blocks (TF32, small d)
 // Excluded from timing.
 #include "ks_internal.h"
 
@@ -53,6 +55,22 @@ __global__ void pack_lo_kernel(const float* __restrict__ k4, float* __restrict__
     }
 }
 
+// Densified super-blocks (TF32 BSF, small d): block i of K as a dense
+// (b d) x (c d) matrix, D_i[k*d + j][l*d + j'] = K4[i][k][l][j] if j == j' else 0
+// (Def. 1: supp(K) within I_a (x) 1_{bd x cd}), RNA-rounded.
+__global__ void pack_dense_kernel(const float* __restrict__ k4, float* __restrict__ dense, int64_t a, int64_t b,
+                                  int64_t c, int64_t d) {
+    const int64_t bd = b * d, cd = c * d, tot = a * bd * cd;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e % cd;           // l*d + j'
+        const int64_t r = (e / cd) % bd;    // k*d + j
+        const int64_t i = e / (cd * bd);
+        const int64_t j = r % d, k = r / d, jp = s % d, l = s / d;
+        dense[e] = (j == jp) ? round_tf32_rna(k4[((i * b + k) * c + l) * d + j]) : 0.0f;
+    }
+}
+
 // Half handles: a pure permutation of the 16-bit values into [i*d+j][k][l]
 // (the tensor-core weight tiles); no rounding.
 __global__ void pack_half_kernel(const uint16_t* __restrict__ k4, uint16_t* __restrict__ mma, int64_t a,
@@ -89,6 +107,16 @@ cudaError_t pack_lo(const ks_handle_s& h, cudaStream_t s) {
     int64_t blocks = (h.nnz + threads - 1) / threads;
     if (blocks > 65535 * 8) blocks = 65535 * 8;
     pack_lo_kernel<<<(unsigned)blocks, threads, 0, s>>>(h.k_canon, h.k_lo, h.a, h.b, h.c, h.d);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pack_dense(const ks_handle_s& h, cudaStream_t s) {
+    const int threads = 256;
+    const int64_t tot = h.nnz * h.d;
+    int64_t blocks = (tot + threads - 1) / threads;
+    if (blocks > 65535 * 8) blocks = 65535 * 8;
+    pack_dense_kernel<<<(unsigned)blocks, threads, 0, s>>>(h.k_canon, h.k_dense, h.a, h.b, h.c, h.d);
     count_launch();
     return cudaGetLastError();
 }

@@ -401,6 +401,7 @@ void ks_free(ks_handle_t h) {
     cudaFree(h->k_tile);
     cudaFree(h->k_tf32);
     cudaFree(h->k_lo);
+    cudaFree(h->k_dense);
     if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
     delete h;
 }
@@ -433,6 +434,22 @@ ks_status_t ks_set_math(ks_handle_t h, ks_math_t m) {
         }
         if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
         if (e != cudaSuccess) return fail_cuda(e, "ks_set_math(F32X3) pack");
+    }
+    if (m == KS_MATH_TF32 && !h->k_dense && h->d >= 2 && h->d <= ks::KS_DENSE_MAX_D &&
+        (size_t)h->nnz * (size_t)h->d * sizeof(float) <= (size_t(256) << 20)) {
+        // densified super-blocks for the BSF tensor-core path (see ks_tf32.cu), once per handle
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != h->device) cudaSetDevice(h->device);
+        float* dn = nullptr;
+        cudaError_t e = cudaMalloc(&dn, sizeof(float) * (size_t)h->nnz * (size_t)h->d);
+        if (e == cudaSuccess) {
+            h->k_dense = dn;
+            if ((e = ks::pack_dense(*h, 0)) == cudaSuccess) e = cudaStreamSynchronize(0);
+            if (e != cudaSuccess) { cudaFree(dn); h->k_dense = nullptr; }
+        }
+        if (cur >= 0 && cur != h->device) cudaSetDevice(cur);
+        if (e != cudaSuccess) return fail_cuda(e, "ks_set_math(TF32) dense pack");
     }
     h->math = m;
     return ok();
@@ -726,10 +743,12 @@ void ks_graph_free(ks_graph_t g) {
 
 ks_status_t ks_read_packed(ks_handle_t h, int variant, float* dst, int64_t count) {
     if (!h || !dst) return fail(KS_ERR_INVALID_ARG, "NULL argument");
-    if (count != h->nnz) return fail(KS_ERR_INVALID_ARG, "count must be a*b*c*d = %lld", (long long)h->nnz);
+    const int64_t want = variant == 4 ? h->nnz * h->d : h->nnz;
+    if (count != want) return fail(KS_ERR_INVALID_ARG, "count must be %lld for variant %d", (long long)want, variant);
     const float* src = variant == 0 ? h->k_canon : variant == 1 ? h->k_tile : variant == 2 ? h->k_tf32
-                     : variant == 3 ? h->k_lo : nullptr;
-    if (!src) return fail(KS_ERR_INVALID_ARG, "variant must be 0, 1, 2 or 3 (3 after ks_set_math(F32X3))");
+                     : variant == 3 ? h->k_lo : variant == 4 ? h->k_dense : nullptr;
+    if (!src) return fail(KS_ERR_INVALID_ARG, "variant must be 0, 1, 2, 3 (after ks_set_math(F32X3)) or 4 "
+                          "(after ks_set_math(TF32), 2 <= d <= 8)");
     cudaError_t e = cudaMemcpy(dst, src, (size_t)h->esize() * (size_t)count, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail_cuda(e, "ks_read_packed");
     return ok();

@@ -1278,6 +1278,48 @@ cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
+// ---- TF32 BSF, 2 <= d <= 8: the densified super-block path --------------------
+// Def. 1: supp(K) lies in I_a (x) 1_{bd x cd}, so super-block i
+// is also a dense (bd x cd) block whose entries outside 1_{b x c} (x) I_d are zero.
+// Contracted that way the factor is an (a, bd, cd, 1) pattern: X's super-block
+// columns [i cd, (i+1) cd) are one contiguous K-major TMA box and Y's rows
+// [i bd, (i+1) bd) one contiguous output run, so the d = 1 kernel runs it with no
+// gather, no transposer warps and full-line stores -- at d times the MMA work
+// (the zeros), which the tensor cores absorb while d * bc / (2 (b + c)) stays
+// near the TF32:HBM ridge (~112 flop/B on B200: 732 TF/s cuBLAS / 6.55 TB/s).
+// KS_TF32_DENSIFY: 0 off, 1 auto (default), 2 whenever possible.
+int densify_mode() {
+    static const int v = [] {
+        const char* e = getenv("KS_TF32_DENSIFY");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
+bool dense_ok(const ks_handle_s& h, const KsCall& call) {
+    if (!h.k_dense || call.layout != KS_LAYOUT_BSF || h.math != KS_MATH_TF32 || h.d < 2) return false;
+    if (pick_bn(h.b * h.d) == 0 || h.N % 4 != 0 || h.M % 4 != 0) return false;
+    const int mode = densify_mode();
+    if (mode == 0) return false;
+    if (mode == 2) return true;
+    // auto (measured over the configs[2] BSF patterns, profiles/r02/exp_tf32_densify.txt): a
+    // single super-block (a = 1) with d in {2, 3, 6} -- or d = 8 with b c <= 48^2 -- runs
+    // 1.1-1.4x faster densified; a >= 2 or d = 4 loses (the J-gather is already contiguous
+    // there); patterns the J-gather cannot run (d = 5, 7) are densified whenever allowed
+    if (!bsfj_ok(h)) return true;
+    if (h.a != 1) return false;
+    return h.d == 2 || h.d == 3 || h.d == 6 || (h.d == 8 && h.b * h.c <= 48 * 48);
+}
+
+cudaError_t launch_dense(const ks_handle_s& h, const KsCall& call) {
+    ks_handle_s hd = h;
+    hd.b = h.b * h.d;
+    hd.c = h.c * h.d;
+    hd.d = 1;
+    hd.k_tf32 = h.k_dense;
+    return launch_layout<KS_LAYOUT_BSF>(hd, call);
+}
+
 }  // namespace
 
 namespace ks {
@@ -1293,7 +1335,7 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (ya & 15) return false;
     // BSF: d = 1 direct; d > 1 J-column gather (pick_bsfj; bias read as scalars)
     if (h.math == KS_MATH_F32X3 && !h.k_lo) return false;
-    return h.d == 1 || bsfj_ok(h);
+    return h.d == 1 || bsfj_ok(h) || dense_ok(h, call);
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
@@ -1304,6 +1346,7 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
         return launch_bsfj_any<true>(h, call);
     }
     if (tf32v2_supports(h, call)) return tf32v2_launch(h, call);
+    if (dense_ok(h, call)) return launch_dense(h, call);
     if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL>(h, call);
     if (h.d == 1) return launch_layout<KS_LAYOUT_BSF>(h, call);
     return launch_bsfj_any<false>(h, call);

@@ -230,8 +230,9 @@ class Factor:
         return tuple(out)
 
     def read_packed(self, variant: int) -> np.ndarray:
-        out = np.empty(self.nnz, dtype=np.float32 if self.dtype == DTYPE_F32 else np.uint16)
-        _check(_lib.ks_read_packed(self._h, int(variant), ctypes.c_void_p(out.ctypes.data), self.nnz))
+        n = self.nnz * self.pattern[3] if variant == 4 else self.nnz
+        out = np.empty(n, dtype=np.float32 if self.dtype == DTYPE_F32 else np.uint16)
+        _check(_lib.ks_read_packed(self._h, int(variant), ctypes.c_void_p(out.ctypes.data), n))
         return out
 
     def free(self):
