@@ -135,6 +135,37 @@ ks_status_t ks_set_kernel(ks_handle_t h, ks_kernel_t k);
 /* The kernel family ks_matmul would launch for (B, layout) on this handle. */
 ks_status_t ks_plan(ks_handle_t h, int64_t B, ks_layout_t layout, ks_kernel_t* out);
 
+/* Launch-plan knobs (the paper's per-pattern "presets",
+ * PAPER.md:735, auto-tuned per pattern and GPU).  Every
+ * kernel family exposes its measured design alternatives as one bit each; the
+ * library takes them, per call, from a compiled-in table generated by an
+ * offline B200 autotune over the configs[2] sweep and configs[3]/[4] factors
+ * (key: a, b, c, d, layout, math, floor(log2 B)), else from its rules.  No knob
+ * changes the result beyond FP rounding order (FP32 kernels: bit-identical).  */
+typedef enum {
+    KS_KNOB_TF32_V2 = 1 << 0,    /* TF32 BSL / BSF d=1: resident-weight, TMA-store kernel  */
+    KS_KNOB_V2_NKB2 = 1 << 1,    /*   ... with double-buffered weight segments             */
+    KS_KNOB_DENSIFY = 1 << 2,    /* TF32 BSF 2<=d<=8: super-blocks as dense (bd x cd)       */
+    KS_KNOB_J8 = 1 << 3,         /* TF32 BSF J-gather: 32-byte runs also for b > 64        */
+    KS_KNOB_BN256 = 1 << 4,      /* TF32 BSF J=2: 256-wide output tiles                    */
+    KS_KNOB_KB32 = 1 << 5,       /* FFMA TMA ring: 32 l per chunk for b = 96 tiles          */
+    KS_KNOB_FFMA_WS = 1 << 6,    /* FFMA: warp-specialised TMA-fed kernels                 */
+    KS_KNOB_FFMA_WSG = 1 << 7    /* FFMA BSF d>1: four-j / all-j TMA kernels               */
+} ks_knob_t;
+
+/* Force the knobs of every call on this handle (autotuning, A/B tests): a
+ * mask of KS_KNOB_* bits, or -1 to return to the preset table / rules.
+ * KS_ERR_INVALID_ARG for anything else.  Not thread-safe against concurrent
+ * calls on the same handle. */
+ks_status_t ks_set_knobs(ks_handle_t h, int64_t knobs);
+
+/* The knobs a call with (B, layout) would use, and where they come from:
+ * *source = 0 rules, 1 preset table, 2 ks_set_knobs override (may be NULL). */
+ks_status_t ks_plan_knobs(ks_handle_t h, int64_t B, ks_layout_t layout, uint32_t* knobs, int* source);
+
+/* Number of entries in the compiled preset table. */
+int         ks_preset_count(void);
+
 /* ---------------------------------------------------------------------------
  * ks_matmul -- Y = X K^T for one factor: ONE fused kernel launch on `stream`,
  * no permutation passes (Alg. 2/3).

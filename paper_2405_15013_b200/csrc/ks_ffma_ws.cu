@@ -787,11 +787,7 @@ cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
     // 32 l per staged chunk pays only for b = 96 tiles (9-12 %: BSL (2,96,96,16) 365 -> 327 us,
     // BSF (64,96,96,1) 839 -> 745 us); elsewhere it is 0-10 % slower
     // (profiles/r01_ffma_kb32_negative.txt).  KS_FFMA_KB32=0 disables.
-    static const bool kb32 = [] {
-        const char* e = getenv("KS_FFMA_KB32");
-        return !(e && atoi(e) == 0);
-    }();
-    if (kb32 && h.c % 32 == 0 && pick_bn_ws(h.b) == 96)
+    if ((call.knobs & KS_KNOB_KB32) && h.c % 32 == 0 && pick_bn_ws(h.b) == 96)
         return launch_ws<LAYOUT, 96, 32>(h, call);
     return launch_ws_kb<LAYOUT, WS_BK>(h, call);
 }
@@ -806,17 +802,9 @@ namespace ks {
 // of 16; 16-byte aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 /
 // KS_FFMA_WSG=0 disable (experiments).
 bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
-    static const bool enabled = [] {
-        const char* e = getenv("KS_FFMA_WS");
-        return !(e && atoi(e) == 0);
-    }();
-    if (!enabled || h.dtype != KS_DTYPE_F32) return false;
+    if (!(call.knobs & KS_KNOB_FFMA_WS) || h.dtype != KS_DTYPE_F32) return false;
     if (call.layout == KS_LAYOUT_BSF && h.d > 1) {            // four-j kernel (d % 4 == 0)
-        static const bool gather_on = [] {
-            const char* e = getenv("KS_FFMA_WSG");
-            return !(e && atoi(e) == 0);
-        }();
-        if (!gather_on || h.c % WS_BK != 0) return false;
+        if (!(call.knobs & KS_KNOB_FFMA_WSG) || h.c % WS_BK != 0) return false;
         if (h.d % 4 == 0 ? pick_tk_wsg(h.b) == 0 : (h.d > 3 || pick_tk_wsc(h.b, h.d) == 0)) return false;
         if (h.d % 4 == 0 && (reinterpret_cast<uintptr_t>(call.bias) & 15) != 0) return false;
     } else if (pick_bn_ws(h.b) == 0 || h.c % WS_BK != 0) {

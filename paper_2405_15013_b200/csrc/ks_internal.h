@@ -22,9 +22,14 @@ struct ks_handle_s {
     ks_kernel_t forced;
     int dtype = KS_DTYPE_F32;   // element type of K, X, Y (half handles: k_canon / k_tf32
                                 // hold half values, k_tile is unused)
+    int64_t knobs_override = -1;  // ks_set_knobs: launch-plan knobs forced for this handle (-1: plan)
     int esize() const { return dtype == KS_DTYPE_F32 ? 4 : 2; }
 };
 
+// Launch-plan knobs: the KS_KNOB_* bits of include/ks.h.  The
+// runtime fills KsCall::knobs from the compiled per-pattern preset table
+// (ks_presets.inc, generated from an offline B200 autotune,
+// scripts/autotune.py), else from the rules (ks::rule_knobs).
 struct KsCall {
     const float* X;
     float* Y;
@@ -32,6 +37,7 @@ struct KsCall {
     int layout;           // ks_layout_t
     cudaStream_t stream;
     const float* bias = nullptr;   // optional length-M vector added in the epilogue
+    uint32_t knobs = 0;            // KsKnob bits (ks::plan_knobs)
 };
 
 namespace ks {
@@ -81,6 +87,13 @@ bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call);
 cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call);
 
 int num_sms(int device);
+
+// Launch-plan knobs of a call (ks_presets.cpp): the handle's ks_set_knobs
+// override, else the preset table entry for (pattern, layout, math, log2 B),
+// else the rules.  *source (optional): 0 rules, 1 preset table, 2 override.
+uint32_t plan_knobs(const ks_handle_s& h, const KsCall& call, int* source = nullptr);
+uint32_t rule_knobs(const ks_handle_s& h, const KsCall& call);
+int preset_count();
 
 }  // namespace ks
 

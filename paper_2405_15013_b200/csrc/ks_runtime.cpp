@@ -174,6 +174,7 @@ cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
 ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, int layout,
                     cudaStream_t s, const float* bias = nullptr) {
     KsCall call{X, Y, B, layout, s, bias};
+    call.knobs = ks::plan_knobs(h, call);
     ks_kernel_t k = choose(h, call);
     if (k == KS_KERNEL_AUTO)
         return fail(KS_ERR_UNSUPPORTED, "forced kernel %d cannot run pattern (%lld,%lld,%lld,%lld) "
@@ -468,11 +469,32 @@ ks_status_t ks_plan(ks_handle_t h, int64_t B, ks_layout_t layout, ks_kernel_t* o
     // Plans assume 256-byte aligned (allocator) pointers.
     KsCall call{reinterpret_cast<const float*>(uintptr_t(256)), reinterpret_cast<float*>(uintptr_t(256)),
                 B, (int)layout, nullptr};
+    call.knobs = ks::plan_knobs(*h, call);
     ks_kernel_t k = choose(*h, call);
     if (k == KS_KERNEL_AUTO) return fail(KS_ERR_UNSUPPORTED, "forced kernel cannot run this call");
     *out = k;
     return ok();
 }
+
+ks_status_t ks_set_knobs(ks_handle_t h, int64_t knobs) {
+    if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (knobs < -1 || knobs > 0xFF) return fail(KS_ERR_INVALID_ARG, "knobs must be -1 or a mask of KS_KNOB_* bits");
+    h->knobs_override = knobs;
+    return ok();
+}
+
+ks_status_t ks_plan_knobs(ks_handle_t h, int64_t B, ks_layout_t layout, uint32_t* knobs, int* source) {
+    if (!h || !knobs || B < 0) return fail(KS_ERR_INVALID_ARG, "bad argument");
+    if (layout != KS_LAYOUT_BSF && layout != KS_LAYOUT_BSL) return fail(KS_ERR_INVALID_ARG, "bad layout");
+    KsCall call{reinterpret_cast<const float*>(uintptr_t(256)), reinterpret_cast<float*>(uintptr_t(256)),
+                B, (int)layout, nullptr};
+    int src = 0;
+    *knobs = ks::plan_knobs(*h, call, &src);
+    if (source) *source = src;
+    return ok();
+}
+
+int ks_preset_count(void) { return ks::preset_count(); }
 
 ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B, ks_layout_t layout,
                       ks_stream_t stream) {

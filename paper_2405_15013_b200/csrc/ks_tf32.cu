@@ -1035,22 +1035,14 @@ struct BsfjPlan {
 // (J = 4) read X at <= 3-4 TB/s, 32-byte runs at 4.6-5.1 TB/s
 // (scripts/probe_tma_gather.cu); BN then halves (J x BN <= 512 TMEM columns) and the
 // b / BN output chunks of one X tile run on adjacent CTAs at the same time (L2 hits).
-bool j8_wide() {
-    static const bool on = [] {
-        const char* e = getenv("KS_BSFJ_J8");
-        return e && atoi(e) == 1;
-    }();
-    return on;
-}
-
 // 3xTF32 doubles every operand tile: J <= 4 there (d = 6 runs FFMA).
-BsfjPlan pick_bsfj(const ks_handle_s& h) {
+BsfjPlan pick_bsfj(const ks_handle_s& h, uint32_t knobs) {
     BsfjPlan p;
     const bool x3 = h.math == KS_MATH_F32X3;
     if (h.c % 16 != 0) return p;
     if (h.d >= 2 && h.d <= (x3 ? 4 : 8) && h.d != 5 && h.d != 7) {
         p.J = (int)h.d;
-    } else if (!x3 && h.d > 8 && h.d % 8 == 0 && (h.b <= 64 || j8_wide())) {
+    } else if (!x3 && h.d > 8 && h.d % 8 == 0 && (h.b <= 64 || (knobs & KS_KNOB_J8))) {
         p.J = 8;
         p.gather = true;
     } else if (h.d > (x3 ? 4 : 8) && h.d % 4 == 0) {
@@ -1060,12 +1052,8 @@ BsfjPlan pick_bsfj(const ks_handle_s& h) {
         return p;
     }
     // BN = 256 (UMMA N maximum) only for wide blocks with J = 2 (b = 768 in ViT-S UP):
-    // it halves the L2 re-reads of X across output chunks; KS_BSFJ_BN256=0 disables
-    static const bool bn256 = [] {
-        const char* e = getenv("KS_BSFJ_BN256");
-        return !(e && atoi(e) == 0);
-    }();
-    if (bn256 && !x3 && p.J == 2 && h.b > 128 && h.b % 256 == 0) {
+    // it halves the L2 re-reads of X across output chunks (knob KS_KNOB_BN256)
+    if ((knobs & KS_KNOB_BN256) && !x3 && p.J == 2 && h.b > 128 && h.b % 256 == 0) {
         p.BN = 256;
         return p;
     }
@@ -1149,7 +1137,7 @@ cudaError_t launch_bsfj_bn(const ks_handle_s& h, const KsCall& call, int BN) {
 
 template <bool X3>
 cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
-    const BsfjPlan p = pick_bsfj(h);
+    const BsfjPlan p = pick_bsfj(h, call.knobs);
     if (p.gather) {
         if (p.J == 4) return launch_bsfj_bn<4, X3, true>(h, call, p.BN);
         if constexpr (!X3)
@@ -1168,7 +1156,7 @@ cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
-bool bsfj_ok(const ks_handle_s& h) { return pick_bsfj(h).J != 0; }
+bool bsfj_ok(const ks_handle_s& h, uint32_t knobs) { return pick_bsfj(h, knobs).J != 0; }
 
 // Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
 // d % 4 == 0 but not 8 (d = 12, 20, ...): J = 4 from an 8-wide box.
@@ -1287,28 +1275,18 @@ cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
 // gather, no transposer warps and full-line stores -- at d times the MMA work
 // (the zeros), which the tensor cores absorb while d * bc / (2 (b + c)) stays
 // near the TF32:HBM ridge (~112 flop/B on B200: 732 TF/s cuBLAS / 6.55 TB/s).
-// KS_TF32_DENSIFY: 0 off, 1 auto (default), 2 whenever possible.
-int densify_mode() {
-    static const int v = [] {
-        const char* e = getenv("KS_TF32_DENSIFY");
-        return e ? atoi(e) : 1;
-    }();
-    return v;
-}
-
+// Chosen by the knob KS_KNOB_DENSIFY (preset table / rules, ks_presets.cpp);
+// patterns the J-gather cannot run (d = 5, 7) are densified whenever the blocks
+// exist, unless KS_TF32_DENSIFY=0 (experiments).
 bool dense_ok(const ks_handle_s& h, const KsCall& call) {
     if (!h.k_dense || call.layout != KS_LAYOUT_BSF || h.math != KS_MATH_TF32 || h.d < 2) return false;
     if (pick_bn(h.b * h.d) == 0 || h.N % 4 != 0 || h.M % 4 != 0) return false;
-    const int mode = densify_mode();
-    if (mode == 0) return false;
-    if (mode == 2) return true;
-    // auto (measured over the configs[2] BSF patterns, profiles/r02/exp_tf32_densify.txt): a
-    // single super-block (a = 1) with d in {2, 3, 6} -- or d = 8 with b c <= 48^2 -- runs
-    // 1.1-1.4x faster densified; a >= 2 or d = 4 loses (the J-gather is already contiguous
-    // there); patterns the J-gather cannot run (d = 5, 7) are densified whenever allowed
-    if (!bsfj_ok(h)) return true;
-    if (h.a != 1) return false;
-    return h.d == 2 || h.d == 3 || h.d == 6 || (h.d == 8 && h.b * h.c <= 48 * 48);
+    if (call.knobs & KS_KNOB_DENSIFY) return true;
+    static const bool never = [] {
+        const char* e = getenv("KS_TF32_DENSIFY");
+        return e && atoi(e) == 0;
+    }();
+    return !never && !bsfj_ok(h, call.knobs);
 }
 
 cudaError_t launch_dense(const ks_handle_s& h, const KsCall& call) {
@@ -1335,7 +1313,7 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (ya & 15) return false;
     // BSF: d = 1 direct; d > 1 J-column gather (pick_bsfj; bias read as scalars)
     if (h.math == KS_MATH_F32X3 && !h.k_lo) return false;
-    return h.d == 1 || bsfj_ok(h) || dense_ok(h, call);
+    return h.d == 1 || bsfj_ok(h, call.knobs) || dense_ok(h, call);
 }
 
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {

@@ -330,7 +330,7 @@ struct V2Plan {
 
 int v2_epi_bytes(int BN) { return 8 * 32 * (BN % 32 == 0 ? 32 : 16) * 4; }
 
-V2Plan v2_plan(const ks_handle_s& h, int64_t B, int sms) {
+V2Plan v2_plan(const ks_handle_s& h, int64_t B, int sms, uint32_t knobs) {
     V2Plan p;
     const int64_t nk = (h.c + 31) / 32;
     for (int bn = 256; bn >= 16; bn -= 16)
@@ -346,9 +346,7 @@ V2Plan v2_plan(const ks_handle_s& h, int64_t B, int sms) {
     p.KT = (uint32_t)(nk * p.BN * 128);
     const int fixed = v2_epi_bytes(p.BN) + 256 + 1024;
     const int room2 = V2_SMEM_MAX - fixed - 2 * (int)p.KT;
-    p.NKB = room2 >= 6 * V2_STAGE ? 2 : 1;
-    static const int nkb_env = env_int("KS_V2_NKB", 0);
-    if (nkb_env == 1 || (nkb_env == 2 && room2 >= 2 * V2_STAGE)) p.NKB = nkb_env;
+    p.NKB = room2 >= ((knobs & KS_KNOB_V2_NKB2) ? 2 : 6) * V2_STAGE ? 2 : 1;
     const int room = V2_SMEM_MAX - fixed - p.NKB * (int)p.KT;
     p.S = room / V2_STAGE;
     static const int smax = env_int("KS_V2_SMAX", 8);
@@ -371,9 +369,14 @@ bool encode5(CUtensorMap* m, const void* base, const cuuint64_t* dims, const cuu
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int v2_order() {
-    static const int v = env_int("KS_V2_ORDER", 0);
-    return v;
+// bit 0: round-robin tiles (else contiguous ranges); bit 1: BSL direct stores (else
+// TMA store); bit 2: BSL canonical SW128_32B atoms by one 5-D box (else 4 boxes).
+// Default: contiguous ranges, TMA store, canonical atoms (1.35x faster than 4 boxes
+// on (1,128,128,64) BSL, profiles/r02/exp_tf32_v2_j8.txt); KS_V2_ORDER overrides.
+int v2_order(int64_t B) {
+    static const int v = env_int("KS_V2_ORDER", -1);
+    if (v >= 0) return v;
+    return B % 32 == 0 ? 4 : 0;
 }
 
 template <int LAYOUT, int BN>
@@ -390,7 +393,7 @@ cudaError_t v2_launch_bn(const ks_handle_s& h, const KsCall& call, const V2Plan&
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
         const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
         const cuuint32_t xb[3] = {32, 1, 32};
-        if (v2_order() & 4) {
+        if (v2_order(call.B) & 4) {
             // 5-D view {32 n, 4 l, B/32 n-groups, d, a c / 4 l-groups}: one box per stage lands the
             // canonical SW128_32B atoms [l-group][n-group][4 l][32 n] (needs B % 32 == 0)
             const cuuint64_t xd5[5] = {32, 4, (cuuint64_t)call.B / 32, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c / 4)};
@@ -428,7 +431,7 @@ cudaError_t v2_launch_bn(const ks_handle_s& h, const KsCall& call, const V2Plan&
     const cudaError_t e =
         ks::launch_pdl(kern, dim3((unsigned)grid), dim3(V2_THREADS), (size_t)p.smem, call.stream, xmap, kmap, ymap,
                        call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles, p.S, p.NKB, p.KT,
-                       v2_order(), call.Y);
+                       v2_order(call.B), call.Y);
     ks::count_launch();
     return e;
 }
@@ -446,13 +449,6 @@ cudaError_t v2_launch_layout(const ks_handle_s& h, const KsCall& call, const V2P
     return cudaErrorInvalidValue;
 }
 
-bool v2_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("KS_TF32_V2");
-        return e && atoi(e) == 1;
-    }();
-    return on;
-}
 
 }  // namespace
 
@@ -461,7 +457,7 @@ namespace ks {
 // TF32 (not 3xTF32), FP32 handle, BSL any d or BSF d = 1, 16-byte aligned
 // X/Y with 16-byte row pitches (TMA), and a plan that fits shared memory.
 bool tf32v2_supports(const ks_handle_s& h, const KsCall& call) {
-    if (!v2_enabled() || h.dtype != KS_DTYPE_F32 || h.math != KS_MATH_TF32) return false;
+    if (!(call.knobs & KS_KNOB_TF32_V2) || h.dtype != KS_DTYPE_F32 || h.math != KS_MATH_TF32) return false;
     if (h.b < 16 || h.c < 16 || h.c % 8 != 0 || h.b % 16 != 0) return false;
     if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31) || call.B >= (int64_t(1) << 31))
         return false;
@@ -472,11 +468,11 @@ bool tf32v2_supports(const ks_handle_s& h, const KsCall& call) {
     } else {
         if (h.d != 1 || h.N % 4 != 0 || h.M % 4 != 0) return false;
     }
-    return v2_plan(h, call.B, 148).BN != 0;
+    return v2_plan(h, call.B, 148, call.knobs).BN != 0;
 }
 
 cudaError_t tf32v2_launch(const ks_handle_s& h, const KsCall& call) {
-    const V2Plan p = v2_plan(h, call.B, ks::num_sms(h.device));
+    const V2Plan p = v2_plan(h, call.B, ks::num_sms(h.device), call.knobs);
     if (p.BN == 0) return cudaErrorInvalidValue;
     if (call.layout == KS_LAYOUT_BSL) return v2_launch_layout<KS_LAYOUT_BSL>(h, call, p);
     return v2_launch_layout<KS_LAYOUT_BSF>(h, call, p);

@@ -19,6 +19,15 @@ BSF, BSL = 0, 1
 MATH_FP32, MATH_TF32, MATH_F32X3 = 0, 1, 2
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STREAM, KERNEL_FFMA, KERNEL_TF32 = range(5)
 KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32", 5: "fused_chain"}
+# launch-plan knobs (ks_knob_t, include/ks.h)
+KNOB_TF32_V2, KNOB_V2_NKB2, KNOB_DENSIFY, KNOB_J8, KNOB_BN256, KNOB_KB32, KNOB_FFMA_WS, KNOB_FFMA_WSG = \
+    (1 << i for i in range(8))
+KNOB_NAMES = {1: "tf32_v2", 2: "v2_nkb2", 4: "densify", 8: "j8", 16: "bn256", 32: "kb32", 64: "ffma_ws",
+              128: "ffma_wsg"}
+
+
+def preset_count() -> int:
+    return int(load_library().ks_preset_count())
 
 STATUS = {0: "KS_OK", 1: "KS_ERR_INVALID_ARG", 2: "KS_ERR_PATTERN", 3: "KS_ERR_CHAIN_SHAPE",
           4: "KS_ERR_UNSUPPORTED", 5: "KS_ERR_DEVICE", 6: "KS_ERR_ALIGNMENT", 7: "KS_ERR_OOM",
@@ -35,7 +44,8 @@ EXPORTS = ["ks_pack_weights", "ks_pack_weights_ex", "ks_get_dtype", "ks_matmul_a
            "ks_trace_enable", "ks_trace_read",
            "ks_last_error", "ks_last_error_message", "ks_status_string",
            "ks_kernel_launch_count", "ks_abi_version",
-           "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free", "ks_peak_ffma"]
+           "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free", "ks_peak_ffma",
+           "ks_set_knobs", "ks_plan_knobs", "ks_preset_count"]
 
 
 class KSError(RuntimeError):
@@ -119,6 +129,12 @@ def load_library(path: str = LIB_PATH):
     lib.ks_graph_free.restype = None
     lib.ks_peak_ffma.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     lib.ks_peak_ffma.restype = st
+    lib.ks_set_knobs.argtypes = [vp, i64]
+    lib.ks_set_knobs.restype = st
+    lib.ks_plan_knobs.argtypes = [vp, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
+    lib.ks_plan_knobs.restype = st
+    lib.ks_preset_count.argtypes = []
+    lib.ks_preset_count.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -223,6 +239,17 @@ class Factor:
         out = ctypes.c_int(0)
         _check(_lib.ks_plan(self._h, int(B), _layout(layout), ctypes.byref(out)))
         return KERNEL_NAMES[out.value]
+
+    def set_knobs(self, knobs: int):
+        """Force the launch-plan knobs (KNOB_* bits) of every call on this handle; -1 = plan."""
+        _check(_lib.ks_set_knobs(self._h, int(knobs)))
+        return self
+
+    def plan_knobs(self, B: int, layout="bsf"):
+        """(knobs, source) a call would use; source 0 rules, 1 preset table, 2 override."""
+        k, src = ctypes.c_uint32(0), ctypes.c_int(0)
+        _check(_lib.ks_plan_knobs(self._h, int(B), _layout(layout), ctypes.byref(k), ctypes.byref(src)))
+        return int(k.value), int(src.value)
 
     def get_pattern(self):
         out = (ctypes.c_int64 * 4)()
