@@ -74,7 +74,9 @@ typedef enum {
     KS_KERNEL_STREAM = 2,   /* vectorised streaming kernel, b,c in {1,2,4}  */
     KS_KERNEL_FFMA = 3,     /* register-tiled FP32 kernel, larger b,c       */
     KS_KERNEL_TF32 = 4,     /* tcgen05 TF32 tensor-core kernel              */
-    KS_KERNEL_FUSED_CHAIN = 5  /* whole chain in one launch (trace records only) */
+    KS_KERNEL_FUSED_CHAIN = 5, /* whole chain in one launch (trace records only) */
+    KS_KERNEL_SPLITC = 6       /* small B (<= 64): lanes split c, warp-shuffle
+                                  butterfly reduction           */
 } ks_kernel_t;
 
 typedef enum {

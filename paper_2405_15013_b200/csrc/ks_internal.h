@@ -67,6 +67,11 @@ cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call);
 bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call);
 
+// small-batch split-c warp-shuffle kernel (ks_splitc.cu): FP32, B <= KS_SPLITC_MAX_B
+constexpr int64_t KS_SPLITC_MAX_B = 64;
+bool splitc_supports(const ks_handle_s& h, const KsCall& call);
+cudaError_t splitc_launch(const ks_handle_s& h, const KsCall& call);
+
 bool tf32_supports(const ks_handle_s& h, const KsCall& call);
 cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call);
 // round-2 TF32 kernel (ks_tf32_v2.cu): BSL and BSF d = 1, MN-major A by TMA,

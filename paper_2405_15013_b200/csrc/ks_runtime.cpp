@@ -146,11 +146,13 @@ ks_kernel_t choose(const ks_handle_s& h, const KsCall& call) {
             case KS_KERNEL_STREAM:  return ks::stream_supports(h, call) ? KS_KERNEL_STREAM : KS_KERNEL_AUTO;
             case KS_KERNEL_FFMA:    return ks::ffma_supports(h, call) ? KS_KERNEL_FFMA : KS_KERNEL_AUTO;
             case KS_KERNEL_TF32:    return ks::tf32_supports(h, call) ? KS_KERNEL_TF32 : KS_KERNEL_AUTO;
+            case KS_KERNEL_SPLITC:  return ks::splitc_supports(h, call) ? KS_KERNEL_SPLITC : KS_KERNEL_AUTO;
             default: return KS_KERNEL_AUTO;
         }
     }
     if ((h.math == KS_MATH_TF32 || h.math == KS_MATH_F32X3) && ks::tf32_supports(h, call)) return KS_KERNEL_TF32;
     if (ks::stream_supports(h, call)) return KS_KERNEL_STREAM;
+    if (ks::splitc_supports(h, call)) return KS_KERNEL_SPLITC;
     if (ks::ffma_supports(h, call)) return KS_KERNEL_FFMA;
     return KS_KERNEL_GENERIC;
 }
@@ -166,6 +168,7 @@ cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
         case KS_KERNEL_STREAM:  return ks::stream_launch(h, call);
         case KS_KERNEL_FFMA:    return ks::ffma_launch(h, call);
         case KS_KERNEL_TF32:    return ks::tf32_launch(h, call);
+        case KS_KERNEL_SPLITC:  return ks::splitc_launch(h, call);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -458,7 +461,8 @@ ks_status_t ks_set_math(ks_handle_t h, ks_math_t m) {
 
 ks_status_t ks_set_kernel(ks_handle_t h, ks_kernel_t k) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
-    if (k < KS_KERNEL_AUTO || k > KS_KERNEL_TF32) return fail(KS_ERR_INVALID_ARG, "bad kernel %d", (int)k);
+    if (k < KS_KERNEL_AUTO || k > KS_KERNEL_SPLITC || k == KS_KERNEL_FUSED_CHAIN)
+        return fail(KS_ERR_INVALID_ARG, "bad kernel %d", (int)k);
     h->forced = k;
     return ok();
 }

@@ -18,7 +18,8 @@ LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_PKG, "lib", "libks.so")   #
 BSF, BSL = 0, 1
 MATH_FP32, MATH_TF32, MATH_F32X3 = 0, 1, 2
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STREAM, KERNEL_FFMA, KERNEL_TF32 = range(5)
-KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32", 5: "fused_chain"}
+KERNEL_SPLITC = 6
+KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32", 5: "fused_chain", 6: "splitc"}
 # launch-plan knobs (ks_knob_t, include/ks.h)
 KNOB_TF32_V2, KNOB_V2_NKB2, KNOB_DENSIFY, KNOB_J8, KNOB_BN256, KNOB_KB32, KNOB_FFMA_WS, KNOB_FFMA_WSG = \
     (1 << i for i in range(8))
