@@ -70,6 +70,7 @@ cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call);
 // small-batch split-c warp-shuffle kernel (ks_splitc.cu): FP32, B <= KS_SPLITC_MAX_B
 constexpr int64_t KS_SPLITC_MAX_B = 64;
 bool splitc_supports(const ks_handle_s& h, const KsCall& call);
+bool splitc_preferred(const ks_handle_s& h, const KsCall& call);   // the auto plan's rule
 cudaError_t splitc_launch(const ks_handle_s& h, const KsCall& call);
 
 bool tf32_supports(const ks_handle_s& h, const KsCall& call);

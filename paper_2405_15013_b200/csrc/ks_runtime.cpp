@@ -152,7 +152,7 @@ ks_kernel_t choose(const ks_handle_s& h, const KsCall& call) {
     }
     if ((h.math == KS_MATH_TF32 || h.math == KS_MATH_F32X3) && ks::tf32_supports(h, call)) return KS_KERNEL_TF32;
     if (ks::stream_supports(h, call)) return KS_KERNEL_STREAM;
-    if (ks::splitc_supports(h, call)) return KS_KERNEL_SPLITC;
+    if (ks::splitc_preferred(h, call)) return KS_KERNEL_SPLITC;
     if (ks::ffma_supports(h, call)) return KS_KERNEL_FFMA;
     return KS_KERNEL_GENERIC;
 }

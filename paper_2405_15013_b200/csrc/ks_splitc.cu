@@ -126,10 +126,14 @@ namespace ks {
 // B >= 32 with more than 8 M multiply-adds per call the FFMA / generic kernels win.
 bool splitc_supports(const ks_handle_s& h, const KsCall& call) {
     if (h.dtype != KS_DTYPE_F32 || call.B < 1 || call.B > KS_SPLITC_MAX_B) return false;
-    if (call.layout == KS_LAYOUT_BSL && call.B > 16 && call.B * h.nnz > (int64_t(8) << 20)) return false;
     if (h.b % SC_K != 0 || h.c < 16 || h.c > 256) return false;
     if (h.a * h.d * h.c >= (int64_t(1) << 31) || h.a * h.d * h.b >= (int64_t(1) << 31)) return false;
     return true;
+}
+
+bool splitc_preferred(const ks_handle_s& h, const KsCall& call) {
+    if (!splitc_supports(h, call)) return false;
+    return !(call.layout == KS_LAYOUT_BSL && call.B > 16 && call.B * h.nnz > (int64_t(8) << 20));
 }
 
 cudaError_t splitc_launch(const ks_handle_s& h, const KsCall& call) {
