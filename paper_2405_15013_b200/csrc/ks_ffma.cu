@@ -66,10 +66,15 @@ struct Cfg {
     static_assert(WARPS <= 8, "at most 8 warps");
 };
 
-template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK>
+// SC (scalar): X loads and Y stores element by element with predicated tails, for
+// BSL batches with B % 4 != 0 and for X / Y views that are only 4-byte aligned
+// (the vector path needs 16 bytes); the arithmetic (l ascending, one FMA chain per
+// output) is the same, so the results are bit-identical to the vector path.
+template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK, bool SC = false>
 __global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>::THREADS, KS_FFMA_MINB)
 ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float* __restrict__ Y,
                const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
+    static_assert(!SC || J == 1, "scalar path: one j per CTA");
     using C = Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>;
     constexpr int BK = C::BK;
     using VT = typename VecJ<J>::T;
@@ -125,9 +130,16 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
                 if (idx < C::A_VECS) {
                     const int l = idx / (C::BMJ / 4);
                     const int n4 = idx % (C::BMJ / 4);
-                    const int64_t n = min(n0 + 4 * n4, B - 4);          // B % 4 == 0
                     const int64_t s = (int64_t)i * c * d + (int64_t)(l0 + l) * d + j0;
-                    ra[r] = __ldg(reinterpret_cast<const float4*>(X + s * B + n));
+                    if constexpr (SC) {               // any B, 4-byte alignment: clamped scalar loads
+                        const int64_t n = n0 + 4 * n4;
+                        const float* xs = X + s * B;
+                        ra[r] = make_float4(__ldg(xs + min(n, B - 1)), __ldg(xs + min(n + 1, B - 1)),
+                                            __ldg(xs + min(n + 2, B - 1)), __ldg(xs + min(n + 3, B - 1)));
+                    } else {
+                        const int64_t n = min(n0 + 4 * n4, B - 4);          // B % 4 == 0
+                        ra[r] = __ldg(reinterpret_cast<const float4*>(X + s * B + n));
+                    }
                 }
             }
         } else {
@@ -250,9 +262,14 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
             float* yr = Y + r * B + n0 + rowA;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                if (n0 + rowA + 32 * h < B)
+                if constexpr (SC) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (n0 + rowA + 32 * h + e < B) __stcs(yr + 32 * h + e, acc[4 * h + e][q]);
+                } else if (n0 + rowA + 32 * h < B) {
                     __stcs(reinterpret_cast<float4*>(yr + 32 * h),
                            make_float4(acc[4 * h][q], acc[4 * h + 1][q], acc[4 * h + 2][q], acc[4 * h + 3][q]));
+                }
             }
         }
     } else if (d == 1) {
@@ -262,7 +279,10 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
             const int64_t n = n0 + rowA + (m & 3) + 32 * (m >> 2);
             if (n >= B) continue;
             float* yr = Y + n * M + (int64_t)i * b + k0 + colB;
-            if constexpr (TN == 8) {
+            if constexpr (SC) {
+#pragma unroll
+                for (int q = 0; q < TN; ++q) __stcs(yr + q, acc[m][q]);
+            } else if constexpr (TN == 8) {
                 __stcs(reinterpret_cast<float4*>(yr), make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]));
                 __stcs(reinterpret_cast<float4*>(yr + 4), make_float4(acc[m][4], acc[m][5], acc[m][6], acc[m][7]));
             } else {
@@ -333,10 +353,10 @@ int pick_j(const ks_handle_s& h, const KsCall& call) {
     return 1;
 }
 
-template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK>
+template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK, bool SC = false>
 cudaError_t launch_cfg(const ks_handle_s& h, const KsCall& call) {
     using C = Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>;
-    auto kern = ks_ffma_kernel<LAYOUT, J, WPJM, WPJN, TN, KBK>;
+    auto kern = ks_ffma_kernel<LAYOUT, J, WPJM, WPJN, TN, KBK, SC>;
     static bool attr_set[64] = {false};
     if (!attr_set[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -354,7 +374,7 @@ cudaError_t launch_cfg(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
-template <int LAYOUT, int J>
+template <int LAYOUT, int J, bool SC = false>
 cudaError_t launch_j(const ks_handle_s& h, const KsCall& call) {
     int wpjn = 0, tn = 0;
     if (!pick_bn(h.b, J, &wpjn, &tn)) return cudaErrorInvalidValue;
@@ -362,8 +382,8 @@ cudaError_t launch_j(const ks_handle_s& h, const KsCall& call) {
 #define KS_FFMA_CASE(WN, T)                                                                \
     if (wpjn == WN && tn == T) {                                                           \
         if constexpr (8 / (J * WN) >= 1 && (8 % (J * WN)) == 0)                            \
-            return ffma_bk(h) == 16 ? launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T, 16>(h, call)   \
-                                    : launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T, 8>(h, call);   \
+            return ffma_bk(h) == 16 ? launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T, 16, SC>(h, call)   \
+                                    : launch_cfg<LAYOUT, J, 8 / (J * WN), WN, T, 8, SC>(h, call);   \
     }
     if constexpr (J <= 2) {
         KS_FFMA_CASE(4, 8)
@@ -386,14 +406,23 @@ bool ffma_supports(const ks_handle_s& h, const KsCall& call) {
     int wpjn, tn;
     if (!pick_bn(h.b, 1, &wpjn, &tn)) return false;
     if (h.b > (1 << 20) || h.c > (1 << 20) || h.a * h.d > (int64_t(1) << 30)) return false;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
-    if ((al & 15) != 0) return false;                 // vector loads/stores need 16 B
-    if (call.layout == KS_LAYOUT_BSL && call.B % 4 != 0) return false;
+    // 4-byte aligned X / Y (the ABI minimum): BSL with B % 4 != 0 or views that are
+    // not 16-byte aligned run the scalar (SC) instantiation, bit-identical results
     return true;
+}
+
+// the vector path needs 16-byte aligned X / Y and, in BSL, B % 4 == 0
+bool ffma_vec_ok(const KsCall& call) {
+    const uintptr_t al = reinterpret_cast<uintptr_t>(call.X) | reinterpret_cast<uintptr_t>(call.Y);
+    return (al & 15) == 0 && (call.layout != KS_LAYOUT_BSL || call.B % 4 == 0);
 }
 
 cudaError_t ffma_launch(const ks_handle_s& h, const KsCall& call) {
     if (ffma_ws_supports(h, call)) return ffma_ws_launch(h, call);
+    if (!ffma_vec_ok(call)) {
+        if (call.layout == KS_LAYOUT_BSL) return launch_j<KS_LAYOUT_BSL, 1, true>(h, call);
+        return launch_j<KS_LAYOUT_BSF, 1, true>(h, call);
+    }
     if (call.layout == KS_LAYOUT_BSL) return launch_j<KS_LAYOUT_BSL, 1>(h, call);
     switch (pick_j(h, call)) {
         case 4: return launch_j<KS_LAYOUT_BSF, 4>(h, call);

@@ -65,6 +65,6 @@ def test_splitc_plan_boundary(ksb):
     assert f.plan(65, "bsf") != "splitc"
     assert f.plan(64, "bsl") == "splitc"
     h = ksb.Factor(64, 64, 64, 1, ksgen.k4_uniform(64, 64, 64, 1, seed=1))  # BSL, B >= 32, > 8 M MACs
-    assert h.plan(16, "bsl") == "splitc" and h.plan(32, "bsl") != "splitc" and h.plan(64, "bsf") == "splitc"
+    assert h.plan(16, "bsl") == "splitc" and h.plan(40, "bsl") != "splitc" and h.plan(64, "bsf") == "splitc"
     g = ksb.Factor(1, 60, 64, 1, ksgen.k4_uniform(1, 60, 64, 1, seed=1))     # b % 8 != 0
     assert g.plan(8, "bsf") != "splitc"
