@@ -227,6 +227,36 @@ ks_status_t ks_set_chain_fusion(int enable);
 int ks_chain_fusion_eligible(const ks_handle_t* handles, int L, int64_t B, ks_layout_t layout);
 
 /* ---------------------------------------------------------------------------
+ * Mixed layouts.  The paper fixes one layout per call (BSF: X is B x N
+ * row-major; BSL: X^T, N x B, the layout its kernel favours,
+ * PAPER.md:631-641 "batch-size-last").  Inside a chain the intermediates are
+ * the library's own buffers, so their layout is free.
+ *
+ * ks_matmul_io -- Y = X K^T with X in x_layout and Y in y_layout (X: device,
+ *   B*N floats; Y: device, B*M floats; 4-byte aligned, no overlap).  FP32
+ *   handles only.  x_layout == y_layout is ks_matmul.  Mixed pairs run the
+ *   TF32 tensor-core kernel (math KS_MATH_TF32: BSF in / BSL out for any
+ *   pattern it supports in BSF; BSL in / BSF out for d = 1 and d in
+ *   {2,3,4,6,8} or d % 4 == 0, B % 4 == 0, Y 16-byte aligned), else the
+ *   generic kernel (FP32, any pattern).  Errors as ks_matmul.
+ *
+ * ks_set_chain_mixed_layouts -- process-wide policy (default on): a BSF chain
+ *   of TF32 factors keeps each intermediate next to a factor with d > 8 in
+ *   BSL, so that factor's d-strided BSF gather or store is
+ *   replaced by unit-stride batch runs; used only when every call of the chain
+ *   then runs the TF32 kernel.  X and Y keep the caller's layout; results
+ *   are those of the per-factor calls in the chosen layouts.
+ * ks_chain_layouts -- the plan a ks_chain_ex call would use: out[t] = layout
+ *   of the output of handles[t] (out[0] = Y's, the caller's), out[L] = X's
+ *   (L+1 ints); handles[t] reads out[t+1] and writes out[t].
+ *   Returns 1 if any intermediate is mixed, 0 if uniform, -1 on bad arguments.
+ * ------------------------------------------------------------------------- */
+ks_status_t ks_matmul_io(ks_handle_t h, const float* X, ks_layout_t x_layout, float* Y, ks_layout_t y_layout,
+                         int64_t B, ks_stream_t stream);
+ks_status_t ks_set_chain_mixed_layouts(int enable);
+int ks_chain_layouts(const ks_handle_t* handles, int L, int64_t B, ks_layout_t layout, int* out);
+
+/* ---------------------------------------------------------------------------
  * ks_chain_host -- end-to-end form of ks_chain_ex for HOST buffers: X_host and
  * Y_host are host memory (pinned for full PCIe speed and copy/compute
  * overlap; pageable works but the copies then serialise).  The batch is cut

@@ -8,5 +8,6 @@ from .ks import (  # noqa: F401
     KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STREAM, KERNEL_FFMA, KERNEL_TF32, KERNEL_SPLITC,
     Factor, KSError, matmul, chain, chain_host, launch_count, load_library, LIB_PATH, EXPORTS,
     trace_enable, trace_read, set_chain_fusion, chain_fusion_eligible, ChainGraph, peak_ffma_tflops,
+    matmul_io, set_chain_mixed_layouts, chain_layouts,
 )
 from .kslinear import KSLinear  # noqa: F401

@@ -373,6 +373,7 @@ namespace ks {
 // all dimensions equal to N, N % 4 == 0, at least one row fits in shared
 // memory, 16-byte aligned X and Y.
 bool fused_chain_supports(const ks_handle_t* hs, int L, const KsCall& call) {
+    if (call.mixed()) return false;
     if (call.layout != KS_LAYOUT_BSF || L < 2 || L > MAXF) return false;
     const int64_t bb = hs[0]->b;
     if (bb != 2 && bb != 4) return false;

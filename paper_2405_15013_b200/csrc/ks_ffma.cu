@@ -402,6 +402,7 @@ cudaError_t launch_j(const ks_handle_s& h, const KsCall& call) {
 namespace ks {
 
 bool ffma_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (h.c % 8 != 0) return false;
     int wpjn, tn;
     if (!pick_bn(h.b, 1, &wpjn, &tn)) return false;

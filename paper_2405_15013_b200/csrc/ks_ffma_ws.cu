@@ -802,6 +802,7 @@ namespace ks {
 // of 16; 16-byte aligned X / Y; 32-bit TMA coordinates.  KS_FFMA_WS=0 /
 // KS_FFMA_WSG=0 disable (experiments).
 bool ffma_ws_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (!(call.knobs & KS_KNOB_FFMA_WS) || h.dtype != KS_DTYPE_F32) return false;
     if (call.layout == KS_LAYOUT_BSF && h.d > 1) {            // four-j kernel (d % 4 == 0)
         if (!(call.knobs & KS_KNOB_FFMA_WSG) || h.c % WS_BK != 0) return false;

@@ -14,7 +14,9 @@
 
 namespace {
 
-template <int LAYOUT>
+// XL / YL: layouts of X and Y (equal except for ks_matmul_io and mixed-layout
+// chain intermediates); outputs are enumerated in Y's order.
+template <int XL, int YL>
 __global__ void __launch_bounds__(256) ks_generic_kernel(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
     const float* __restrict__ bias, int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
@@ -25,7 +27,7 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         int64_t n, r;
-        if (LAYOUT == KS_LAYOUT_BSF) { n = e / M; r = e - n * M; }
+        if (YL == KS_LAYOUT_BSF) { n = e / M; r = e - n * M; }
         else                         { r = e / B; n = e - r * B; }
         const int64_t i = r / (b * d);
         const int64_t rem = r - i * b * d;
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
         float acc = 0.f;
         for (int64_t l = 0; l < c; ++l) {
             const int64_t s = s0 + l * d;
-            const float x = LAYOUT == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n];
+            const float x = XL == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n];
             acc = fmaf(x, kp[l * d], acc);
         }
         Y[e] = bias ? acc + bias[r] : acc;
@@ -46,7 +48,7 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
 // Half-precision generic kernel: same reduction order, FP32 accumulation,
 // output rounded to nearest-even (half handles whose pattern the tensor-core
 // kernel cannot take).
-template <typename T, int LAYOUT>
+template <typename T, int XL, int YL>
 __global__ void __launch_bounds__(256) ks_generic_half_kernel(
     const T* __restrict__ X, const T* __restrict__ K4, T* __restrict__ Y, const T* __restrict__ bias,
     int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(256) ks_generic_half_kernel(
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         int64_t n, r;
-        if (LAYOUT == KS_LAYOUT_BSF) { n = e / M; r = e - n * M; }
+        if (YL == KS_LAYOUT_BSF) { n = e / M; r = e - n * M; }
         else                         { r = e / B; n = e - r * B; }
         const int64_t i = r / (b * d);
         const int64_t rem = r - i * b * d;
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(256) ks_generic_half_kernel(
         float acc = 0.f;
         for (int64_t l = 0; l < c; ++l) {
             const int64_t s = s0 + l * d;
-            const float x = (float)(LAYOUT == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n]);
+            const float x = (float)(XL == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n]);
             acc = fmaf(x, (float)kp[l * d], acc);
         }
         if (bias) acc += (float)bias[r];
@@ -88,8 +90,10 @@ cudaError_t launch_generic_half(const ks_handle_s& h, const KsCall& call) {
     T* Y = reinterpret_cast<T*>(call.Y);
     const T* K = reinterpret_cast<const T*>(h.k_canon);
     const T* bias = reinterpret_cast<const T*>(call.bias);
-    auto kern = call.layout == KS_LAYOUT_BSF ? ks_generic_half_kernel<T, KS_LAYOUT_BSF>
-                                             : ks_generic_half_kernel<T, KS_LAYOUT_BSL>;
+    constexpr int F = KS_LAYOUT_BSF, L = KS_LAYOUT_BSL;
+    const bool xf = call.layout == F, yf = call.ylayout() == F;
+    auto kern = xf ? (yf ? ks_generic_half_kernel<T, F, F> : ks_generic_half_kernel<T, F, L>)
+                   : (yf ? ks_generic_half_kernel<T, L, F> : ks_generic_half_kernel<T, L, L>);
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, X, K, Y, bias,
                                          call.B, (int64_t)h.a, (int64_t)h.b, (int64_t)h.c, (int64_t)h.d);
     ks::count_launch();
@@ -114,7 +118,10 @@ cudaError_t generic_launch(const ks_handle_s& h, const KsCall& call) {
     const int64_t cap = (int64_t)num_sms(h.device) * 8 * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    auto kern = call.layout == KS_LAYOUT_BSF ? ks_generic_kernel<KS_LAYOUT_BSF> : ks_generic_kernel<KS_LAYOUT_BSL>;
+    constexpr int F = KS_LAYOUT_BSF, L = KS_LAYOUT_BSL;
+    const bool xf = call.layout == F, yf = call.ylayout() == F;
+    auto kern = xf ? (yf ? ks_generic_kernel<F, F> : ks_generic_kernel<F, L>)
+                   : (yf ? ks_generic_kernel<L, F> : ks_generic_kernel<L, L>);
     const cudaError_t e = launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, call.X,
                                      (const float*)h.k_canon, call.Y, call.bias, call.B, (int64_t)h.a, (int64_t)h.b,
                                      (int64_t)h.c, (int64_t)h.d);

@@ -268,6 +268,7 @@ cudaError_t launch_hb(const ks_handle_s& h, const KsCall& call) {
 namespace ks {
 
 bool half_bsl_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (h.b < 16 || h.c < 16 || h.c % 16 != 0 || hb_pick_bn(h.b) == 0) return false;
     if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31)) return false;
     if (call.B >= (int64_t(1) << 31) || call.B % 8 != 0) return false;

@@ -38,6 +38,9 @@ struct KsCall {
     cudaStream_t stream;
     const float* bias = nullptr;   // optional length-M vector added in the epilogue
     uint32_t knobs = 0;            // KsKnob bits (ks::plan_knobs)
+    int out_layout = -1;           // layout of Y (ks_matmul_io / chain intermediates); -1: `layout`
+    int ylayout() const { return out_layout < 0 ? layout : out_layout; }
+    bool mixed() const { return ylayout() != layout; }
 };
 
 namespace ks {

@@ -175,14 +175,15 @@ cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
 
 // One factor, arguments already validated.
 ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, int layout,
-                    cudaStream_t s, const float* bias = nullptr) {
+                    cudaStream_t s, const float* bias = nullptr, int out_layout = -1) {
     KsCall call{X, Y, B, layout, s, bias};
+    call.out_layout = out_layout;
     call.knobs = ks::plan_knobs(h, call);
     ks_kernel_t k = choose(h, call);
     if (k == KS_KERNEL_AUTO)
         return fail(KS_ERR_UNSUPPORTED, "forced kernel %d cannot run pattern (%lld,%lld,%lld,%lld) "
-                    "B=%lld layout=%d", (int)h.forced, (long long)h.a, (long long)h.b,
-                    (long long)h.c, (long long)h.d, (long long)B, layout);
+                    "B=%lld layout=%d->%d", (int)h.forced, (long long)h.a, (long long)h.b,
+                    (long long)h.c, (long long)h.d, (long long)B, layout, call.ylayout());
     TraceRec rec{nullptr, nullptr, (int)k, 0.0};
     const bool tracing = g_trace_on.load(std::memory_order_relaxed) && !t_capturing;
     if (tracing) {
@@ -227,6 +228,43 @@ ks_status_t validate_chain(const ks_handle_t* hs, int L, int64_t B, int layout) 
 }
 
 std::atomic<bool> g_fusion{true};
+std::atomic<bool> g_mixed{true};
+
+// Mixed-layout intermediates (BSF chains of TF32 factors): an intermediate next
+// to a factor with d > 8 is kept batch-size-last, so that factor reads (BSL in:
+// each j's operand rows are 512-byte runs, no d-strided gather) or writes
+// (BSL out: 128-byte warp stores per output row) it without the BSF d > 1
+// penalty of PAPER.md:641.  d > 8 because only there the BSF kernel gathers J < d
+// columns per tile (32-byte runs); for d <= 8 (J = d, whole-row runs) measured
+// on B200 the uniform plan is as fast or faster (profiles/r02/time_models_m1.jsonl:
+// ViT-S chains 8-12% slower mixed, GPT-2 UP 13% faster).  lay[t] = layout of the output of hs[t] (lay[0] = Y's,
+// the caller's); lay[L] = X's; so hs[t] reads lay[t + 1] and writes lay[t].
+// Applied only when every resulting call runs the TF32 tensor-core family
+// (pointers: the 256-byte aligned workspace, X and Y as given); else uniform.
+bool plan_chain_layouts(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B, int layout,
+                        int* lay) {
+    for (int t = 0; t <= L; ++t) lay[t] = layout;
+    if (!g_mixed.load(std::memory_order_relaxed) || layout != KS_LAYOUT_BSF || L < 2) return false;
+    bool any = false;
+    for (int t = 0; t + 1 < L; ++t)          // output of hs[t + 1] = input of hs[t]
+        if (hs[t]->d > 8 || hs[t + 1]->d > 8) {
+            lay[t + 1] = KS_LAYOUT_BSL;
+            any = true;
+        }
+    if (!any) return false;
+    const float* ws = reinterpret_cast<const float*>(uintptr_t(256));
+    for (int t = 0; t < L; ++t) {
+        const ks_handle_s& h = *hs[t];
+        if (h.forced != KS_KERNEL_AUTO || h.math != KS_MATH_TF32 || h.dtype != KS_DTYPE_F32) break;
+        KsCall call{t == L - 1 ? X : ws, t == 0 ? Y : const_cast<float*>(ws), B, lay[t + 1], nullptr};
+        call.out_layout = lay[t];
+        call.knobs = ks::plan_knobs(h, call);
+        if (choose(h, call) != KS_KERNEL_TF32) break;
+        if (t == L - 1) return true;
+    }
+    for (int t = 0; t <= L; ++t) lay[t] = layout;
+    return false;
+}
 
 bool fusion_ok(const ks_handle_t* hs, int L, const KsCall& call) {
     if (!g_fusion.load(std::memory_order_relaxed) || L < 2) return false;
@@ -297,11 +335,13 @@ ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, in
         }
     }
     ks_status_t st = KS_OK;
+    std::vector<int> lay(L + 1);
+    plan_chain_layouts(hs, L, X, Y, B, layout, lay.data());
     const float* in = X;
     for (int l = L - 1; l >= 0 && st == KS_OK; --l) {
         float* out = (l == 0) ? Y : static_cast<float*>(buf[(L - 1 - l) % nbuf]);
-        st = run_one(*hs[l], in, out, B, layout, s, l == 0 ? bias : nullptr);   // bias after the last hop
-        in = out;
+        st = run_one(*hs[l], in, out, B, lay[l + 1], s, l == 0 ? bias : nullptr, lay[l]);
+        in = out;                                                    // bias after the last hop
     }
     if (!ws)
         for (int i = 0; i < nbuf; ++i) cudaFreeAsync(buf[i], s);
@@ -571,6 +611,39 @@ ks_status_t ks_get_dtype(ks_handle_t h, ks_dtype_t* out) {
 ks_status_t ks_set_chain_fusion(int enable) {
     g_fusion.store(enable != 0);
     return ok();
+}
+
+ks_status_t ks_set_chain_mixed_layouts(int enable) {
+    g_mixed.store(enable != 0);
+    return ok();
+}
+
+int ks_chain_layouts(const ks_handle_t* hs, int L, int64_t B, ks_layout_t layout, int* out) {
+    if (!out || validate_chain(hs, L, B, (int)layout) != KS_OK) return -1;
+    const float* p = reinterpret_cast<const float*>(uintptr_t(256));
+    const int mixed = plan_chain_layouts(hs, L, p, const_cast<float*>(p), B, (int)layout, out) ? 1 : 0;
+    ok();
+    return mixed;
+}
+
+ks_status_t ks_matmul_io(ks_handle_t h, const float* X, ks_layout_t x_layout, float* Y, ks_layout_t y_layout,
+                         int64_t B, ks_stream_t stream) {
+    if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (h->dtype != KS_DTYPE_F32) return fail(KS_ERR_INVALID_ARG, "half handle: ks_matmul_io is FP32 / TF32 only");
+    if (B < 0) return fail(KS_ERR_INVALID_ARG, "B must be >= 0");
+    for (int l : {(int)x_layout, (int)y_layout})
+        if (l != KS_LAYOUT_BSF && l != KS_LAYOUT_BSL) return fail(KS_ERR_INVALID_ARG, "bad layout %d", l);
+    ks_status_t s = check_device(h);
+    if (s != KS_OK) return s;
+    if (B == 0) return ok();
+    if (!X || !Y) return fail(KS_ERR_INVALID_ARG, "NULL X or Y");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 3)
+        return fail(KS_ERR_ALIGNMENT, "X and Y must be 4-byte aligned");
+    int64_t xb, yb;
+    if (!mul_ok(B, h->N * 4, &xb) || !mul_ok(B, h->M * 4, &yb)) return fail(KS_ERR_INVALID_ARG, "B too large");
+    if (overlap(X, xb, Y, yb)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
+    s = run_one(*h, X, Y, B, (int)x_layout, static_cast<cudaStream_t>(stream), nullptr, (int)y_layout);
+    return s == KS_OK ? ok() : s;
 }
 
 int ks_chain_fusion_eligible(const ks_handle_t* hs, int L, int64_t B, ks_layout_t layout) {

@@ -125,6 +125,7 @@ namespace ks {
 // BSL up to B = 16; in BSL a warp's 4 rows are 16-byte pieces of each X row, so at
 // B >= 32 with more than 8 M multiply-adds per call the FFMA / generic kernels win.
 bool splitc_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (h.dtype != KS_DTYPE_F32 || call.B < 1 || call.B > KS_SPLITC_MAX_B) return false;
     if (h.b % SC_K != 0 || h.c < 16 || h.c > 256) return false;
     if (h.a * h.d * h.c >= (int64_t(1) << 31) || h.a * h.d * h.b >= (int64_t(1) << 31)) return false;

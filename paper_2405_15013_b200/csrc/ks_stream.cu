@@ -226,6 +226,7 @@ cudaError_t dispatch_c(const ks_handle_s& h, const KsCall& call) {
 namespace ks {
 
 bool stream_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (!small_bc(h.b) || !small_bc(h.c)) return false;
     if (h.a > (int64_t(1) << 30) || h.d > (int64_t(1) << 30)) return false;
     if (call.layout == KS_LAYOUT_BSL && h.a * h.d > (int64_t(1) << 31) / 64) return false;

@@ -41,7 +41,9 @@ constexpr int NTHREADS = 320;
 // RB = bytes of K per operand row per stage: 128 (SWIZZLE_128B; TF32 32 l, half
 // 64 l) or 64 (SWIZZLE_64B, 16 l) for the 3xTF32 split (X3), whose doubled A
 // and B tiles would not leave room for two CTAs per SM at 128.
-template <int LAYOUT, int BN, bool X3 = false>
+// OUTL: layout of Y (= LAYOUT except for the mixed-layout calls of ks_matmul_io
+// and chain intermediates: BSF in / BSL out, or BSL in / BSF out with d = 1).
+template <int LAYOUT, int BN, bool X3 = false, int OUTL = LAYOUT>
 struct Tf32Cfg {
     static constexpr int RB = X3 ? 64 : 128;
     static constexpr int A_TILE = BM * RB;                // 16 KB (8 KB for X3)
@@ -58,7 +60,7 @@ struct Tf32Cfg {
     static constexpr int BUDGET = CTAS == 2 ? 110 * 1024 : 200 * 1024;
     static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 || X3 ? 3 : 2) : 3) : 0;   // staging
     // BSF: 4 epilogue warps x 32 rows x (4 + 1) 16-byte units of store scratch (WarpStore<float, 1, 16>)
-    static constexpr int SCR = LAYOUT == KS_LAYOUT_BSL ? 0 : 4 * 32 * 5 * 16;
+    static constexpr int SCR = OUTL == KS_LAYOUT_BSL ? 0 : 4 * 32 * 5 * 16;
     static constexpr int S_FIT = (BUDGET - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 6 ? 6 : S_FIT;                              // operand slots
     static constexpr int SCR_OFF = S * SLOT + P * STG;
@@ -108,12 +110,12 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-template <int LAYOUT, int BN, typename T = float, bool X3 = false>
-__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3>::CTAS)
+template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT>
+__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3, OUTL>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap kmap_lo, T* __restrict__ Y, const T* __restrict__ bias,
                int64_t B, int a, int b, int c, int d, int64_t ntiles, int dbg) {
-    using C = Tf32Cfg<LAYOUT, BN, X3>;
+    using C = Tf32Cfg<LAYOUT, BN, X3, OUTL>;
     static_assert(LAYOUT != KS_LAYOUT_BSL || sizeof(T) == 4, "half BSL runs the swap-AB kernel (ks_half_bsl.cu)");
     static_assert(!X3 || sizeof(T) == 4, "3xTF32 is an FP32 mode");
     constexpr int RB = C::RB;
@@ -337,8 +339,15 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     for (int e = 0; e < 16; ++e)
                         v[e] += ElemTraits<T>::to_f(bias[(int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j]);
                 }
-                if constexpr (LAYOUT != KS_LAYOUT_BSL) {
-                    // BSF (d = 1): row n's 16 outputs are contiguous; coalesce through scratch
+                if constexpr (OUTL != KS_LAYOUT_BSL) {
+                    // BSF out (d = 1): row n's 16 outputs are contiguous; coalesce through scratch
+                    if constexpr (sizeof(T) == 4) {
+                        if (dbg & 4) {            // experiment: direct stores, no shared-memory staging
+                            direct_store_rows<1, 16>(vv, Y, (int64_t)tc.n0 + lq * 32, B, M,
+                                                     (int64_t)tc.i * b + tc.k0 + col, 1, lane);
+                            continue;
+                        }
+                    }
                     if (!(dbg & 1))
                         warp_store_rows<T, 1, 16>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, 1, 16>::BYTES, vv, Y,
                                                   (int64_t)tc.n0 + lq * 32, B, M, (int64_t)tc.i * b + tc.k0 + col, 1, lane);
@@ -382,7 +391,14 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 // epilogue stores through warp_store_rows (coalesced 16-byte units; direct
 // per-row stores touched 32 sectors per instruction, 4x ideal).
 // ==========================================================================
-template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false>
+// INL / OUTL: layouts of X and Y.  INL = BSL (the mixed BSL-in / BSF-out calls
+// of ks_matmul_io and chain intermediates): one 3-D TMA box {128 n, J j, BKJ l}
+// of X viewed as [a*c][d][B] per stage, staged [l][j][n] (each j's run of 128
+// batch values is 512 contiguous bytes: no gather), and the transposers read
+// it with conflict-free 4-byte loads.  OUTL = BSL: the epilogue writes each
+// output row r = (i, k, j) of Y^T as 128-byte warp stores (lane = batch row).
+template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false, int INL = KS_LAYOUT_BSF,
+          int OUTL = KS_LAYOUT_BSF>
 struct Tf32JCfg {
     static constexpr int RB = BKJ * 4;                    // operand row bytes (SW32 / SW64)
     static constexpr int NA = X3 ? 2 : 1;                 // hi (+ lo) tiles
@@ -391,11 +407,11 @@ struct Tf32JCfg {
     static constexpr int SLOT = J * NA * (AJ_TILE + BJ_TILE);
     // staged row: [BKJ l][J j] + padding: 4 floats past the run (2-D box), or one
     // more l (3-D box; J = 8 then gives an even pitch: 2-way read conflicts)
-    static constexpr int STG_ROW = GATHER ? (BKJ + 1) * J * 4 : BKJ * J * 4 + 16;
+    static constexpr int STG_ROW = INL == KS_LAYOUT_BSL ? BKJ * J * 4 : GATHER ? (BKJ + 1) * J * 4 : BKJ * J * 4 + 16;
     static constexpr int STG = BM * STG_ROW;
     static constexpr int NACC = 2 * J * BN <= 512 ? 2 : 1;
     static constexpr int EC = J > 2 ? 8 : 16;             // epilogue columns per TMEM load
-    static constexpr int SCR = 4 * WarpStore<float, J, EC>::BYTES;    // epilogue store scratch
+    static constexpr int SCR = OUTL == KS_LAYOUT_BSL ? 0 : 4 * WarpStore<float, J, EC>::BYTES;    // store scratch
     // X staging ring: ~96 KB of X loads in flight per SM (Little's law: ~45 GB/s
     // per SM x ~2 us loaded latency), leaving room for 2 operand slots; measured:
     // P = 2 at BKJ = 8 (36 KB in flight) left the J = 3 kernel latency-bound.
@@ -439,13 +455,15 @@ __device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_
     return t;
 }
 
-template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false>
+template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false, int INL = KS_LAYOUT_BSF,
+          int OUTL = KS_LAYOUT_BSF>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     const __grid_constant__ CUtensorMap kmap_lo, float* __restrict__ Y,
                     const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles,
                     int dbg) {
-    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER>;
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL>;
+    static_assert(INL == KS_LAYOUT_BSF || !GATHER, "BSL input needs no gather");
     constexpr int S = C::S;
     constexpr int P = C::P;
     constexpr int RB = C::RB;
@@ -517,7 +535,9 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 const int p = (int)(gx % P);
                 if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
                 mbar_expect_tx(sfull0 + 8 * p, C::STG);
-                if constexpr (GATHER)
+                if constexpr (INL == KS_LAYOUT_BSL)
+                    tma_3d(stg0 + p * C::STG, &xmap, tc.n0, tc.j0, tc.i * c + l0, sfull0 + 8 * p);
+                else if constexpr (GATHER)
                     tma_3d(stg0 + p * C::STG, &xmap, tc.j0, tc.i * c + l0, tc.n0, sfull0 + 8 * p);
                 else
                     tma_2d(stg0 + p * C::STG, &xmap, (tc.i * c + l0) * d, tc.n0, sfull0 + 8 * p);
@@ -551,6 +571,9 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             if (dbg & 2) {                // profiling experiment: skip the staging reads
 #pragma unroll
                 for (int q = 0; q < 4 * NV; ++q) v[q] = 0.f;
+            } else if constexpr (INL == KS_LAYOUT_BSL) {   // staged [l][j][n]: column r
+#pragma unroll
+                for (int q = 0; q < BKJ * J; ++q) v[q] = lds32(stg0 + p * C::STG + (uint32_t)(q * BM + r) * 4);
             } else {
 #pragma unroll
                 for (int q = 0; q < NV; ++q)
@@ -652,9 +675,20 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
                         for (int jj = 0; jj < J; ++jj) v[jj][e] += __ldg(bias + r0 + (int64_t)e * d + jj);
                 }
-                if (!(dbg & 1))                   // profiling experiment: skip the stores
+                if constexpr (OUTL == KS_LAYOUT_BSL) {    // Y^T row r0 + e d + jj: lanes = 32 batch rows
+                    const int64_t n = (int64_t)tc.n0 + lq * 32 + lane;
+                    if (n < B && !(dbg & 1)) {
+#pragma unroll
+                        for (int e = 0; e < EC; ++e)
+#pragma unroll
+                            for (int jj = 0; jj < J; ++jj) __stcs(Y + (r0 + (int64_t)e * d + jj) * B + n, v[jj][e]);
+                    }
+                } else if ((dbg & 4) && (J == d || J % 4 == 0)) {   // experiment: direct stores
+                    direct_store_rows<J, EC>(v, Y, (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                } else if (!(dbg & 1)) {          // profiling experiment: skip the stores
                     warp_store_rows<float, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, J, EC>::BYTES, v, Y,
                                                   (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                }
             }
         }
     }
@@ -977,9 +1011,9 @@ int pick_bn(int64_t b) {
     return 0;
 }
 
-template <int LAYOUT, int BN, typename T = float, bool X3 = false>
+template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT>
 cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
-    using C = Tf32Cfg<LAYOUT, BN, X3>;
+    using C = Tf32Cfg<LAYOUT, BN, X3, OUTL>;
     constexpr cuuint32_t BK = C::RB / sizeof(T);
     constexpr cuuint64_t ES = sizeof(T);
     constexpr CUtensorMapSwizzle SW = C::RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
@@ -1004,7 +1038,7 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t xb[2] = {BK, BM};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, SW, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3>;
+    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3, OUTL>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1066,22 +1100,45 @@ BsfjPlan pick_bsfj(const ks_handle_s& h, uint32_t knobs) {
     return p;
 }
 
+// BSL in / BSF out, d > 1 (mixed-layout calls): every j's X rows are 512-byte
+// runs whatever J is, so J only sets the output run length (J = d: whole
+// contiguous row segments); BN as in pick_bsfj.
+BsfjPlan pick_bslj(const ks_handle_s& h, uint32_t knobs) {
+    BsfjPlan p;
+    if (h.c % 16 != 0 || h.d < 2) return p;
+    if (h.d <= 8 && h.d != 5 && h.d != 7) p.J = (int)h.d;
+    else if (h.d % 8 == 0) p.J = 8;
+    else if (h.d % 4 == 0) p.J = 4;
+    else return p;
+    if ((knobs & KS_KNOB_BN256) && p.J == 2 && h.b > 128 && h.b % 256 == 0) {
+        p.BN = 256;
+        return p;
+    }
+    for (int bn : {128, 96, 64, 48, 32, 16})
+        if (h.b % bn == 0 && p.J * bn <= 512) {
+            p.BN = bn;
+            break;
+        }
+    if (p.BN == 0) p.J = 0;
+    return p;
+}
+
 // l per stage: 16 (SWIZZLE_64B rows, half the padding / barrier traffic per
 // byte) when 2 operand slots and >= 64 KB of X staging fit, else 8 (SWIZZLE_32B).
-template <int J, int BN, bool X3, bool GATHER>
+template <int J, int BN, bool X3, bool GATHER, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 constexpr int bsfj_bkj() {
     constexpr int NA = X3 ? 2 : 1;
     constexpr int slot16 = J * NA * (BM + BN) * 64;
-    constexpr int stg16 = BM * (GATHER ? 17 * J * 4 : 16 * J * 4 + 16);
-    constexpr int scr = 4 * WarpStore<float, J, (J > 2 ? 8 : 16)>::BYTES;
+    constexpr int stg16 = BM * (INL == KS_LAYOUT_BSL ? 16 * J * 4 : GATHER ? 17 * J * 4 : 16 * J * 4 + 16);
+    constexpr int scr = OUTL == KS_LAYOUT_BSL ? 0 : 4 * WarpStore<float, J, (J > 2 ? 8 : 16)>::BYTES;
     constexpr int p16 = stg16 >= 32 * 1024 ? 2 : (64 * 1024 + stg16 - 1) / stg16;
     return 214 * 1024 - p16 * stg16 - scr >= 2 * slot16 ? 16 : 8;
 }
 
-template <int J, int BN, bool X3, bool GATHER>
+template <int J, int BN, bool X3, bool GATHER, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
-    constexpr int BKJ = bsfj_bkj<J, BN, X3, GATHER>();
-    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER>;
+    constexpr int BKJ = bsfj_bkj<J, BN, X3, GATHER, INL, OUTL>();
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL>;
     constexpr CUtensorMapSwizzle SW = C::RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUtensorMap xmap, kmap, kmap_lo;
     {
@@ -1092,7 +1149,12 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
         kmap_lo = kmap;
         if (X3 && !encode(&kmap_lo, h.k_lo, 2, kd, ks, kb, SW)) return cudaErrorInvalidValue;
     }
-    if (GATHER) {
+    if (INL == KS_LAYOUT_BSL) {
+        const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
+        const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
+        const cuuint32_t xb[3] = {BM, (cuuint32_t)J, (cuuint32_t)BKJ};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    } else if (GATHER) {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
         const cuuint32_t xb[3] = {(cuuint32_t)J, (cuuint32_t)BKJ + 1, BM};
@@ -1103,7 +1165,7 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t xb[2] = {(cuuint32_t)(BKJ * J + 4), BM};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER>;
+    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER, INL, OUTL>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1121,42 +1183,46 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
-template <int J, bool X3, bool GATHER>
+template <int J, bool X3, bool GATHER, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 cudaError_t launch_bsfj_bn(const ks_handle_s& h, const KsCall& call, int BN) {
     switch (BN) {
-        case 256: if constexpr (J == 2 && !X3 && !GATHER) return launch_bsfj<J, 256, X3, GATHER>(h, call); break;
-        case 128: if constexpr (J * 128 <= 512) return launch_bsfj<J, 128, X3, GATHER>(h, call); break;
-        case 96: if constexpr (J * 96 <= 512) return launch_bsfj<J, 96, X3, GATHER>(h, call); break;
-        case 64: return launch_bsfj<J, 64, X3, GATHER>(h, call);
-        case 48: return launch_bsfj<J, 48, X3, GATHER>(h, call);
-        case 32: return launch_bsfj<J, 32, X3, GATHER>(h, call);
-        case 16: return launch_bsfj<J, 16, X3, GATHER>(h, call);
+        case 256: if constexpr (J == 2 && !X3 && !GATHER) return launch_bsfj<J, 256, X3, GATHER, INL, OUTL>(h, call); break;
+        case 128: if constexpr (J * 128 <= 512) return launch_bsfj<J, 128, X3, GATHER, INL, OUTL>(h, call); break;
+        case 96: if constexpr (J * 96 <= 512) return launch_bsfj<J, 96, X3, GATHER, INL, OUTL>(h, call); break;
+        case 64: return launch_bsfj<J, 64, X3, GATHER, INL, OUTL>(h, call);
+        case 48: return launch_bsfj<J, 48, X3, GATHER, INL, OUTL>(h, call);
+        case 32: return launch_bsfj<J, 32, X3, GATHER, INL, OUTL>(h, call);
+        case 16: return launch_bsfj<J, 16, X3, GATHER, INL, OUTL>(h, call);
     }
     return cudaErrorInvalidValue;
 }
 
-template <bool X3>
+// INL / OUTL: BSF / BSF (X3 or TF32), BSF / BSL or BSL / BSF (TF32 mixed-layout calls)
+template <bool X3, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
-    const BsfjPlan p = pick_bsfj(h, call.knobs);
-    if (p.gather) {
-        if (p.J == 4) return launch_bsfj_bn<4, X3, true>(h, call, p.BN);
-        if constexpr (!X3)
-            if (p.J == 8) return launch_bsfj_bn<8, X3, true>(h, call, p.BN);
-        return cudaErrorInvalidValue;
+    const BsfjPlan p = INL == KS_LAYOUT_BSL ? pick_bslj(h, call.knobs) : pick_bsfj(h, call.knobs);
+    if constexpr (INL == KS_LAYOUT_BSF) {
+        if (p.gather) {
+            if (p.J == 4) return launch_bsfj_bn<4, X3, true, INL, OUTL>(h, call, p.BN);
+            if constexpr (!X3)
+                if (p.J == 8) return launch_bsfj_bn<8, X3, true, INL, OUTL>(h, call, p.BN);
+            return cudaErrorInvalidValue;
+        }
     }
     switch (p.J) {
-        case 2: return launch_bsfj_bn<2, X3, false>(h, call, p.BN);
-        case 3: return launch_bsfj_bn<3, X3, false>(h, call, p.BN);
-        case 4: return launch_bsfj_bn<4, X3, false>(h, call, p.BN);
+        case 2: return launch_bsfj_bn<2, X3, false, INL, OUTL>(h, call, p.BN);
+        case 3: return launch_bsfj_bn<3, X3, false, INL, OUTL>(h, call, p.BN);
+        case 4: return launch_bsfj_bn<4, X3, false, INL, OUTL>(h, call, p.BN);
     }
     if constexpr (!X3) {
-        if (p.J == 6) return launch_bsfj_bn<6, X3, false>(h, call, p.BN);
-        if (p.J == 8) return launch_bsfj_bn<8, X3, false>(h, call, p.BN);
+        if (p.J == 6) return launch_bsfj_bn<6, X3, false, INL, OUTL>(h, call, p.BN);
+        if (p.J == 8) return launch_bsfj_bn<8, X3, false, INL, OUTL>(h, call, p.BN);
     }
     return cudaErrorInvalidValue;
 }
 
 bool bsfj_ok(const ks_handle_s& h, uint32_t knobs) { return pick_bsfj(h, knobs).J != 0; }
+
 
 // Half BSF, d > 1: J j-values per tile (see ks_half_bsfj_kernel), 0 = unsupported.
 // d % 4 == 0 but not 8 (d = 12, 20, ...): J = 4 from an 8-wide box.
@@ -1251,17 +1317,17 @@ cudaError_t launch_halfj_any(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
-template <int LAYOUT, typename T = float, bool X3 = false>
+template <int LAYOUT, typename T = float, bool X3 = false, int OUTL = LAYOUT>
 cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn(h.b)) {
-        case 128: return launch_bn<LAYOUT, 128, T, X3>(h, call);
-        case 112: return launch_bn<LAYOUT, 112, T, X3>(h, call);
-        case 96: return launch_bn<LAYOUT, 96, T, X3>(h, call);
-        case 80: return launch_bn<LAYOUT, 80, T, X3>(h, call);
-        case 64: return launch_bn<LAYOUT, 64, T, X3>(h, call);
-        case 48: return launch_bn<LAYOUT, 48, T, X3>(h, call);
-        case 32: return launch_bn<LAYOUT, 32, T, X3>(h, call);
-        case 16: return launch_bn<LAYOUT, 16, T, X3>(h, call);
+        case 128: return launch_bn<LAYOUT, 128, T, X3, OUTL>(h, call);
+        case 112: return launch_bn<LAYOUT, 112, T, X3, OUTL>(h, call);
+        case 96: return launch_bn<LAYOUT, 96, T, X3, OUTL>(h, call);
+        case 80: return launch_bn<LAYOUT, 80, T, X3, OUTL>(h, call);
+        case 64: return launch_bn<LAYOUT, 64, T, X3, OUTL>(h, call);
+        case 48: return launch_bn<LAYOUT, 48, T, X3, OUTL>(h, call);
+        case 32: return launch_bn<LAYOUT, 32, T, X3, OUTL>(h, call);
+        case 16: return launch_bn<LAYOUT, 16, T, X3, OUTL>(h, call);
     }
     return cudaErrorInvalidValue;
 }
@@ -1280,6 +1346,7 @@ cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
 // exist, unless KS_TF32_DENSIFY=0 (experiments).
 bool dense_ok(const ks_handle_s& h, const KsCall& call) {
     if (!h.k_dense || call.layout != KS_LAYOUT_BSF || h.math != KS_MATH_TF32 || h.d < 2) return false;
+    if (call.mixed() && !(call.knobs & KS_KNOB_DENSIFY)) return false;   // BSL out: the J kernel's stores are whole lines
     if (pick_bn(h.b * h.d) == 0 || h.N % 4 != 0 || h.M % 4 != 0) return false;
     if (call.knobs & KS_KNOB_DENSIFY) return true;
     static const bool never = [] {
@@ -1295,6 +1362,7 @@ cudaError_t launch_dense(const ks_handle_s& h, const KsCall& call) {
     hd.c = h.c * h.d;
     hd.d = 1;
     hd.k_tf32 = h.k_dense;
+    if (call.mixed()) return launch_layout<KS_LAYOUT_BSF, float, false, KS_LAYOUT_BSL>(hd, call);
     return launch_layout<KS_LAYOUT_BSF>(hd, call);
 }
 
@@ -1309,6 +1377,13 @@ bool tf32_supports(const ks_handle_s& h, const KsCall& call) {
     if (call.B >= (int64_t(1) << 31)) return false;
     const uintptr_t xa = reinterpret_cast<uintptr_t>(call.X), ya = reinterpret_cast<uintptr_t>(call.Y);
     if (xa & 15) return false;                                   // TMA global address
+    if (call.mixed()) {            // TF32 only: BSF in / BSL out, or BSL in / BSF out
+        if (h.math != KS_MATH_TF32) return false;
+        if (call.layout == KS_LAYOUT_BSF)
+            return (ya & 3) == 0 && (h.d == 1 || bsfj_ok(h, call.knobs) || dense_ok(h, call));
+        if (call.B % 4 != 0 || (ya & 15)) return false;
+        return h.d == 1 || pick_bslj(h, call.knobs).J != 0;
+    }
     if (call.layout == KS_LAYOUT_BSL) return call.B % 4 == 0 && (ya & 3) == 0;
     if (ya & 15) return false;
     // BSF: d = 1 direct; d > 1 J-column gather (pick_bsfj; bias read as scalars)
@@ -1323,6 +1398,15 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
         if (h.d == 1) return launch_layout<KS_LAYOUT_BSF, float, true>(h, call);
         return launch_bsfj_any<true>(h, call);
     }
+    if (call.mixed()) {
+        if (call.layout == KS_LAYOUT_BSL) {
+            if (h.d == 1) return launch_layout<KS_LAYOUT_BSL, float, false, KS_LAYOUT_BSF>(h, call);
+            return launch_bsfj_any<false, KS_LAYOUT_BSL, KS_LAYOUT_BSF>(h, call);
+        }
+        if (dense_ok(h, call)) return launch_dense(h, call);
+        if (h.d == 1) return launch_layout<KS_LAYOUT_BSF, float, false, KS_LAYOUT_BSL>(h, call);
+        return launch_bsfj_any<false, KS_LAYOUT_BSF, KS_LAYOUT_BSL>(h, call);
+    }
     if (tf32v2_supports(h, call)) return tf32v2_launch(h, call);
     if (dense_ok(h, call)) return launch_dense(h, call);
     if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL>(h, call);
@@ -1334,6 +1418,7 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
 // kind::f16 (BF16 or FP16 operands, FP32 accumulation, output rounded to
 // nearest-even).  BSL any d; BSF d = 1.
 bool half_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (h.b < 16 || h.c < 16 || h.c % 16 != 0 || pick_bn(h.b) == 0) return false;
     if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31)) return false;
     if (call.B >= (int64_t(1) << 31)) return false;

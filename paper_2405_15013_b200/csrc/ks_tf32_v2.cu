@@ -457,6 +457,7 @@ namespace ks {
 // TF32 (not 3xTF32), FP32 handle, BSL any d or BSF d = 1, 16-byte aligned
 // X/Y with 16-byte row pitches (TMA), and a plan that fits shared memory.
 bool tf32v2_supports(const ks_handle_s& h, const KsCall& call) {
+    if (call.mixed()) return false;
     if (!(call.knobs & KS_KNOB_TF32_V2) || h.dtype != KS_DTYPE_F32 || h.math != KS_MATH_TF32) return false;
     if (h.b < 16 || h.c < 16 || h.c % 8 != 0 || h.b % 16 != 0) return false;
     if (h.a * h.d * h.b >= (int64_t(1) << 31) || h.a * h.c >= (int64_t(1) << 31) || call.B >= (int64_t(1) << 31))

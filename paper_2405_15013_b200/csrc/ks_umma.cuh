@@ -198,6 +198,38 @@ __device__ __forceinline__ void warp_store_rows(uint32_t scr, const float (&v)[J
     __syncwarp();
 }
 
+// Direct BSF store (no shared-memory staging): lane l holds row n0w + l, v[j][k]
+// is the output at element offset off0 + k*d + j.  When the J outputs of one k
+// are contiguous with the next k's (J == d) a lane stores 16-byte units of
+// consecutive outputs; else each run of J outputs (J % 4 == 0) in 16-byte units.
+// Each warp store instruction writes 32 rows x 16 bytes (half sectors that L2
+// merges) but costs no shared-memory bandwidth -- the scarce resource of the
+// TF32 kernels (tensor-core operand reads, TMA fills and transposes share it).
+template <int J, int KB>
+__device__ __forceinline__ void direct_store_rows(const float (&v)[J][KB], float* __restrict__ Y, int64_t n0w,
+                                                  int64_t B, int64_t ldy, int64_t off0, int d, int lane) {
+    const int64_t n = n0w + lane;
+    if (n >= B) return;
+    float* row = Y + n * ldy + off0;
+    if (J == d) {
+        static_assert((KB * J) % 4 == 0, "whole 16-byte units");
+#pragma unroll
+        for (int q = 0; q < KB * J / 4; ++q) {
+            float w[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) w[x] = v[(q * 4 + x) % J][(q * 4 + x) / J];
+            __stcs(reinterpret_cast<float4*>(row + q * 4), make_float4(w[0], w[1], w[2], w[3]));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < KB; ++k)
+#pragma unroll
+            for (int j4 = 0; j4 < J; j4 += 4)
+                __stcs(reinterpret_cast<float4*>(row + (int64_t)k * d + j4),
+                       make_float4(v[j4][k], v[j4 + 1][k], v[j4 + 2][k], v[j4 + 3][k]));
+    }
+}
+
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
     asm volatile(

@@ -46,7 +46,8 @@ EXPORTS = ["ks_pack_weights", "ks_pack_weights_ex", "ks_get_dtype", "ks_matmul_a
            "ks_last_error", "ks_last_error_message", "ks_status_string",
            "ks_kernel_launch_count", "ks_abi_version",
            "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free", "ks_peak_ffma",
-           "ks_set_knobs", "ks_plan_knobs", "ks_preset_count"]
+           "ks_set_knobs", "ks_plan_knobs", "ks_preset_count",
+           "ks_matmul_io", "ks_set_chain_mixed_layouts", "ks_chain_layouts"]
 
 
 class KSError(RuntimeError):
@@ -101,6 +102,12 @@ def load_library(path: str = LIB_PATH):
     lib.ks_set_chain_fusion.argtypes = [ctypes.c_int]
     lib.ks_set_chain_fusion.restype = st
     lib.ks_chain_fusion_eligible.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int]
+    lib.ks_matmul_io.argtypes = [vp, fp, ctypes.c_int, fp, ctypes.c_int, i64, vp]
+    lib.ks_matmul_io.restype = ctypes.c_int
+    lib.ks_set_chain_mixed_layouts.argtypes = [ctypes.c_int]
+    lib.ks_set_chain_mixed_layouts.restype = ctypes.c_int
+    lib.ks_chain_layouts.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    lib.ks_chain_layouts.restype = ctypes.c_int
     lib.ks_chain_fusion_eligible.restype = ctypes.c_int
     lib.ks_chain_host.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, i64, ctypes.c_int, vp]
     lib.ks_chain_host.restype = st
@@ -373,6 +380,45 @@ def set_chain_fusion(enable: bool):
 
 def chain_fusion_eligible(factors, B: int, layout="bsf") -> bool:
     return bool(load_library().ks_chain_fusion_eligible(_handles(factors), len(factors), int(B), _layout(layout)))
+
+
+def matmul_io(f: Factor, X, x_layout, Y=None, y_layout="bsf", stream=None, B: int | None = None):
+    """Y = X K^T with X in x_layout and Y in y_layout (ks_matmul_io; FP32 handles)."""
+    import torch
+    xl, yl = _layout(x_layout), _layout(y_layout)
+    if f.dtype != DTYPE_F32:
+        raise TypeError("matmul_io: FP32 handles only")
+    if B is None:
+        B = X.shape[0] if xl == BSF else X.shape[1]
+    if Y is None:
+        Y = torch.empty((B, f.M) if yl == BSF else (f.M, B), device=X.device, dtype=torch.float32)
+    if B < 0:
+        raise ValueError(f"B must be >= 0, got {B}")
+    for t, what, n, lay in ((X, "X", f.N, xl), (Y, "Y", f.M, yl)):
+        if t.dtype != torch.float32:
+            raise TypeError(f"{what} has dtype {t.dtype}, the factor computes in torch.float32")
+        exp = (B, n) if lay == BSF else (n, B)
+        if tuple(t.shape) != exp:
+            raise ValueError(f"{what} must have shape {exp} ({'BSF' if lay == BSF else 'BSL'}), got {tuple(t.shape)}")
+    if X.device != Y.device:
+        raise ValueError(f"X is on {X.device}, Y on {Y.device}")
+    _check(_lib.ks_matmul_io(f.handle, _dev_ptr(X, "X"), xl, _dev_ptr(Y, "Y"), yl, int(B), _stream_ptr(stream)))
+    return Y
+
+
+def set_chain_mixed_layouts(enable: bool):
+    """Process-wide mixed-layout intermediate policy (ks_set_chain_mixed_layouts); default on."""
+    _check(load_library().ks_set_chain_mixed_layouts(1 if enable else 0))
+
+
+def chain_layouts(factors, B: int, layout="bsf"):
+    """(mixed, [layout of the output of K_1 (= Y's) .. K_L, X's layout]) that ks_chain_ex would use."""
+    L = len(factors)
+    out = (ctypes.c_int * (L + 1))()
+    r = load_library().ks_chain_layouts(_handles(factors), L, int(B), _layout(layout), out)
+    if r < 0:
+        raise ValueError("invalid chain")
+    return bool(r), ["bsf" if v == BSF else "bsl" for v in out]
 
 
 def chain_host(factors, X_host, Y_host, layout="bsf", stream=None):

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r02v_smi.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r02v_pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r02v_pytest.log
+timeout 300 python __graft_entry__.py --smoke > gpurun_out/r02v_smoke.txt 2>&1; echo "smoke exit $?" >> gpurun_out/r02v_smoke.txt
+timeout 900 python bench.py > gpurun_out/r02v_bench.json 2> gpurun_out/r02v_bench.err; echo "bench exit $?" >> gpurun_out/r02v_bench.err
