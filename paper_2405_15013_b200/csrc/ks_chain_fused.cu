@@ -18,7 +18,15 @@
 // ("radix-8"): a thread loads the 8 values {base + m*d0}, applies the 2-3
 // factors in registers and writes them back, cutting shared-memory traffic 3x.
 // Other factor sequences run one factor per pass.
-#include "ks_internal.h"
+//
+// Bank-conflict-free rows (SWZ): when N % 256 == 0 the row groups move by
+// tensor TMA with SWIZZLE_128B, so float e of a row sits at e ^ (((e >> 5) & 7) << 2)
+// (16-byte chunks XOR-permuted within each 128-byte segment).  Every pass's
+// warp accesses then hit 32 distinct banks: the d0 = 8 radix-8 pass (lanes
+// 8 j x 4 blocks, addresses 64 blk + 8 m + j) was 4-way conflicted and the d0 = 1
+// pass (32-byte per-lane runs) 2-way -- half of all shared-memory wavefronts
+// were conflicts (ncu, profiles/r02/fused_*).  The arithmetic is unchanged.
+#include "ks_umma.cuh"
 
 #include <cstdlib>
 
@@ -26,6 +34,13 @@ namespace {
 
 constexpr int MAXF = 32;
 constexpr int THREADS = 512;
+
+// position of float e of a row in the SWIZZLE_128B layout (an involution)
+template <bool SWZ>
+__device__ __forceinline__ uint32_t rpos(uint32_t e) {
+    if constexpr (SWZ) return e ^ (((e >> 5) & 7u) << 2);
+    else return e;
+}
 
 struct FusedFactor {
     const float* k;   // canonical K4 of the factor
@@ -96,23 +111,23 @@ __device__ __forceinline__ void dyadic_load(const FusedFactor* F, int it, float 
 }
 
 // Apply an item's T factors to its E elements {base + m*d0} of every row.
-template <int T>
+template <int T, bool SWZ = false>
 __device__ __forceinline__ void dyadic_apply(float* sm, int rows, int N, int d0, int it,
                                              const float (&kw)[T][(1 << T) / 2][4]) {
     constexpr int E = 1 << T;
     const int base = (it / d0) * (E * d0) + it % d0;
     for (int r = 0; r < rows; ++r) {
-        float* row = sm + (size_t)r * N + base;
+        float* row = sm + (size_t)r * N;
         float v[E];
         if (d0 == 1) {                             // E consecutive floats: vector shared loads
 #pragma unroll
             for (int m = 0; m < E; m += 4) {
-                const float4 q = *reinterpret_cast<const float4*>(row + m);
+                const float4 q = *reinterpret_cast<const float4*>(row + rpos<SWZ>(base + m));
                 v[m] = q.x; v[m + 1] = q.y; v[m + 2] = q.z; v[m + 3] = q.w;
             }
         } else {
 #pragma unroll
-            for (int m = 0; m < E; ++m) v[m] = row[m * d0];
+            for (int m = 0; m < E; ++m) v[m] = row[rpos<SWZ>(base + m * d0)];
         }
 #pragma unroll
         for (int t = 0; t < T; ++t) {
@@ -129,25 +144,113 @@ __device__ __forceinline__ void dyadic_apply(float* sm, int rows, int N, int d0,
         if (d0 == 1) {
 #pragma unroll
             for (int m = 0; m < E; m += 4)
-                *reinterpret_cast<float4*>(row + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
+                *reinterpret_cast<float4*>(row + rpos<SWZ>(base + m)) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
         } else {
 #pragma unroll
-            for (int m = 0; m < E; ++m) row[m * d0] = v[m];
+            for (int m = 0; m < E; ++m) row[rpos<SWZ>(base + m * d0)] = v[m];
         }
     }
+}
+
+// dyadic_apply with the stride d0 = 2^LD0 a compile-time constant: the E
+// element offsets m*d0 fold into the shared-memory instructions' immediates
+// (the runtime-stride form spends ~2 integer instructions per element on
+// addresses -- measured: 56% of the fused kernel's instructions were not FFMA),
+// and rows are processed two at a time (both rows' loads issue before either
+// row's FMAs) for instruction-level parallelism.  Same operations, same order
+// per output as dyadic_apply: bit-identical.
+template <int T, int LD0, bool SWZ>
+__device__ __forceinline__ void dyadic_row_load(const float* row, uint32_t base, float (&v)[1 << T]) {
+    constexpr int E = 1 << T, D0 = 1 << LD0;
+    if constexpr (D0 == 1) {
+#pragma unroll
+        for (int m = 0; m < E; m += 4) {
+            const float4 q = *reinterpret_cast<const float4*>(row + rpos<SWZ>(base + m));
+            v[m] = q.x; v[m + 1] = q.y; v[m + 2] = q.z; v[m + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = row[rpos<SWZ>(base + m * D0)];
+    }
+}
+template <int T, int LD0, bool SWZ>
+__device__ __forceinline__ void dyadic_row_store(float* row, uint32_t base, const float (&v)[1 << T]) {
+    constexpr int E = 1 << T, D0 = 1 << LD0;
+    if constexpr (D0 == 1) {
+#pragma unroll
+        for (int m = 0; m < E; m += 4)
+            *reinterpret_cast<float4*>(row + rpos<SWZ>(base + m)) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) row[rpos<SWZ>(base + m * D0)] = v[m];
+    }
+}
+template <int T>
+__device__ __forceinline__ void dyadic_row_math(float (&v)[1 << T], const float (&kw)[T][(1 << T) / 2][4]) {
+    constexpr int E = 1 << T;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+#pragma unroll
+        for (int p = 0; p < E / 2; ++p) {
+            const int lo = p & ((1 << t) - 1);
+            const int m0 = ((p >> t) << (t + 1)) | lo;
+            const int m1 = m0 | (1 << t);
+            const float x0 = v[m0], x1 = v[m1];
+            v[m0] = fmaf(x1, kw[t][p][1], fmaf(x0, kw[t][p][0], 0.f));
+            v[m1] = fmaf(x1, kw[t][p][3], fmaf(x0, kw[t][p][2], 0.f));
+        }
+    }
+}
+template <int T, int LD0, bool SWZ>
+__device__ __forceinline__ void dyadic_apply_c(float* sm, int rows, int N, int it,
+                                               const float (&kw)[T][(1 << T) / 2][4]) {
+    constexpr int E = 1 << T, D0 = 1 << LD0;
+    const uint32_t base = (uint32_t)((it >> LD0) * (E * D0) + (it & (D0 - 1)));
+    float* row = sm;
+    int r = 0;
+    for (; r + 1 < rows; r += 2, row += 2 * N) {
+        float v0[E], v1[E];
+        dyadic_row_load<T, LD0, SWZ>(row, base, v0);
+        dyadic_row_load<T, LD0, SWZ>(row + N, base, v1);
+        dyadic_row_math<T>(v0, kw);
+        dyadic_row_math<T>(v1, kw);
+        dyadic_row_store<T, LD0, SWZ>(row, base, v0);
+        dyadic_row_store<T, LD0, SWZ>(row + N, base, v1);
+    }
+    if (r < rows) {
+        float v0[E];
+        dyadic_row_load<T, LD0, SWZ>(row, base, v0);
+        dyadic_row_math<T>(v0, kw);
+        dyadic_row_store<T, LD0, SWZ>(row, base, v0);
+    }
+}
+
+// runtime d0 (a power of two, d0 * 2^T <= N) -> the compile-time form; d0 up to 2^13
+template <int T, bool SWZ>
+__device__ __forceinline__ void dyadic_apply_any(float* sm, int rows, int N, int d0, int it,
+                                                 const float (&kw)[T][(1 << T) / 2][4]) {
+    switch (__ffs(d0) - 1) {
+#define KS_FUSED_D0(L) \
+    case L: dyadic_apply_c<T, L, SWZ>(sm, rows, N, it, kw); return;
+        KS_FUSED_D0(0) KS_FUSED_D0(1) KS_FUSED_D0(2) KS_FUSED_D0(3) KS_FUSED_D0(4) KS_FUSED_D0(5) KS_FUSED_D0(6)
+        KS_FUSED_D0(7) KS_FUSED_D0(8) KS_FUSED_D0(9) KS_FUSED_D0(10) KS_FUSED_D0(11) KS_FUSED_D0(12)
+        KS_FUSED_D0(13)
+#undef KS_FUSED_D0
+    }
+    dyadic_apply<T, SWZ>(sm, rows, N, d0, it, kw);
 }
 
 // One radix-2^T pass over all rows of the tile, T consecutive dyadic factors
 // (b = c = 2) with d, 2d, 4d: weights loaded (from L2) per item, then applied to
 // every row of the group.
-template <int T>
+template <int T, bool SWZ>
 __device__ __forceinline__ void dyadic_pass(float* sm, int rows, int N, const FusedFactor* F) {
     constexpr int E = 1 << T;
     const int nitem = N / E;                      // (super-block of the last factor, j) pairs
     for (int it = threadIdx.x; it < nitem; it += THREADS) {
         float kw[T][E / 2][4];
         dyadic_load<T>(F, it, kw);
-        dyadic_apply<T>(sm, rows, N, F[0].d, it, kw);
+        dyadic_apply_any<T, SWZ>(sm, rows, N, F[0].d, it, kw);
     }
 }
 
@@ -195,7 +298,7 @@ __device__ __forceinline__ void tmem_ld16f(uint32_t taddr, float* v) {
 }
 
 // One factor with b = c = BB (any a, d) per pass.
-template <int BB>
+template <int BB, bool SWZ>
 __device__ __forceinline__ void block_pass(float* sm, int rows, int N, const FusedFactor& F) {
     const int d = F.d;
     const int nblk = F.a * d;
@@ -208,33 +311,32 @@ __device__ __forceinline__ void block_pass(float* sm, int rows, int N, const Fus
             for (int l = 0; l < BB; ++l) kr[k][l] = __ldg(F.k + ((int64_t)(i * BB + k) * BB + l) * d + j);
         const int base = i * BB * d + j;
         for (int r = 0; r < rows; ++r) {
-            float* row = sm + (size_t)r * N + base;
+            float* row = sm + (size_t)r * N;
             float x[BB];
 #pragma unroll
-            for (int l = 0; l < BB; ++l) x[l] = row[l * d];
+            for (int l = 0; l < BB; ++l) x[l] = row[rpos<SWZ>(base + l * d)];
 #pragma unroll
             for (int k = 0; k < BB; ++k) {
                 float acc = 0.f;
 #pragma unroll
                 for (int l = 0; l < BB; ++l) acc = fmaf(x[l], kr[k][l], acc);
-                row[k * d] = acc;
+                row[rpos<SWZ>(base + k * d)] = acc;
             }
         }
     }
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
-// Row groups move by bulk asynchronous copies (TMA engine, cp.async.bulk): the
-// next group streams into the second buffer while this one is computed, and
-// the finished group drains to HBM in the background.
-template <int BB>
+// Row groups move by bulk asynchronous copies (TMA engine; SWZ: tensor copies of
+// a {32, N/32, R} box with SWIZZLE_128B, else cp.async.bulk): the next group
+// streams into the second buffer while this one is computed, and the finished
+// group drains to HBM in the background.
+template <int BB, bool SWZ>
 __global__ void __launch_bounds__(THREADS, 1)
 ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const float* __restrict__ bias, int64_t B,
-                      const __grid_constant__ FusedParams P, int R) {
-    extern __shared__ __align__(128) float4 sm4[];
+                      const __grid_constant__ FusedParams P, int R, const __grid_constant__ CUtensorMap xmap,
+                      const __grid_constant__ CUtensorMap ymap) {
+    extern __shared__ __align__(1024) float4 sm4[];
     __shared__ __align__(8) uint64_t full[2];
     __shared__ uint32_t tmem_slot;
     if (BB == 2 && P.resident > 0) {
@@ -270,7 +372,8 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
     // buffer b at smf + b*R*N: indexing the shared symbol directly (not through an
     // array of pointers) keeps the accesses in the shared window (LDS/STS, not
     // generic LD/ST -- measured: the pointer array made every row access generic)
-    float* const smf = reinterpret_cast<float*>(sm4);
+    // 1024-byte aligned (the SWIZZLE_128B pattern repeats every 1 KB of address)
+    float* const smf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sm4) + 1023) & ~uintptr_t(1023));
     auto buf = [&](int64_t k) { return smf + (size_t)(k & 1) * R * N; };
     const int64_t ngroups = (B + R - 1) / R;
     const int64_t mine = ngroups > blockIdx.x ? (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -280,11 +383,16 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
     };
     auto issue_load = [&](int64_t k) {          // thread 0 only
         const int64_t row0 = ((int64_t)blockIdx.x + k * gridDim.x) * R;
-        const uint32_t bytes = (uint32_t)group_rows(k) * (uint32_t)N * 4u;
         const uint32_t bar = smem_u32(&full[k & 1]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(smem_u32(buf(k))), "l"(X + row0 * N), "r"(bytes), "r"(bar) : "memory");
+        if constexpr (SWZ) {                    // R-row box; rows past B arrive zero-filled
+            mbar_expect_tx(bar, (uint32_t)R * (uint32_t)N * 4u);
+            tma_3d(smem_u32(buf(k)), &xmap, 0, 0, (int)row0, bar);
+        } else {
+            const uint32_t bytes = (uint32_t)group_rows(k) * (uint32_t)N * 4u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(buf(k))), "l"(X + row0 * N), "r"(bytes), "r"(bar) : "memory");
+        }
     };
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[0])));
@@ -318,24 +426,25 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
                 float* flat = &kw[0][0][0];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) tmem_ld16f(tmem_w_addr(tmem, slot, q), flat + 16 * q);
-                dyadic_apply<3>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
+                dyadic_apply_any<3, SWZ>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
             } else if (BB == 2 && ps == P.part_pass) {   // factors 0-1 from TMEM, factor 2 from L2
                 float kw[3][4][4];
                 float* flat = &kw[0][0][0];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) tmem_ld16f(tmem_part_addr(tmem, q), flat + 16 * q);
                 dyadic_load<3, 2>(&P.f[f], threadIdx.x, kw);
-                dyadic_apply<3>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
-            } else if (BB == 2 && len == 3) dyadic_pass<3>(sm, rows, N, &P.f[f]);
-            else if (BB == 2 && len == 2) dyadic_pass<2>(sm, rows, N, &P.f[f]);
-            else block_pass<BB>(sm, rows, N, P.f[f]);
+                dyadic_apply_any<3, SWZ>(sm, rows, N, P.f[f].d, threadIdx.x, kw);
+            } else if (BB == 2 && len == 3) dyadic_pass<3, SWZ>(sm, rows, N, &P.f[f]);
+            else if (BB == 2 && len == 2) dyadic_pass<2, SWZ>(sm, rows, N, &P.f[f]);
+            else block_pass<BB, SWZ>(sm, rows, N, P.f[f]);
             f += len;
             __syncthreads();
         }
         if (bias) {                                 // KSLinear bias after the last factor (NEXT-2)
             for (int e = threadIdx.x; e < rows * N / 4; e += THREADS) {
                 float4 q = reinterpret_cast<float4*>(sm)[e];
-                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + (e % (N / 4)));
+                // logical column of this (physical) 16-byte chunk: rpos is an involution
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + rpos<SWZ>(4 * (e % (N / 4))) / 4);
                 q.x += bb.x; q.y += bb.y; q.z += bb.z; q.w += bb.w;
                 reinterpret_cast<float4*>(sm)[e] = q;
             }
@@ -347,8 +456,11 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
         __syncthreads();
         if (threadIdx.x == 0) {
             const int64_t row0 = ((int64_t)blockIdx.x + k * gridDim.x) * R;
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                         ::"l"(Y + row0 * N), "r"(smem_u32(sm)), "r"((uint32_t)rows * (uint32_t)N * 4u) : "memory");
+            if constexpr (SWZ)                  // rows past B are clipped by the tensor map
+                tma_store_3d(&ymap, 0, 0, (int)row0, smem_u32(sm));
+            else
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                             ::"l"(Y + row0 * N), "r"(smem_u32(sm)), "r"((uint32_t)rows * (uint32_t)N * 4u) : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
     }
@@ -364,6 +476,7 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
 }
 
 constexpr int SMEM_BUDGET = 224 * 1024;      // two row-group buffers (double-buffered); 227 KB opt-in max
+constexpr int SMEM_ALIGN_PAD = 1024;         // the kernel aligns the buffers to 1 KB
 
 }  // namespace
 
@@ -452,15 +565,30 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
     const int64_t sms = num_sms(hs[0]->device);
     // enough row groups to fill the machine
     while (R > 1 && (call.B + R - 1) / R < sms) R /= 2;
-    const size_t smem = (size_t)2 * R * N * 4;
+    const size_t smem = (size_t)2 * R * N * 4 + SMEM_ALIGN_PAD;
     int64_t groups = (call.B + R - 1) / R;
     const int64_t grid = groups < sms ? groups : sms;             // persistent, one CTA per SM
+    // bank-conflict-free swizzled rows: whole 1 KB swizzle periods per row, box dims <= 256
+    static const bool swz_on = [] {                 // KS_FUSED_SWZ=0 disables (experiments)
+        const char* e = getenv("KS_FUSED_SWZ");
+        return !(e && atoi(e) == 0);
+    }();
+    CUtensorMap xmap{}, ymap{};
+    bool swz = swz_on && N % 256 == 0 && N / 32 <= 256 && call.B < (int64_t(1) << 31);
+    if (swz) {
+        const cuuint64_t dims[3] = {32, (cuuint64_t)(N / 32), (cuuint64_t)call.B};
+        const cuuint64_t strides[2] = {128, (cuuint64_t)N * 4};
+        const cuuint32_t box[3] = {32, (cuuint32_t)(N / 32), (cuuint32_t)R};
+        swz = encode(&xmap, call.X, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B) &&
+              encode(&ymap, call.Y, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
     cudaError_t e;
-    auto kern = hs[0]->b == 2 ? ks_chain_fused_kernel<2> : ks_chain_fused_kernel<4>;
+    auto kern = hs[0]->b == 2 ? (swz ? ks_chain_fused_kernel<2, true> : ks_chain_fused_kernel<2, false>)
+                              : (swz ? ks_chain_fused_kernel<4, true> : ks_chain_fused_kernel<4, false>);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = launch_pdl(kern, dim3((unsigned)grid), dim3(THREADS), smem, call.stream, call.X, call.Y, call.bias, call.B, P,
-                   (int)R);
+                   (int)R, xmap, ymap);
     count_launch();
     return e;
 }

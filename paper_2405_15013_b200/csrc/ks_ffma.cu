@@ -1,5 +1,5 @@
 // Register-tiled FP32 (CUDA-core FFMA) KS kernel for the GEMM-like patterns
-// (b a multiple of 24 or 32, c a multiple of 8): the paper's sweep
+// (b a multiple of 8 -- widest tiles for 24 / 32 multiples -- c a multiple of 8): the paper's sweep
 // (b = c in {48..128}), ViT-S/16 and GPT-2 KSLinear factors.
 //
 // Alg. 3, re-tiled for sm_100a: each CTA owns the output
@@ -331,6 +331,10 @@ bool pick_bn(int64_t b, int J, int* wpjn, int* tn) {
     if (b % 48 == 0)            { *wpjn = 2; *tn = 6; return true; }
     if (b % 32 == 0)            { *wpjn = 1; *tn = 8; return true; }
     if (b % 24 == 0)            { *wpjn = 1; *tn = 6; return true; }
+    // any other b % 8 == 0 (80, 112, 40, ...): narrower warp tiles instead of the
+    // one-thread-per-output generic kernel (VERDICT r1 "perf cliffs")
+    if (b % 16 == 0)            { *wpjn = 1; *tn = 4; return true; }
+    if (b % 8 == 0)             { *wpjn = 1; *tn = 2; return true; }
     return false;
 }
 
@@ -393,6 +397,8 @@ cudaError_t launch_j(const ks_handle_s& h, const KsCall& call) {
     KS_FFMA_CASE(2, 6)
     KS_FFMA_CASE(1, 8)
     KS_FFMA_CASE(1, 6)
+    KS_FFMA_CASE(1, 4)
+    KS_FFMA_CASE(1, 2)
 #undef KS_FFMA_CASE
     return cudaErrorInvalidValue;
 }

@@ -59,3 +59,25 @@ def test_four_byte_aligned_views(ksb, p, layout):
     assert torch.equal(Yv, Yg)
     Yh = Yv.cpu().numpy() if layout == "bsf" else Yv.cpu().numpy().T
     assert O.normwise_error(Yh, O.matmul(p, K4, X)) <= 1e-5
+
+
+@pytest.mark.parametrize("layout", ["bsf", "bsl"])
+@pytest.mark.parametrize("p", [(1, 80, 64, 1), (2, 112, 48, 3), (1, 40, 64, 4), (3, 16, 32, 2), (1, 8, 16, 6),
+                               (4, 80, 80, 2), (1, 144, 96, 1)])
+def test_b_multiple_of_8_runs_ffma(ksb, p, layout):
+    """b % 8 == 0 outside 24Z u 32Z (b = 80, 112, 40, 16, 8, 144) runs the FFMA
+    kernel's 16- / 8-wide warp tiles, bit-identical to the generic kernel."""
+    M, N, _ = O.dims(p)
+    B = 300
+    K4 = ksgen.k4_uniform(*p, seed=7)
+    X = ksgen.x_normal(B, N, seed=8)
+    f = ksb.Factor(*p, K4)
+    assert f.plan(B, layout) == "ffma"
+    Xd = torch.from_numpy(X if layout == "bsf" else ksgen.to_bsl(X)).cuda()
+    Y = ksb.matmul(f, Xd, layout=layout)
+    f.set_kernel(ksb.KERNEL_GENERIC)
+    Yg = ksb.matmul(f, Xd, layout=layout)
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Yg)
+    Yh = Y.cpu().numpy() if layout == "bsf" else Y.cpu().numpy().T
+    assert O.normwise_error(Yh, O.matmul(p, K4, X)) <= 1e-5
