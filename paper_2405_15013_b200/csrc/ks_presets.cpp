@@ -81,6 +81,7 @@ const EnvKnobs& env_knobs() {
         if ((v = env_switch("KS_FFMA_KB32")) >= 0) put(v != 0, KS_KNOB_KB32);
         if ((v = env_switch("KS_FFMA_WS")) >= 0) put(v != 0, KS_KNOB_FFMA_WS);
         if ((v = env_switch("KS_FFMA_WSG")) >= 0) put(v != 0, KS_KNOB_FFMA_WSG);
+        if ((v = env_switch("KS_TF32_MN")) >= 0) put(v != 0, KS_KNOB_TF32_MN);
         return r;
     }();
     return k;
@@ -99,6 +100,9 @@ uint32_t rule_knobs(const ks_handle_s& h, const KsCall& call) {
     // small blocks, measured 1.1-1.4x faster (profiles/r02/exp_tf32_densify.txt)
     if (h.a == 1 && (h.d == 2 || h.d == 3 || h.d == 6 || (h.d == 8 && h.b * h.c <= 48 * 48)))
         k |= KS_KNOB_DENSIFY;
+    // MN-major A for TF32 BSL inputs: 1.04-1.21x on every b = 48 sweep pattern, 0.89-1.0x
+    // on b >= 64 (profiles/r02/mn_time.jsonl); the preset table refines it per pattern
+    if (h.b <= 48) k |= KS_KNOB_TF32_MN;
     const EnvKnobs& e = env_knobs();
     return (k | e.set) & ~e.clear;
 }

@@ -43,7 +43,10 @@ constexpr int NTHREADS = 320;
 // and B tiles would not leave room for two CTAs per SM at 128.
 // OUTL: layout of Y (= LAYOUT except for the mixed-layout calls of ks_matmul_io
 // and chain intermediates: BSF in / BSL out, or BSL in / BSF out with d = 1).
-template <int LAYOUT, int BN, bool X3 = false, int OUTL = LAYOUT>
+// MNA (BSL, FP32 TF32 only): A is loaded MN-major by TMA straight into the
+// operand slot (4 boxes {32 n, 1 j, 32 l}, SWIZZLE_128B_ATOM_32B) and the MMA
+// reads it with an MN-major descriptor: no staging ring, no transposer warps.
+template <int LAYOUT, int BN, bool X3 = false, int OUTL = LAYOUT, bool MNA = false>
 struct Tf32Cfg {
     static constexpr int RB = X3 ? 64 : 128;
     static constexpr int A_TILE = BM * RB;                // 16 KB (8 KB for X3)
@@ -58,7 +61,7 @@ struct Tf32Cfg {
     // tiles in flight hide TMA latency better than a deeper ring.
     static constexpr int CTAS = BN <= 128 ? 2 : 1;                                // CTAs per SM
     static constexpr int BUDGET = CTAS == 2 ? 110 * 1024 : 200 * 1024;
-    static constexpr int P = LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 || X3 ? 3 : 2) : 3) : 0;   // staging
+    static constexpr int P = MNA ? 0 : LAYOUT == KS_LAYOUT_BSL ? (CTAS == 2 ? (BN <= 64 || X3 ? 3 : 2) : 3) : 0;   // staging
     // BSF: 4 epilogue warps x 32 rows x (4 + 1) 16-byte units of store scratch (WarpStore<float, 1, 16>)
     static constexpr int SCR = OUTL == KS_LAYOUT_BSL ? 0 : 4 * 32 * 5 * 16;
     static constexpr int S_FIT = (BUDGET - P * STG - SCR) / SLOT;
@@ -71,6 +74,7 @@ struct Tf32Cfg {
     static_assert(BN % 16 == 0 && BN <= 256, "UMMA N for M=128");
     static_assert(S >= 2, "pipeline too shallow");
     static_assert((3 * S + 4 + 2 * (P > 0 ? P : 1)) * 8 + 4 <= 256, "barrier area");
+    static_assert(!MNA || (LAYOUT == KS_LAYOUT_BSL && !X3), "MN-major A: BSL TF32");
 };
 
 template <int RB>
@@ -110,13 +114,14 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT>
-__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3, OUTL>::CTAS)
+template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT, bool MNA = false>
+__global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap kmap_lo, T* __restrict__ Y, const T* __restrict__ bias,
                int64_t B, int a, int b, int c, int d, int64_t ntiles, int dbg) {
-    using C = Tf32Cfg<LAYOUT, BN, X3, OUTL>;
+    using C = Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>;
     static_assert(LAYOUT != KS_LAYOUT_BSL || sizeof(T) == 4, "half BSL runs the swap-AB kernel (ks_half_bsl.cu)");
+    constexpr bool STAGED = LAYOUT == KS_LAYOUT_BSL && !MNA;    // X through the staging ring + transposers
     static_assert(!X3 || sizeof(T) == 4, "3xTF32 is an FP32 mode");
     constexpr int RB = C::RB;
     constexpr int BKC = RB / (int)sizeof(T);         // K elements per stage (one operand row)
@@ -156,7 +161,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, LAYOUT == KS_LAYOUT_BSL ? 1 + NTRANS : 2);
+            mbar_init(full0 + 8 * s, STAGED ? 1 + NTRANS : 2);
             mbar_init(empty0 + 8 * s, 1);
             mbar_init(xfull0 + 8 * s, NTRANS);
         }
@@ -197,10 +202,10 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 mbar_expect_tx(sfull0 + 8 * p, C::STG);
                 tma_3d(stg0 + p * C::STG, &xmap, tc.n0, tc.j, tc.i * c + l0, sfull0 + 8 * p);
             };
-            if (LAYOUT == KS_LAYOUT_BSL)
+            if (STAGED)
                 for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
             for (int64_t g = 0; g < G; ++g) {
-                if (LAYOUT == KS_LAYOUT_BSL && g + P - 1 < G) issue_x(g + P - 1);
+                if (STAGED && g + P - 1 < G) issue_x(g + P - 1);
                 const TileCoord tc = decode(blockIdx.x + (g / nk) * gridDim.x, nkc, nnb, d, BN);
                 const int l0 = (int)(g % nk) * BKC;
                 const int st = (int)(g % S);
@@ -209,6 +214,11 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 if (LAYOUT != KS_LAYOUT_BSL) {
                     mbar_expect_tx(full0 + 8 * st, C::A_TILE);
                     tma_2d(sa, &xmap, tc.i * c + l0, tc.n0, full0 + 8 * st);
+                } else if constexpr (MNA) {   // MN-major A: 4 boxes of 32 batch columns x 32 l
+                    mbar_expect_tx(full0 + 8 * st, C::A_TILE);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        tma_3d(sa + q4 * 4096, &xmap, tc.n0 + 32 * q4, tc.j, tc.i * c + l0, full0 + 8 * st);
                 }
                 mbar_expect_tx(full0 + 8 * st, C::B_BYTES);
                 tma_2d(sa + C::A_BYTES, &kmap, l0, tc.q * b + tc.k0, full0 + 8 * st);
@@ -219,7 +229,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         const int r = tid - 32;                                    // batch row in the tile
         const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
         const int sw = RB == 128 ? (r % 8) : (r % 8) / 2;          // SW128 / SW64 chunk XOR
-        if constexpr (LAYOUT == KS_LAYOUT_BSL) {
+        if constexpr (STAGED) {
             // ---------------- BSL transposers: staging [l][n] -> K-major A (and x_lo for X3) ----------------
             for (int64_t g = 0; g < G; ++g) {
                 const int p = (int)(g % P);
@@ -281,7 +291,7 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     } else if (warp == 5) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc_t<T>(BN);
+            constexpr uint32_t idesc = make_idesc_t<T>(BN) | (MNA ? 1u << 15 : 0u);   // bit 15: A MN-major
             int64_t g = 0;
             int64_t it = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -305,6 +315,9 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                             mma_tf32(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + C::B_TILE + 32 * s),
                                      idesc, 1u);
                             mma_tf32(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + 32 * s), idesc, 1u);
+                        } else if constexpr (MNA) {   // k-step s = rows 8s.. of each 32-l box; boxes 4 KB apart
+                            mma_tf32(dtm, mn_sw128_32b_desc(sa + 1024 * s, 4096, 512), kmajor_desc<RB>(sb + 32 * s),
+                                     idesc, acc);
                         } else if constexpr (sizeof(T) == 4) {
                             mma_tf32(dtm, kmajor_desc<RB>(sa + 32 * s), kmajor_desc<RB>(sb + 32 * s), idesc, acc);
                         } else {
@@ -1011,9 +1024,9 @@ int pick_bn(int64_t b) {
     return 0;
 }
 
-template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT>
+template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT, bool MNA = false>
 cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
-    using C = Tf32Cfg<LAYOUT, BN, X3, OUTL>;
+    using C = Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>;
     constexpr cuuint32_t BK = C::RB / sizeof(T);
     constexpr cuuint64_t ES = sizeof(T);
     constexpr CUtensorMapSwizzle SW = C::RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
@@ -1030,15 +1043,20 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     if (LAYOUT == KS_LAYOUT_BSL) {
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
         const cuuint64_t xs[2] = {(cuuint64_t)call.B * ES, (cuuint64_t)(h.d * call.B) * ES};
-        const cuuint32_t xb[3] = {BM, 1, BK};
-        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
+        if constexpr (MNA) {
+            const cuuint32_t xb[3] = {32, 1, 32};
+            if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, dt)) return cudaErrorInvalidValue;
+        } else {
+            const cuuint32_t xb[3] = {BM, 1, BK};
+            if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE, dt)) return cudaErrorInvalidValue;
+        }
     } else {
         const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
         const cuuint64_t xs[1] = {(cuuint64_t)h.N * ES};
         const cuuint32_t xb[2] = {BK, BM};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, SW, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3, OUTL>;
+    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3, OUTL, MNA>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1317,17 +1335,17 @@ cudaError_t launch_halfj_any(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
-template <int LAYOUT, typename T = float, bool X3 = false, int OUTL = LAYOUT>
+template <int LAYOUT, typename T = float, bool X3 = false, int OUTL = LAYOUT, bool MNA = false>
 cudaError_t launch_layout(const ks_handle_s& h, const KsCall& call) {
     switch (pick_bn(h.b)) {
-        case 128: return launch_bn<LAYOUT, 128, T, X3, OUTL>(h, call);
-        case 112: return launch_bn<LAYOUT, 112, T, X3, OUTL>(h, call);
-        case 96: return launch_bn<LAYOUT, 96, T, X3, OUTL>(h, call);
-        case 80: return launch_bn<LAYOUT, 80, T, X3, OUTL>(h, call);
-        case 64: return launch_bn<LAYOUT, 64, T, X3, OUTL>(h, call);
-        case 48: return launch_bn<LAYOUT, 48, T, X3, OUTL>(h, call);
-        case 32: return launch_bn<LAYOUT, 32, T, X3, OUTL>(h, call);
-        case 16: return launch_bn<LAYOUT, 16, T, X3, OUTL>(h, call);
+        case 128: return launch_bn<LAYOUT, 128, T, X3, OUTL, MNA>(h, call);
+        case 112: return launch_bn<LAYOUT, 112, T, X3, OUTL, MNA>(h, call);
+        case 96: return launch_bn<LAYOUT, 96, T, X3, OUTL, MNA>(h, call);
+        case 80: return launch_bn<LAYOUT, 80, T, X3, OUTL, MNA>(h, call);
+        case 64: return launch_bn<LAYOUT, 64, T, X3, OUTL, MNA>(h, call);
+        case 48: return launch_bn<LAYOUT, 48, T, X3, OUTL, MNA>(h, call);
+        case 32: return launch_bn<LAYOUT, 32, T, X3, OUTL, MNA>(h, call);
+        case 16: return launch_bn<LAYOUT, 16, T, X3, OUTL, MNA>(h, call);
     }
     return cudaErrorInvalidValue;
 }
@@ -1400,6 +1418,8 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
     }
     if (call.mixed()) {
         if (call.layout == KS_LAYOUT_BSL) {
+            if (h.d == 1 && (call.knobs & KS_KNOB_TF32_MN))
+                return launch_layout<KS_LAYOUT_BSL, float, false, KS_LAYOUT_BSF, true>(h, call);
             if (h.d == 1) return launch_layout<KS_LAYOUT_BSL, float, false, KS_LAYOUT_BSF>(h, call);
             return launch_bsfj_any<false, KS_LAYOUT_BSL, KS_LAYOUT_BSF>(h, call);
         }
@@ -1409,6 +1429,8 @@ cudaError_t tf32_launch(const ks_handle_s& h, const KsCall& call) {
     }
     if (tf32v2_supports(h, call)) return tf32v2_launch(h, call);
     if (dense_ok(h, call)) return launch_dense(h, call);
+    if (call.layout == KS_LAYOUT_BSL && (call.knobs & KS_KNOB_TF32_MN))
+        return launch_layout<KS_LAYOUT_BSL, float, false, KS_LAYOUT_BSL, true>(h, call);
     if (call.layout == KS_LAYOUT_BSL) return launch_layout<KS_LAYOUT_BSL>(h, call);
     if (h.d == 1) return launch_layout<KS_LAYOUT_BSF>(h, call);
     return launch_bsfj_any<false>(h, call);

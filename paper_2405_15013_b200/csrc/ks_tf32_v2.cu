@@ -42,15 +42,6 @@ constexpr int V2_STAGE = V2_BM * 128;            // 16 KB: 128 rows x 32 l x 4 B
 constexpr int V2_SMEM_MAX = 227 * 1024;
 constexpr int V2_KT_MAX = 112 * 1024;            // largest resident weight tile
 
-__device__ __forceinline__ uint64_t mn_sw128_32b_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)(lbo >> 4) << 16;             // LBO: next 32-n group
-    d |= (uint64_t)(sbo >> 4) << 32;             // SBO: next group of 4 l rows
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)1 << 61;                      // SWIZZLE_128B_BASE32B
-    return d;
-}
 
 struct V2Tile {
     int i, j, k0, n0;

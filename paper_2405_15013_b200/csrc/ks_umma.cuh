@@ -99,6 +99,19 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
     return d;
 }
 
+// UMMA descriptor of an MN-major TF32 operand in the SW128_32B canonical layout
+// (layout type 1; what TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes): 32-byte
+// chunks XOR-swizzled in 128-byte rows; measured on B200 (scripts/probe_umma_mn.cu).
+__device__ __forceinline__ uint64_t mn_sw128_32b_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)(lbo >> 4) << 16;             // LBO: next 32-n group
+    d |= (uint64_t)(sbo >> 4) << 32;             // SBO: next group of 4 l rows
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;                      // SWIZZLE_128B_BASE32B
+    return d;
+}
+
 // Instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128.
 __host__ __device__ constexpr uint32_t make_idesc(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);

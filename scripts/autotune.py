@@ -30,6 +30,7 @@ ap.add_argument("--out", required=True)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--margin", type=float, default=0.03)
 ap.add_argument("--limit", type=int, default=0)
+ap.add_argument("--only", default="", help="restrict to math:layout pairs, e.g. tf32:bsl")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -62,6 +63,8 @@ def candidates(p, layout, math, rules):
     if math == "tf32":
         if layout == "bsl" or d == 1:
             out |= {rules | ks.KNOB_TF32_V2, rules | ks.KNOB_TF32_V2 | ks.KNOB_V2_NKB2}
+            if layout == "bsl":           # the v1 kernel with / without MN-major A
+                out |= {(rules & ~ks.KNOB_TF32_V2) ^ ks.KNOB_TF32_MN, rules & ~ks.KNOB_TF32_V2 & ~ks.KNOB_TF32_MN}
         else:
             opts = [0]
             if 2 <= d <= 8:
@@ -96,6 +99,8 @@ for p, B in work:
                 continue
             f.set_math(ksb.MATH_TF32)
         for layout in ("bsf", "bsl"):
+            if args.only and f"{math}:{layout}" not in args.only.split(","):
+                continue
             X = Xb if layout == "bsf" else Xb.t().contiguous()
             Y = torch.empty((B, M) if layout == "bsf" else (M, B), device=dev)
             f.set_knobs(-1)
