@@ -202,11 +202,12 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
         }
     };
 
-    float acc[TM][TN];
+    static_assert(TN % 2 == 0, "FFMA2 pairs of outputs");
+    uint64_t acc2[TM][TN / 2];                    // (acc[m][2p], acc[m][2p+1]) packed for FFMA2
 #pragma unroll
     for (int m = 0; m < TM; ++m)
 #pragma unroll
-        for (int n = 0; n < TN; ++n) acc[m][n] = 0.f;
+        for (int p = 0; p < TN / 2; ++p) acc2[m][p] = 0;
 
     load_tile(0);
     store_tile(0);
@@ -238,13 +239,22 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
 #pragma unroll
             for (int m = 0; m < TM; ++m)
 #pragma unroll
-                for (int n = 0; n < TN; ++n) acc[m][n] = fmaf(av[m], bv[n], acc[m][n]);
+                for (int p = 0; p < TN / 2; ++p)
+                    acc2[m][p] = ffma2(f2pack(av[m], av[m]), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
         }
         if (t + 1 < nk) store_tile((t + 1) & 1);
         __syncthreads();
     }
 
     // ---- epilogue: each owned Y element written exactly once ------------------
+    float acc[TM][TN];
+#pragma unroll
+    for (int m = 0; m < TM; ++m)
+#pragma unroll
+        for (int p = 0; p < TN / 2; ++p) {
+            acc[m][2 * p] = f2lo(acc2[m][p]);
+            acc[m][2 * p + 1] = f2hi(acc2[m][p]);
+        }
     const int j = j0 + wj;
     if (bias) {                                   // KSLinear bias (NEXT-2), per output row r
 #pragma unroll

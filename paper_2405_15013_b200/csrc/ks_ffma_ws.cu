@@ -129,11 +129,12 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
         int64_t n0;
         decode(tile, q, k0, n0);
         const int i = q / d, j = q % d;
-        float acc[8][TN];
+        static_assert(TN % 2 == 0, "FFMA2 pairs of outputs");
+        uint64_t acc2[8][TN / 2];                 // (acc[m][2p], acc[m][2p+1]) packed for FFMA2
 #pragma unroll
         for (int m = 0; m < 8; ++m)
 #pragma unroll
-            for (int e = 0; e < TN; ++e) acc[m][e] = 0.f;
+            for (int p = 0; p < TN / 2; ++p) acc2[m][p] = 0;
 
         for (int t = 0; t < nk; ++t, ++g) {
             const int st = (int)(g % S);
@@ -165,7 +166,8 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
 #pragma unroll
                     for (int m = 0; m < 8; ++m)
 #pragma unroll
-                        for (int e = 0; e < TN; ++e) acc[m][e] = fmaf(av[m], bv[e], acc[m][e]);
+                        for (int p = 0; p < TN / 2; ++p)
+                            acc2[m][p] = ffma2(f2pack(av[m], av[m]), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
                 }
             } else {
                 // A[n][l] (64-byte rows, SWIZZLE_64B: 16-byte chunk u of row n at u ^ ((n >> 1) & 3)):
@@ -201,7 +203,8 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                         for (int m = 0; m < 8; ++m) {
                             const float x = e4 == 0 ? av[m].x : e4 == 1 ? av[m].y : e4 == 2 ? av[m].z : av[m].w;
 #pragma unroll
-                            for (int e = 0; e < TN; ++e) acc[m][e] = fmaf(x, bv[e], acc[m][e]);
+                            for (int p = 0; p < TN / 2; ++p)
+                                acc2[m][p] = ffma2(f2pack(x, x), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
                         }
                     }
                 }
@@ -222,6 +225,14 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
         }
 
         // ---- epilogue: each owned Y element written exactly once ----------------
+        float acc[8][TN];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int p = 0; p < TN / 2; ++p) {
+                acc[m][2 * p] = f2lo(acc2[m][p]);
+                acc[m][2 * p + 1] = f2hi(acc2[m][p]);
+            }
         if (bias) {                               // KSLinear bias (NEXT-2)
 #pragma unroll
             for (int e = 0; e < TN; ++e) {
@@ -365,12 +376,17 @@ ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         int64_t n0;
         decode(tile, i, j0, k0, n0);
         float acc[4][4][TK];                              // [row r][j][output e]
+        constexpr int TK2 = TK % 2 == 0 ? TK / 2 : 1;     // FFMA2 pairs of outputs (TK even)
+        uint64_t acc2[4][4][TK2];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
+            for (int jj = 0; jj < 4; ++jj) {
 #pragma unroll
                 for (int e = 0; e < TK; ++e) acc[r][jj][e] = 0.f;
+#pragma unroll
+                for (int p = 0; p < TK2; ++p) acc2[r][jj][p] = 0;
+            }
         for (int t = 0; t < nk; ++t, ++g) {
             const int st = (int)(g % S);
             mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
@@ -403,9 +419,17 @@ ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                 for (int r = 0; r < 4; ++r) {
                     const float x[4] = {av[r].x, av[r].y, av[r].z, av[r].w};
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
+                    for (int jj = 0; jj < 4; ++jj) {
+                        if constexpr (TK % 2 == 0) {
 #pragma unroll
-                        for (int e = 0; e < TK; ++e) acc[r][jj][e] = fmaf(x[jj], bv[jj][e], acc[r][jj][e]);
+                            for (int p = 0; p < TK2; ++p)
+                                acc2[r][jj][p] = ffma2(f2pack(x[jj], x[jj]), f2pack(bv[jj][2 * p], bv[jj][2 * p + 1]),
+                                                       acc2[r][jj][p]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < TK; ++e) acc[r][jj][e] = fmaf(x[jj], bv[jj][e], acc[r][jj][e]);
+                        }
+                    }
                 }
             }
             fence_proxy_async();
@@ -421,6 +445,17 @@ ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
             }
         }
         // epilogue: the 4 j of one (row, output k) are one 16-byte run of Y
+        if constexpr (TK % 2 == 0) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                    for (int p = 0; p < TK2; ++p) {
+                        acc[r][jj][2 * p] = f2lo(acc2[r][jj][p]);
+                        acc[r][jj][2 * p + 1] = f2hi(acc2[r][jj][p]);
+                    }
+        }
         const int64_t rbase = (int64_t)i * b * d + (int64_t)(k0 + colB) * d + j0;
         if (bias) {
 #pragma unroll
@@ -586,12 +621,17 @@ ks_ffma_wsc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         int64_t n0;
         decode(tile, i, k0, n0);
         float acc[R][D][TK];
+        constexpr int TK2 = TK % 2 == 0 ? TK / 2 : 1;     // FFMA2 pairs of outputs (TK even)
+        uint64_t acc2[R][D][TK2];
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int jj = 0; jj < D; ++jj)
+            for (int jj = 0; jj < D; ++jj) {
 #pragma unroll
                 for (int e = 0; e < TK; ++e) acc[r][jj][e] = 0.f;
+#pragma unroll
+                for (int p = 0; p < TK2; ++p) acc2[r][jj][p] = 0;
+            }
         for (int t = 0; t < nk; ++t, ++g) {
             const int st = (int)(g % S);
             mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
@@ -628,10 +668,19 @@ ks_ffma_wsc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
 #pragma unroll
                     for (int h = 0; h < 4; ++h)
 #pragma unroll
-                        for (int jj = 0; jj < D; ++jj)
+                        for (int jj = 0; jj < D; ++jj) {
+                            if constexpr (TK % 2 == 0) {
+                                const float xv = x[h * D + jj];
 #pragma unroll
-                            for (int e = 0; e < TK; ++e)
-                                acc[r][jj][e] = fmaf(x[h * D + jj], bv[h][jj][e], acc[r][jj][e]);
+                                for (int p = 0; p < TK2; ++p)
+                                    acc2[r][jj][p] = ffma2(f2pack(xv, xv), f2pack(bv[h][jj][2 * p], bv[h][jj][2 * p + 1]),
+                                                           acc2[r][jj][p]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < TK; ++e)
+                                    acc[r][jj][e] = fmaf(x[h * D + jj], bv[h][jj][e], acc[r][jj][e]);
+                            }
+                        }
                 }
             }
             fence_proxy_async();
@@ -647,6 +696,17 @@ ks_ffma_wsc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
             }
         }
         // epilogue: outputs (k, j), k in [k0+colB, +TK), j < D, are D TK consecutive floats
+        if constexpr (TK % 2 == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int jj = 0; jj < D; ++jj)
+#pragma unroll
+                    for (int p = 0; p < TK2; ++p) {
+                        acc[r][jj][2 * p] = f2lo(acc2[r][jj][p]);
+                        acc[r][jj][2 * p + 1] = f2hi(acc2[r][jj][p]);
+                    }
+        }
         const int64_t rbase = (int64_t)i * b * D + (int64_t)(k0 + colB) * D;
         if (bias) {
 #pragma unroll

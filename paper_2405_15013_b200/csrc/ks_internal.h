@@ -134,6 +134,24 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }  // namespace ks
 
 #ifdef __CUDACC__
+// Packed FP32 pairs for FFMA2 (fma.rn.f32x2, sm_100a): two independent
+// correctly rounded FMAs per instruction -- each lane is exactly fmaf, so FFMA2
+// kernels stay bit-identical to the FFMA ones (measured: 0 mismatches in 1.3e8,
+// scripts/probe_ffma2.cu) at the same 74 TF/s peak, with half the issue slots.
+// A scalar broadcast operand (f2pack(x, x)) folds into FFMA2's .F32 operand form.
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 #endif
