@@ -153,7 +153,8 @@ typedef enum {
     KS_KNOB_KB32 = 1 << 5,       /* FFMA TMA ring: 32 l per chunk for b = 96 tiles          */
     KS_KNOB_FFMA_WS = 1 << 6,    /* FFMA: warp-specialised TMA-fed kernels                 */
     KS_KNOB_FFMA_WSG = 1 << 7,   /* FFMA BSF d>1: four-j / all-j TMA kernels               */
-    KS_KNOB_TF32_MN = 1 << 8     /* TF32 BSL in: A MN-major by TMA (no transposer warps)   */
+    KS_KNOB_TF32_MN = 1 << 8,    /* TF32 BSL in: A MN-major by TMA (no transposer warps)   */
+    KS_KNOB_FFMA_WSL = 1 << 9    /* FFMA BSF d%4==0: one j per lane, FFMA2 (else four-j)   */
 } ks_knob_t;
 
 /* Force the knobs of every call on this handle (autotuning, A/B tests): a

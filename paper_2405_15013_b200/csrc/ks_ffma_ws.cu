@@ -514,6 +514,215 @@ cudaError_t launch_wsg(const ks_handle_s& h, const KsCall& call) {
     return e;
 }
 
+// ---- BSF, d % 4 == 0, FFMA2: four j per tile, one j per LANE ---------------------
+// Same staging as the four-j kernel (one TMA box {4 j, 17 l, 64 n} per chunk of 16 l,
+// the K^T tiles of the 4 j), but the 4 lanes of a quad (tx = lane & 3) own j = tx:
+// a thread's micro-tile is 8 rows (ty + 8m) x 8 outputs of ONE j, so per l it reads
+// 8 scalars of A (rows x its j: the 32 lanes hit 32 distinct banks, row pitch 68
+// words) and 2 float4 of its j's K^T row, then 32 FFMA2 -- twice
+// the reuse of the four-j kernel, whose 4 rows x 4 j x TK micro-tile needed 8 float4
+// loads per 64 FMA (2 bytes of shared memory per FMA: at most half the FFMA rate).
+// Warps split the outputs: warp w owns k = 8w .. 8w+7 of the tile (BN = 8 NW).  The
+// epilogue transposes each 4 x 4 (k, j) block across the quad with shuffles, so a
+// lane writes the 4 j of one (row, k) as one float4 (d = 4: 64 contiguous bytes per
+// quad).  The K^T tiles of the 4 j arrive interleaved by ONE 4-D TMA box
+// {8 k, 4 j, BN/8 k-groups, 16 l} of k_tile: B[l][k-group][j][8 k], so the 4
+// distinct addresses a warp reads per l (one per j) are 32 bytes apart and fall on
+// 4 bank groups.  One FP32 FMA chain per output, l ascending: bit-identical.
+constexpr int WSL_BM = 64;
+
+template <int NW>
+struct WslCfg {
+    static constexpr int BN = 8 * NW;
+    static constexpr int THREADS = 32 * NW;
+    static constexpr int PITCH = (WS_BK + 1) * 16;         // staged row: 17 l x 4 j floats
+    static constexpr int A_BYTES = WSL_BM * PITCH;          // 17 KB
+    static constexpr int B_BYTES = 4 * WS_BK * BN * 4;      // [16 l][BN/8][4 j][8 k]
+    static constexpr int SLOT0 = A_BYTES + B_BYTES;
+    static constexpr int SLOT = (SLOT0 + 1023) / 1024 * 1024;
+    static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
+    static constexpr int BAR_OFF = S * SLOT;
+    static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;
+    static_assert(NW == 6 || NW == 8, "BN in {48, 64}");
+    static_assert(S >= 3, "ring depth");
+};
+
+template <int NW>
+__global__ void __launch_bounds__(WslCfg<NW>::THREADS, 2)
+ks_ffma_wsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                   float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                   int64_t ntiles) {
+    using C = WslCfg<NW>;
+    constexpr int S = C::S;
+    constexpr int BN = C::BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t slot0 = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    const uint32_t full0 = smem_u32(&bars[0]);
+    const uint32_t cnt0 = smem_u32(&bars[8]);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nkc = b / BN;
+    const int njg = d / 4;
+    const int64_t nnb = (B + WSL_BM - 1) / WSL_BM;
+    const int nk = c / WS_BK;
+    const int64_t M = (int64_t)a * b * d;
+
+    auto decode = [&](int64_t tile, int& i, int& j0, int& k0, int64_t& n0) {
+        k0 = (int)(tile % nkc) * BN;
+        tile /= nkc;
+        j0 = (int)(tile % njg) * 4;
+        tile /= njg;
+        n0 = (tile % nnb) * WSL_BM;
+        i = (int)(tile / nnb);
+    };
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t G = my_tiles * nk;
+    auto issue = [&](int64_t gx) {
+        int i, j0, k0;
+        int64_t n0;
+        decode(blockIdx.x + (gx / nk) * gridDim.x, i, j0, k0, n0);
+        const int st = (int)(gx % S);
+        const int l0 = (int)(gx % nk) * WS_BK;
+        const uint32_t sa = slot0 + st * C::SLOT;
+        mbar_expect_tx(full0 + 8 * st, C::A_BYTES + C::B_BYTES);
+        tma_3d(sa, &xmap, j0, i * c + l0, (int)n0, full0 + 8 * st);
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+            ::"r"(sa + C::A_BYTES), "l"(&kmap), "r"(0), "r"(i * d + j0), "r"(k0 / 8), "r"(l0), "r"(full0 + 8 * st)
+            : "memory");
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            asm volatile("st.shared.u32 [%0], 0;" ::"r"(cnt0 + 4 * s) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_launch_dependents();
+    if (tid == 0)
+        for (int64_t gx = 0; gx < S && gx < G; ++gx) issue(gx);
+
+    const int ty = lane >> 2, tx = lane & 3;             // rows ty + 8m, j = j0 + tx
+    const int colB = warp * 8;                           // outputs k0 + colB .. + 7
+    int64_t g = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int i, j0, k0;
+        int64_t n0;
+        decode(tile, i, j0, k0, n0);
+        uint64_t acc2[8][4];                             // (acc[m][2p], acc[m][2p+1])
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) acc2[m][p] = 0;
+        for (int t = 0; t < nk; ++t, ++g) {
+            const int st = (int)(g % S);
+            mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+            const uint32_t sa = slot0 + st * C::SLOT;
+            const uint32_t pa = sa + ty * C::PITCH + tx * 4;                       // row ty, j = tx
+            const uint32_t pb = sa + C::A_BYTES + (warp * 4 + tx) * 32;            // B[l][warp][tx][8]
+#pragma unroll
+            for (int l = 0; l < WS_BK; ++l) {
+                float x[8], bv[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) x[m] = lds32(pa + m * 8 * C::PITCH + l * 16);
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(bv[0]), "=f"(bv[1]), "=f"(bv[2]), "=f"(bv[3]) : "r"(pb + l * BN * 16));
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(bv[4]), "=f"(bv[5]), "=f"(bv[6]), "=f"(bv[7]) : "r"(pb + l * BN * 16 + 16));
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        acc2[m][p] = ffma2(f2pack(x[m], x[m]), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                uint32_t old;
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(cnt0 + 4 * st)
+                             : "memory");
+                if (old == NW - 1) {
+                    asm volatile("st.shared.u32 [%0], 0;" ::"r"(cnt0 + 4 * st) : "memory");
+                    if (g + S < G) issue(g + S);
+                }
+            }
+        }
+        // epilogue: per row m and half h, the quad holds a 4 (k) x 4 (j) block, lane tx
+        // with j = tx; after the exchange lane tx holds k = colB + 4h + tx, j = j0 .. j0+3
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int64_t n = n0 + ty + 8 * m;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float blk[4] = {f2lo(acc2[m][2 * h]), f2hi(acc2[m][2 * h]), f2lo(acc2[m][2 * h + 1]),
+                                      f2hi(acc2[m][2 * h + 1])};
+                float out[4];
+#pragma unroll
+                for (int sx = 0; sx < 4; ++sx) {           // exchange with the lane tx ^ sx
+                    const int want = tx ^ sx;              // the partner's k offset = my j slot
+                    const float send = want == 0 ? blk[0] : want == 1 ? blk[1] : want == 2 ? blk[2] : blk[3];
+                    const float got = __shfl_xor_sync(0xffffffffu, send, sx);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (jj == (tx ^ sx)) out[jj] = got;
+                }
+                const int64_t r = (int64_t)i * b * d + (int64_t)(k0 + colB + 4 * h + tx) * d + j0;
+                if (bias) {
+                    const float4 bq = __ldg(reinterpret_cast<const float4*>(bias + r));
+                    out[0] += bq.x; out[1] += bq.y; out[2] += bq.z; out[3] += bq.w;
+                }
+                if (n < B) __stcs(reinterpret_cast<float4*>(Y + n * M + r), make_float4(out[0], out[1], out[2], out[3]));
+            }
+        }
+    }
+}
+
+template <int NW>
+cudaError_t launch_wsl(const ks_handle_s& h, const KsCall& call) {
+    using C = WslCfg<NW>;
+    constexpr int BN = C::BN;
+    CUtensorMap xmap, kmap;
+    {
+        const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
+        const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
+        const cuuint32_t xb[3] = {4, WS_BK + 1, WSL_BM};
+        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    {   // k_tile[(q c + l) b + k] as 4-D {8 k, a d q, b/8 k-groups, c l}: box {8, 4, BN/8, 16}
+        const cuuint64_t kd[4] = {8, (cuuint64_t)(h.a * h.d), (cuuint64_t)(h.b / 8), (cuuint64_t)h.c};
+        const cuuint64_t ks[3] = {(cuuint64_t)(h.c * h.b) * 4, 32, (cuuint64_t)h.b * 4};
+        const cuuint32_t kb[4] = {8, 4, BN / 8, WS_BK};
+        if (!encode(&kmap, h.k_tile, 4, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_ffma_wsl_kernel<NW>;
+    static bool attr[64] = {false};
+    if (!attr[h.device & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr[h.device & 63] = true;
+    }
+    const int64_t ntiles = (h.b / BN) * (h.d / 4) * ((call.B + WSL_BM - 1) / WSL_BM) * h.a;
+    int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
+    if (max_grid() > 0) slots = max_grid();
+    const int64_t grid = ntiles < slots ? ntiles : slots;
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(C::THREADS), C::SMEM, call.stream, xmap,
+                                         kmap, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
+                                         ntiles);
+    ks::count_launch();
+    return e;
+}
+
+// warps along the outputs for the lane-j kernel: BN = 64 (8 warps) or 48 (6); 0 = unsupported
+int pick_nw_wsl(int64_t b) { return b % 64 == 0 ? 8 : b % 48 == 0 ? 6 : 0; }
+
 // TK (outputs per thread per j) for the 4-j kernel: the widest of 4, 3, 2 with
 // 16 TK dividing b; 0 = unsupported.
 int pick_tk_wsg(int64_t b) {
@@ -883,6 +1092,8 @@ cudaError_t ffma_ws_launch(const ks_handle_s& h, const KsCall& call) {
     if (h.d == 2) return launch_wsc_tk<2>(h, call);        // all d j per thread
     if (h.d == 3) return launch_wsc_tk<3>(h, call);
     if (h.d > 1) {
+        if ((call.knobs & KS_KNOB_FFMA_WSL) && pick_nw_wsl(h.b) != 0)
+            return pick_nw_wsl(h.b) == 8 ? launch_wsl<8>(h, call) : launch_wsl<6>(h, call);
         switch (pick_tk_wsg(h.b)) {
             case 4: return launch_wsg<4>(h, call);
             case 3: return launch_wsg<3>(h, call);

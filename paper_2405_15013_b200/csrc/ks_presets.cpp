@@ -82,6 +82,7 @@ const EnvKnobs& env_knobs() {
         if ((v = env_switch("KS_FFMA_WS")) >= 0) put(v != 0, KS_KNOB_FFMA_WS);
         if ((v = env_switch("KS_FFMA_WSG")) >= 0) put(v != 0, KS_KNOB_FFMA_WSG);
         if ((v = env_switch("KS_TF32_MN")) >= 0) put(v != 0, KS_KNOB_TF32_MN);
+        if ((v = env_switch("KS_FFMA_WSL")) >= 0) put(v != 0, KS_KNOB_FFMA_WSL);
         return r;
     }();
     return k;

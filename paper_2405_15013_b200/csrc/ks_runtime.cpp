@@ -522,7 +522,7 @@ ks_status_t ks_plan(ks_handle_t h, int64_t B, ks_layout_t layout, ks_kernel_t* o
 
 ks_status_t ks_set_knobs(ks_handle_t h, int64_t knobs) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
-    if (knobs < -1 || knobs > 0x1FF) return fail(KS_ERR_INVALID_ARG, "knobs must be -1 or a mask of KS_KNOB_* bits");
+    if (knobs < -1 || knobs > 0x3FF) return fail(KS_ERR_INVALID_ARG, "knobs must be -1 or a mask of KS_KNOB_* bits");
     h->knobs_override = knobs;
     return ok();
 }

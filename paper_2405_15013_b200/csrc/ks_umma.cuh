@@ -325,7 +325,7 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
             CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     auto fn = encode_fn();
     if (!fn) return false;
-    cuuint32_t es[3] = {1, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims,
                     strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -22,9 +22,9 @@ KERNEL_SPLITC = 6
 KERNEL_NAMES = {0: "auto", 1: "generic", 2: "stream", 3: "ffma", 4: "tf32", 5: "fused_chain", 6: "splitc"}
 # launch-plan knobs (ks_knob_t, include/ks.h)
 KNOB_TF32_V2, KNOB_V2_NKB2, KNOB_DENSIFY, KNOB_J8, KNOB_BN256, KNOB_KB32, KNOB_FFMA_WS, KNOB_FFMA_WSG, \
-    KNOB_TF32_MN = (1 << i for i in range(9))
+    KNOB_TF32_MN, KNOB_FFMA_WSL = (1 << i for i in range(10))
 KNOB_NAMES = {1: "tf32_v2", 2: "v2_nkb2", 4: "densify", 8: "j8", 16: "bn256", 32: "kb32", 64: "ffma_ws",
-              128: "ffma_wsg", 256: "tf32_mn"}
+              128: "ffma_wsg", 256: "tf32_mn", 512: "ffma_wsl"}
 
 
 def preset_count() -> int:

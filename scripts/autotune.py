@@ -76,10 +76,12 @@ def candidates(p, layout, math, rules):
             base = rules & ~(ks.KNOB_DENSIFY | ks.KNOB_J8 | ks.KNOB_BN256)
             out |= {base | m for m in opts}
     else:
-        base = rules & ~(ks.KNOB_KB32 | ks.KNOB_FFMA_WS | ks.KNOB_FFMA_WSG)
+        base = rules & ~(ks.KNOB_KB32 | ks.KNOB_FFMA_WS | ks.KNOB_FFMA_WSG | ks.KNOB_FFMA_WSL)
         opts = [ks.KNOB_FFMA_WS | ks.KNOB_FFMA_WSG | ks.KNOB_KB32, ks.KNOB_FFMA_WS | ks.KNOB_FFMA_WSG, 0]
         if layout == "bsf" and d > 1:
             opts.append(ks.KNOB_FFMA_WS | ks.KNOB_KB32)
+        if layout == "bsf" and d % 4 == 0:      # the lane-j FFMA2 kernel instead of the four-j one
+            opts.append(ks.KNOB_FFMA_WS | ks.KNOB_FFMA_WSG | ks.KNOB_KB32 | ks.KNOB_FFMA_WSL)
         out |= {base | m for m in opts}
     return sorted(out)
 

@@ -9,7 +9,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 INC = os.path.join(ROOT, "paper_2405_15013_b200", "csrc", "ks_presets.inc")
 # the table is generated from these records; later ones replace earlier rows with the same key
-JSNS = [os.path.join(ROOT, "profiles", "r02", n) for n in ("autotune.json", "autotune_tf32_bsl.json")]
+JSNS = [os.path.join(ROOT, "profiles", "r02", n) for n in ("autotune.json", "autotune_tf32_bsl.json", "autotune_fp32_bsf.json")]
 
 
 def _rows():
