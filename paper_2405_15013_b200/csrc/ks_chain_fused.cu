@@ -209,11 +209,32 @@ __device__ __forceinline__ void dyadic_apply_c(float* sm, int rows, int N, int i
     float* row = sm;
     int r = 0;
     for (; r + 1 < rows; r += 2, row += 2 * N) {
+        // two rows at once with FFMA2: lane 0 = row r, lane 1 = row r+1, the weight a
+        // broadcast scalar -- per lane exactly dyadic_row_math's fmaf chain (bit-identical)
         float v0[E], v1[E];
         dyadic_row_load<T, LD0, SWZ>(row, base, v0);
         dyadic_row_load<T, LD0, SWZ>(row + N, base, v1);
-        dyadic_row_math<T>(v0, kw);
-        dyadic_row_math<T>(v1, kw);
+        uint64_t v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = f2pack(v0[m], v1[m]);
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+#pragma unroll
+            for (int p = 0; p < E / 2; ++p) {
+                const int lo = p & ((1 << t) - 1);
+                const int m0 = ((p >> t) << (t + 1)) | lo;
+                const int m1 = m0 | (1 << t);
+                const uint64_t x0 = v[m0], x1 = v[m1];
+                const float* k = kw[t][p];
+                v[m0] = ffma2(x1, f2pack(k[1], k[1]), ffma2(x0, f2pack(k[0], k[0]), 0));
+                v[m1] = ffma2(x1, f2pack(k[3], k[3]), ffma2(x0, f2pack(k[2], k[2]), 0));
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            v0[m] = f2lo(v[m]);
+            v1[m] = f2hi(v[m]);
+        }
         dyadic_row_store<T, LD0, SWZ>(row, base, v0);
         dyadic_row_store<T, LD0, SWZ>(row + N, base, v1);
     }

@@ -175,3 +175,21 @@ def test_chain_layouts_uniform_cases(ksb):
     fs = [f.set_math(ksb.MATH_TF32) for f in fs]
     assert ksb.chain_layouts(fs, 256, "bsl") == (False, ["bsl"] * 3)   # caller chose BSL
     assert ksb.chain_layouts(fs, 258)[0] is False                      # BSL in needs B % 4 == 0
+
+
+def test_chain_graph_replays_mixed_plan_bit_identical(ksb):
+    """ks_chain_graph captures the mixed-layout plan (BSL intermediate) and its
+    replay equals the direct chain bit for bit."""
+    pats = MODEL_CHAINS["gpt2_up"]
+    K4s = [ksgen.k4_uniform(*q, seed=400 + l) for l, q in enumerate(pats)]
+    fs = [ksb.Factor(*q, k).set_math(ksb.MATH_TF32) for q, k in zip(pats, K4s)]
+    B = 512
+    X = to_dev(ksgen.x_normal(B, O.dims(pats[-1])[1], seed=9))
+    assert ksb.chain_layouts(fs, B)[0]
+    Y = ksb.chain(fs, X)
+    Yg = torch.empty_like(Y)
+    g = ksb.ChainGraph(fs, X, Yg)
+    g.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(Yg, Y)
+    g.free()
