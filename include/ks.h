@@ -67,6 +67,12 @@ typedef enum { KS_MATH_FP32 = 0, KS_MATH_TF32 = 1, KS_MATH_F32X3 = 2 } ks_math_t
  * FP32 accumulation.                                                         */
 typedef enum { KS_DTYPE_F32 = 0, KS_DTYPE_BF16 = 1, KS_DTYPE_F16 = 2 } ks_dtype_t;
 
+/* Epilogue activation of ks_matmul_act / ks_chain_act (the
+ * "+ GELU" of the FFN row): applied in FP32 to each output after
+ * the bias, in the epilogue of the last factor applied (K_1).  GELU is the exact
+ * form 0.5 y (1 + erf(y / sqrt 2)) (erff).                                   */
+typedef enum { KS_ACT_NONE = 0, KS_ACT_GELU = 1 } ks_activation_t;
+
 /* Kernel families; KS_KERNEL_AUTO lets the plan table choose (default).    */
 typedef enum {
     KS_KERNEL_AUTO = 0,
@@ -214,6 +220,18 @@ ks_status_t ks_matmul_any(ks_handle_t h, const void* X, void* Y, const void* bia
                           ks_layout_t layout, ks_stream_t stream);
 ks_status_t ks_chain_any(const ks_handle_t* handles, int L, const void* X, void* Y,
                          const void* bias, int64_t B, ks_layout_t layout, ks_stream_t stream);
+
+/* Same as ks_matmul_any / ks_chain_any with an epilogue activation applied to
+ * every output after the bias (NEXT-2; FFN "2 x Linear + GELU"):
+ * Y = act(X K^T + bias), for a chain act(X K_L^T ... K_1^T + bias), fused into
+ * the epilogue of the last factor applied (K_1) in every kernel family (and of
+ * the fused chain kernel).  act: KS_ACT_NONE or KS_ACT_GELU (exact erf form,
+ * FP32 erff), else KS_ERR_INVALID_ARG.  Half handles: applied in FP32 before
+ * the output is rounded.                                                     */
+ks_status_t ks_matmul_act(ks_handle_t h, const void* X, void* Y, const void* bias, ks_activation_t act,
+                          int64_t B, ks_layout_t layout, ks_stream_t stream);
+ks_status_t ks_chain_act(const ks_handle_t* handles, int L, const void* X, void* Y, const void* bias,
+                         ks_activation_t act, int64_t B, ks_layout_t layout, ks_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Chain fusion policy (process-wide, default on).  When on, ks_chain /

@@ -382,6 +382,17 @@ def model_flops(p, B: int) -> int:
     return 2 * B * dims(p)[2]
 
 
+def gelu(Y) -> np.ndarray:
+    """GELU, the FFN activation of the paper's ViT-S/16 layer table (Table 7
+    "2 x Linear + GELU + LN"; NEXT-2's optional epilogue): the exact form
+    gelu(y) = y * Phi(y) = 0.5 * y * (1 + erf(y / sqrt 2)), FP64 (math.erf per
+    element; the paper does not define it, R18)."""
+    import math
+    y = np.asarray(Y, dtype=np.float64)
+    erf = np.vectorize(math.erf, otypes=[np.float64])
+    return 0.5 * y * (1.0 + erf(y / math.sqrt(2.0)))
+
+
 def normwise_error(Y_hat, Y_ref) -> float:
     """max |Y_hat - Y| / max |Y| over the tensor (§8c-10 reading of the
     north-star 'max relative error').  |.| is the modulus, so complex inputs

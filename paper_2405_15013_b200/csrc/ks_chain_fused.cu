@@ -56,6 +56,7 @@ struct FusedParams {
     int resident;          // number of radix-8 passes whose weights live in TMEM (0..2)
     int res_pass[2];       // which passes (the TMEM slot is the index in this list)
     int part_pass;         // a third pass whose first two factors live in the last 128 columns, or -1
+    int act;               // epilogue activation after the bias (ks_activation_t, NEXT-2)
 };
 
 // Weights of one radix-2^T item (T consecutive dyadic factors, b = c = 2, with
@@ -461,12 +462,18 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
             f += len;
             __syncthreads();
         }
-        if (bias) {                                 // KSLinear bias after the last factor (NEXT-2)
+        if (bias || P.act) {                        // KSLinear bias / activation after the last factor (NEXT-2)
             for (int e = threadIdx.x; e < rows * N / 4; e += THREADS) {
                 float4 q = reinterpret_cast<float4*>(sm)[e];
-                // logical column of this (physical) 16-byte chunk: rpos is an involution
-                const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + rpos<SWZ>(4 * (e % (N / 4))) / 4);
-                q.x += bb.x; q.y += bb.y; q.z += bb.z; q.w += bb.w;
+                if (bias) {
+                    // logical column of this (physical) 16-byte chunk: rpos is an involution
+                    const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + rpos<SWZ>(4 * (e % (N / 4))) / 4);
+                    q.x += bb.x; q.y += bb.y; q.z += bb.z; q.w += bb.w;
+                }
+                if (P.act) {
+                    q.x = ks_act(q.x, P.act); q.y = ks_act(q.y, P.act);
+                    q.z = ks_act(q.z, P.act); q.w = ks_act(q.w, P.act);
+                }
                 reinterpret_cast<float4*>(sm)[e] = q;
             }
             __syncthreads();
@@ -532,6 +539,7 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
     FusedParams P{};
     const int64_t N = hs[0]->N;
     P.N = (int)N;
+    P.act = call.act;
     // application order: K_L first (handles[L-1])
     for (int t = 0; t < L; ++t) {
         const ks_handle_s& h = *hs[L - 1 - t];

@@ -73,7 +73,7 @@ struct Cfg {
 template <int LAYOUT, int J, int WPJM, int WPJN, int TN, int KBK, bool SC = false>
 __global__ void __launch_bounds__(Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>::THREADS, KS_FFMA_MINB)
 ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float* __restrict__ Y,
-               const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
+               const float* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d) {
     static_assert(!SC || J == 1, "scalar path: one j per CTA");
     using C = Cfg<LAYOUT, J, WPJM, WPJN, TN, KBK>;
     constexpr int BK = C::BK;
@@ -264,6 +264,12 @@ ks_ffma_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float*
             for (int m = 0; m < TM; ++m) acc[m][q] += bq;
         }
     }
+    if (act) {                                    // epilogue activation (NEXT-2), after the bias
+#pragma unroll
+        for (int m = 0; m < TM; ++m)
+#pragma unroll
+            for (int q = 0; q < TN; ++q) acc[m][q] = ks_act(acc[m][q], act);
+    }
     if (LAYOUT == KS_LAYOUT_BSL) {
         // Y[(i*b*d + k*d + j) * B + n], n contiguous
 #pragma unroll
@@ -382,7 +388,7 @@ cudaError_t launch_cfg(const ks_handle_s& h, const KsCall& call) {
     const int64_t blocks = nkc * nnb * (h.a * h.d / J);
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(C::THREADS), C::SMEM_BYTES, call.stream,
-                                         call.X, (const float*)h.k_tile, call.Y, call.bias, call.B, (int)h.a,
+                                         call.X, (const float*)h.k_tile, call.Y, call.bias, call.act, call.B, (int)h.a,
                                          (int)h.b, (int)h.c, (int)h.d);
     ks::count_launch();
     return e;

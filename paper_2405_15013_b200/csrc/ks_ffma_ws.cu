@@ -60,7 +60,7 @@ struct WsCfg {
 template <int LAYOUT, int BN, int KB = WS_BK>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                  float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                  float* __restrict__ Y, const float* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d,
                   int64_t ntiles) {
     using C = WsCfg<LAYOUT, BN, KB>;
     constexpr int S = C::S;
@@ -241,6 +241,12 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                 for (int m = 0; m < 8; ++m) acc[m][e] += bq;
             }
         }
+        if (act) {                                // epilogue activation (NEXT-2)
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int e = 0; e < TN; ++e) acc[m][e] = ks_act(acc[m][e], act);
+        }
         if constexpr (LAYOUT == KS_LAYOUT_BSL) {
             const int64_t nr = n0 + wm * 64 + ty * 4;
 #pragma unroll
@@ -306,7 +312,7 @@ struct WsgCfg {
 template <int TK>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                   float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                   float* __restrict__ Y, const float* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d,
                    int64_t ntiles) {
     using C = WsgCfg<TK>;
     constexpr int S = C::S;
@@ -467,6 +473,14 @@ ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                 }
             }
         }
+        if (act) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                    for (int e = 0; e < TK; ++e) acc[r][jj][e] = ks_act(acc[r][jj][e], act);
+        }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int64_t n = n0 + wm * 32 + ty + 8 * r;
@@ -509,7 +523,7 @@ cudaError_t launch_wsg(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(WS_THREADS), C::SMEM, call.stream, xmap, kmap,
-                                         call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
+                                         call.Y, call.bias, call.act, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
     return e;
 }
@@ -550,7 +564,7 @@ struct WslCfg {
 template <int NW>
 __global__ void __launch_bounds__(WslCfg<NW>::THREADS, 2)
 ks_ffma_wsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                   float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                   float* __restrict__ Y, const float* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d,
                    int64_t ntiles) {
     using C = WslCfg<NW>;
     constexpr int S = C::S;
@@ -679,6 +693,10 @@ ks_ffma_wsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                     const float4 bq = __ldg(reinterpret_cast<const float4*>(bias + r));
                     out[0] += bq.x; out[1] += bq.y; out[2] += bq.z; out[3] += bq.w;
                 }
+                if (act) {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) out[jj] = ks_act(out[jj], act);
+                }
                 if (n < B) __stcs(reinterpret_cast<float4*>(Y + n * M + r), make_float4(out[0], out[1], out[2], out[3]));
             }
         }
@@ -714,7 +732,7 @@ cudaError_t launch_wsl(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(C::THREADS), C::SMEM, call.stream, xmap,
-                                         kmap, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
+                                         kmap, call.Y, call.bias, call.act, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
                                          ntiles);
     ks::count_launch();
     return e;
@@ -763,7 +781,7 @@ struct WscCfg {
 template <int D, int TK>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 ks_ffma_wsc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                   float* __restrict__ Y, const float* __restrict__ bias, int64_t B, int a, int b, int c,
+                   float* __restrict__ Y, const float* __restrict__ bias, int act, int64_t B, int a, int b, int c,
                    int64_t ntiles) {
     using C = WscCfg<D, TK>;
     constexpr int S = C::S;
@@ -927,6 +945,14 @@ ks_ffma_wsc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                     for (int r = 0; r < R; ++r) acc[r][jj][e] += bq;
                 }
         }
+        if (act) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int jj = 0; jj < D; ++jj)
+#pragma unroll
+                    for (int e = 0; e < TK; ++e) acc[r][jj][e] = ks_act(acc[r][jj][e], act);
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int64_t n = n0 + wm * (8 * R) + ty + 8 * r;
@@ -972,7 +998,7 @@ cudaError_t launch_wsc(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(WS_THREADS), C::SMEM, call.stream, xmap, kmap,
-                                         call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, ntiles);
+                                         call.Y, call.bias, call.act, call.B, (int)h.a, (int)h.b, (int)h.c, ntiles);
     ks::count_launch();
     return e;
 }
@@ -1029,7 +1055,7 @@ cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(WS_THREADS), C::SMEM, call.stream, xmap, kmap,
-                                         call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
+                                         call.Y, call.bias, call.act, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
     return e;
 }

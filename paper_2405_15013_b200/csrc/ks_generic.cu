@@ -19,7 +19,7 @@ namespace {
 template <int XL, int YL>
 __global__ void __launch_bounds__(256) ks_generic_kernel(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
-    const float* __restrict__ bias, int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
+    const float* __restrict__ bias, int act, int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
     pdl_wait();
     pdl_launch_dependents();
     const int64_t M = a * b * d, N = a * c * d;
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
             const float x = XL == KS_LAYOUT_BSF ? X[n * N + s] : X[s * B + n];
             acc = fmaf(x, kp[l * d], acc);
         }
-        Y[e] = bias ? acc + bias[r] : acc;
+        Y[e] = ks_act(bias ? acc + bias[r] : acc, act);
     }
 }
 
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) ks_generic_kernel(
 // kernel cannot take).
 template <typename T, int XL, int YL>
 __global__ void __launch_bounds__(256) ks_generic_half_kernel(
-    const T* __restrict__ X, const T* __restrict__ K4, T* __restrict__ Y, const T* __restrict__ bias,
+    const T* __restrict__ X, const T* __restrict__ K4, T* __restrict__ Y, const T* __restrict__ bias, int act,
     int64_t B, int64_t a, int64_t b, int64_t c, int64_t d) {
     pdl_wait();
     pdl_launch_dependents();
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) ks_generic_half_kernel(
             acc = fmaf(x, (float)kp[l * d], acc);
         }
         if (bias) acc += (float)bias[r];
-        Y[e] = T(acc);
+        Y[e] = T(ks_act(acc, act));
     }
 }
 
@@ -94,7 +94,7 @@ cudaError_t launch_generic_half(const ks_handle_s& h, const KsCall& call) {
     const bool xf = call.layout == F, yf = call.ylayout() == F;
     auto kern = xf ? (yf ? ks_generic_half_kernel<T, F, F> : ks_generic_half_kernel<T, F, L>)
                    : (yf ? ks_generic_half_kernel<T, L, F> : ks_generic_half_kernel<T, L, L>);
-    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, X, K, Y, bias,
+    const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, X, K, Y, bias, call.act,
                                          call.B, (int64_t)h.a, (int64_t)h.b, (int64_t)h.c, (int64_t)h.d);
     ks::count_launch();
     return e;
@@ -123,7 +123,7 @@ cudaError_t generic_launch(const ks_handle_s& h, const KsCall& call) {
     auto kern = xf ? (yf ? ks_generic_kernel<F, F> : ks_generic_kernel<F, L>)
                    : (yf ? ks_generic_kernel<L, F> : ks_generic_kernel<L, L>);
     const cudaError_t e = launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream, call.X,
-                                     (const float*)h.k_canon, call.Y, call.bias, call.B, (int64_t)h.a, (int64_t)h.b,
+                                     (const float*)h.k_canon, call.Y, call.bias, call.act, call.B, (int64_t)h.a, (int64_t)h.b,
                                      (int64_t)h.c, (int64_t)h.d);
     count_launch();
     return e;

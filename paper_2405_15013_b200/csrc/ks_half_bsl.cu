@@ -71,7 +71,7 @@ __device__ __forceinline__ HbTile hb_decode(int64_t tile, int nkc, int64_t nnb, 
 template <typename T, int NT>
 __global__ void __launch_bounds__(HB_THREADS, HalfBslCfg<NT>::CTAS)
 ks_half_bsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                   T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d, int BN,
+                   T* __restrict__ Y, const T* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d, int BN,
                    int64_t ntiles) {
     using C = HalfBslCfg<NT>;
     constexpr int S = C::S;
@@ -185,7 +185,8 @@ ks_half_bsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                     uint32_t pk[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        const T lo = ElemTraits<T>::from_f(v[2 * e] + bv), hi = ElemTraits<T>::from_f(v[2 * e + 1] + bv);
+                        const T lo = ElemTraits<T>::from_f(ks_act(v[2 * e] + bv, act)),
+                                hi = ElemTraits<T>::from_f(ks_act(v[2 * e + 1] + bv, act));
                         pk[e] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
                                 ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
                     }
@@ -258,7 +259,7 @@ cudaError_t launch_hb(const ks_handle_s& h, const KsCall& call) {
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(HB_THREADS), C::SMEM, call.stream, xmap,
                                          kmap, reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias),
-                                         call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, BN, ntiles);
+                                         call.act, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, BN, ntiles);
     ks::count_launch();
     return e;
 }

@@ -39,6 +39,7 @@ struct KsCall {
     const float* bias = nullptr;   // optional length-M vector added in the epilogue
     uint32_t knobs = 0;            // KsKnob bits (ks::plan_knobs)
     int out_layout = -1;           // layout of Y (ks_matmul_io / chain intermediates); -1: `layout`
+    int act = KS_ACT_NONE;         // epilogue activation after the bias (ks_activation_t)
     int ylayout() const { return out_layout < 0 ? layout : out_layout; }
     bool mixed() const { return ylayout() != layout; }
 };
@@ -151,6 +152,11 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
 }
 __device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
+// Epilogue activation (NEXT-2): the exact GELU 0.5 y (1 + erf(y / sqrt 2)), FP32.
+__device__ __forceinline__ float ks_act(float y, int act) {
+    return act == KS_ACT_GELU ? 0.5f * y * (1.f + erff(y * 0.7071067811865476f)) : y;
+}
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

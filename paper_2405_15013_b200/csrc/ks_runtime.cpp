@@ -175,9 +175,10 @@ cudaError_t launch(ks_kernel_t k, const ks_handle_s& h, const KsCall& call) {
 
 // One factor, arguments already validated.
 ks_status_t run_one(const ks_handle_s& h, const float* X, float* Y, int64_t B, int layout,
-                    cudaStream_t s, const float* bias = nullptr, int out_layout = -1) {
+                    cudaStream_t s, const float* bias = nullptr, int out_layout = -1, int act = KS_ACT_NONE) {
     KsCall call{X, Y, B, layout, s, bias};
     call.out_layout = out_layout;
+    call.act = act;
     call.knobs = ks::plan_knobs(h, call);
     ks_kernel_t k = choose(h, call);
     if (k == KS_KERNEL_AUTO)
@@ -310,10 +311,12 @@ void chain_workspace(const ks_handle_t* hs, int L, int64_t B, size_t* bytes, int
 // caller-owned intermediate buffers (ks_chain_graph), else stream-ordered
 // allocations from the device pool.
 ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, int64_t B,
-                      int layout, cudaStream_t s, const float* bias = nullptr, void* const* ws = nullptr) {
-    if (L == 1) return run_one(*hs[0], X, Y, B, layout, s, bias);
+                      int layout, cudaStream_t s, const float* bias = nullptr, void* const* ws = nullptr,
+                      int act = KS_ACT_NONE) {
+    if (L == 1) return run_one(*hs[0], X, Y, B, layout, s, bias, -1, act);
     {
         KsCall call{X, Y, B, layout, s, bias};
+        call.act = act;
         if (fusion_ok(hs, L, call)) return run_fused(hs, L, call);
     }
     size_t bytes;
@@ -340,7 +343,7 @@ ks_status_t run_chain(const ks_handle_t* hs, int L, const float* X, float* Y, in
     const float* in = X;
     for (int l = L - 1; l >= 0 && st == KS_OK; --l) {
         float* out = (l == 0) ? Y : static_cast<float*>(buf[(L - 1 - l) % nbuf]);
-        st = run_one(*hs[l], in, out, B, lay[l + 1], s, l == 0 ? bias : nullptr, lay[l]);
+        st = run_one(*hs[l], in, out, B, lay[l + 1], s, l == 0 ? bias : nullptr, lay[l], l == 0 ? act : KS_ACT_NONE);
         in = out;                                                    // bias after the last hop
     }
     if (!ws)
@@ -545,9 +548,10 @@ ks_status_t ks_matmul(ks_handle_t h, const float* X, float* Y, int64_t B, ks_lay
     return ks_matmul_bias(h, X, Y, nullptr, B, layout, stream);
 }
 
-ks_status_t ks_matmul_any(ks_handle_t h, const void* X, void* Y, const void* bias, int64_t B,
+ks_status_t ks_matmul_act(ks_handle_t h, const void* X, void* Y, const void* bias, ks_activation_t act, int64_t B,
                           ks_layout_t layout, ks_stream_t stream) {
     if (!h) return fail(KS_ERR_INVALID_ARG, "NULL handle");
+    if (act != KS_ACT_NONE && act != KS_ACT_GELU) return fail(KS_ERR_INVALID_ARG, "bad activation %d", (int)act);
     const uintptr_t amask = (uintptr_t)h->esize() - 1;
     if (reinterpret_cast<uintptr_t>(bias) & amask) return fail(KS_ERR_ALIGNMENT, "bias must be element-aligned");
     if (B < 0) return fail(KS_ERR_INVALID_ARG, "B must be >= 0");
@@ -563,8 +567,13 @@ ks_status_t ks_matmul_any(ks_handle_t h, const void* X, void* Y, const void* bia
         return fail(KS_ERR_INVALID_ARG, "B too large");
     if (overlap(X, xb, Y, yb)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
     s = run_one(*h, static_cast<const float*>(X), static_cast<float*>(Y), B, layout,
-                static_cast<cudaStream_t>(stream), static_cast<const float*>(bias));
+                static_cast<cudaStream_t>(stream), static_cast<const float*>(bias), -1, (int)act);
     return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_matmul_any(ks_handle_t h, const void* X, void* Y, const void* bias, int64_t B,
+                          ks_layout_t layout, ks_stream_t stream) {
+    return ks_matmul_act(h, X, Y, bias, KS_ACT_NONE, B, layout, stream);
 }
 
 ks_status_t ks_matmul_bias(ks_handle_t h, const float* X, float* Y, const float* bias, int64_t B,
@@ -578,8 +587,9 @@ ks_status_t ks_chain_ex(const ks_handle_t* hs, int L, const float* X, float* Y, 
     return ks_chain_bias(hs, L, X, Y, nullptr, B, layout, stream);
 }
 
-ks_status_t ks_chain_any(const ks_handle_t* hs, int L, const void* X, void* Y, const void* bias,
-                         int64_t B, ks_layout_t layout, ks_stream_t stream) {
+ks_status_t ks_chain_act(const ks_handle_t* hs, int L, const void* X, void* Y, const void* bias,
+                         ks_activation_t act, int64_t B, ks_layout_t layout, ks_stream_t stream) {
+    if (act != KS_ACT_NONE && act != KS_ACT_GELU) return fail(KS_ERR_INVALID_ARG, "bad activation %d", (int)act);
     ks_status_t s = validate_chain(hs, L, B, (int)layout);
     if (s != KS_OK) return s;
     const int es = hs[0]->esize();
@@ -591,8 +601,13 @@ ks_status_t ks_chain_any(const ks_handle_t* hs, int L, const void* X, void* Y, c
         return fail(KS_ERR_ALIGNMENT, "X and Y must be element-aligned");
     if (overlap(X, B * hs[L - 1]->N * es, Y, B * hs[0]->M * es)) return fail(KS_ERR_INVALID_ARG, "X and Y overlap");
     s = run_chain(hs, L, static_cast<const float*>(X), static_cast<float*>(Y), B, (int)layout,
-                  static_cast<cudaStream_t>(stream), static_cast<const float*>(bias));
+                  static_cast<cudaStream_t>(stream), static_cast<const float*>(bias), nullptr, (int)act);
     return s == KS_OK ? ok() : s;
+}
+
+ks_status_t ks_chain_any(const ks_handle_t* hs, int L, const void* X, void* Y, const void* bias,
+                         int64_t B, ks_layout_t layout, ks_stream_t stream) {
+    return ks_chain_act(hs, L, X, Y, bias, KS_ACT_NONE, B, layout, stream);
 }
 
 ks_status_t ks_chain_bias(const ks_handle_t* hs, int L, const float* X, float* Y, const float* bias,

@@ -26,7 +26,7 @@ constexpr int SC_WARPS = 4;    // warps per CTA
 template <int LAYOUT, int CL>
 __global__ void __launch_bounds__(SC_WARPS * 32)
 ks_splitc_kernel(const float* __restrict__ X, const float* __restrict__ Kt, float* __restrict__ Y,
-                 const float* __restrict__ bias, int64_t B, int a, int b, int c, int d) {
+                 const float* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * SC_WARPS + (threadIdx.x >> 5);
     const int nkc = b / SC_K;
@@ -87,6 +87,7 @@ ks_splitc_kernel(const float* __restrict__ X, const float* __restrict__ Kt, floa
         const int64_t row = (int64_t)i * b * d + (int64_t)(k0 + k) * d + j;
         float y = v[0];
         if (bias) y += __ldg(bias + row);
+        y = ks_act(y, act);
         if (LAYOUT == KS_LAYOUT_BSL)
             Y[row * B + n] = y;
         else
@@ -103,7 +104,7 @@ cudaError_t launch_splitc(const ks_handle_s& h, const KsCall& call) {
 #define KS_SC_CASE(n)                                                                                     \
     case n:                                                                                               \
         e = ks::launch_pdl(ks_splitc_kernel<LAYOUT, n>, grid, block, 0, call.stream, call.X, h.k_tile, call.Y, \
-                           call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d);                    \
+                           call.bias, call.act, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d);          \
         break;
     switch (cl) {
         KS_SC_CASE(1) KS_SC_CASE(2) KS_SC_CASE(3) KS_SC_CASE(4) KS_SC_CASE(5) KS_SC_CASE(6) KS_SC_CASE(7)

@@ -55,12 +55,17 @@ __device__ __forceinline__ float4 vadd(float4 a, float4 b) {
 __device__ __forceinline__ float vadds(float a, float s) { return a + s; }
 __device__ __forceinline__ float2 vadds(float2 a, float s) { return make_float2(a.x + s, a.y + s); }
 __device__ __forceinline__ float4 vadds(float4 a, float s) { return make_float4(a.x + s, a.y + s, a.z + s, a.w + s); }
+__device__ __forceinline__ float vact(float a, int act) { return ks_act(a, act); }
+__device__ __forceinline__ float2 vact(float2 a, int act) { return make_float2(ks_act(a.x, act), ks_act(a.y, act)); }
+__device__ __forceinline__ float4 vact(float4 a, int act) {
+    return make_float4(ks_act(a.x, act), ks_act(a.y, act), ks_act(a.z, act), ks_act(a.w, act));
+}
 
 // ---------------------------------------------------------------- BSF ------
 template <int BB, int CC, int V, int RT>
 __global__ void __launch_bounds__(256) ks_stream_bsf(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
-    const float* __restrict__ bias, int64_t B, int a, int d) {
+    const float* __restrict__ bias, int act, int64_t B, int a, int d) {
     using T = typename Vec<V>::T;
     pdl_wait();
     pdl_launch_dependents();
@@ -105,6 +110,7 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
 #pragma unroll
             for (int l = 0; l < CC; ++l) acc = vfma(xr[r][l], kr[k][l], acc);
             if (bias) acc = vadd(acc, br[k]);
+            if (act) acc = vact(acc, act);
             __stcs(reinterpret_cast<T*>(yb + r * M + k * d), acc);
         }
     }
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
 template <int BB, int CC, int V, int RT>
 __global__ void __launch_bounds__(256) ks_stream_bsl(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
-    const float* __restrict__ bias, int64_t B, int a, int d, int64_t nblocks) {
+    const float* __restrict__ bias, int act, int64_t B, int a, int d, int64_t nblocks) {
     using T = typename Vec<V>::T;
     pdl_wait();
     pdl_launch_dependents();
@@ -152,6 +158,7 @@ __global__ void __launch_bounds__(256) ks_stream_bsl(
 #pragma unroll
             for (int l = 0; l < CC; ++l) acc = vfmas(xr[r][l], kr[k][l], acc);
             if (bias) acc = vadds(acc, __ldg(bias + (int64_t)i * BB * d + k * d + j));
+            if (act) acc = vact(acc, act);
             __stcs(reinterpret_cast<T*>(yb + k * rowx) + nv, acc);
         }
     }
@@ -167,7 +174,7 @@ cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
     const int64_t items = P * ((call.B + RT - 1) / RT);
     const int64_t blocks = (items + threads - 1) / threads;
     cudaError_t e = ks::launch_pdl(ks_stream_bsf<BB, CC, V, RT>, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
-                                   call.X, (const float*)h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d);
+                                   call.X, (const float*)h.k_canon, call.Y, call.bias, call.act, call.B, (int)h.a, (int)h.d);
     ks::count_launch();
     return e;
 }
@@ -181,8 +188,8 @@ cudaError_t launch_bsl(const ks_handle_s& h, const KsCall& call) {
     const int64_t nblocks = (NV + (int64_t)threads * RT - 1) / ((int64_t)threads * RT);
     const int64_t blocks = h.a * h.d * nblocks;
     cudaError_t e = ks::launch_pdl(ks_stream_bsl<BB, CC, V, RT>, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
-                                   call.X, (const float*)h.k_canon, call.Y, call.bias, call.B, (int)h.a, (int)h.d,
-                                   nblocks);
+                                   call.X, (const float*)h.k_canon, call.Y, call.bias, call.act, call.B, (int)h.a,
+                                   (int)h.d, nblocks);
     ks::count_launch();
     return e;
 }

@@ -118,7 +118,9 @@ template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LA
 __global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap kmap_lo, T* __restrict__ Y, const T* __restrict__ bias,
-               int64_t B, int a, int b, int c, int d, int64_t ntiles, int dbg) {
+               int64_t B, int a, int b, int c, int d, int64_t ntiles, int flags) {
+    // flags: bits 0-7 = KS_TF32_DEBUG experiment switches, bits 8-15 = epilogue activation
+    const int dbg = flags & 0xFF, act = (flags >> 8) & 0xFF;
     using C = Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>;
     static_assert(LAYOUT != KS_LAYOUT_BSL || sizeof(T) == 4, "half BSL runs the swap-AB kernel (ks_half_bsl.cu)");
     constexpr bool STAGED = LAYOUT == KS_LAYOUT_BSL && !MNA;    // X through the staging ring + transposers
@@ -352,6 +354,10 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     for (int e = 0; e < 16; ++e)
                         v[e] += ElemTraits<T>::to_f(bias[(int64_t)tc.i * b * d + (int64_t)(tc.k0 + col + e) * d + tc.j]);
                 }
+                if (act) {                        // epilogue activation (NEXT-2), after the bias
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = ks_act(v[e], act);
+                }
                 if constexpr (OUTL != KS_LAYOUT_BSL) {
                     // BSF out (d = 1): row n's 16 outputs are contiguous; coalesce through scratch
                     if constexpr (sizeof(T) == 4) {
@@ -474,7 +480,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     const __grid_constant__ CUtensorMap kmap_lo, float* __restrict__ Y,
                     const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles,
-                    int dbg) {
+                    int flags) {
+    // flags: bits 0-7 = KS_TF32_DEBUG experiment switches, bits 8-15 = epilogue activation
+    const int dbg = flags & 0xFF, act = (flags >> 8) & 0xFF;
     using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL>;
     static_assert(INL == KS_LAYOUT_BSF || !GATHER, "BSL input needs no gather");
     constexpr int S = C::S;
@@ -688,6 +696,12 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
                         for (int jj = 0; jj < J; ++jj) v[jj][e] += __ldg(bias + r0 + (int64_t)e * d + jj);
                 }
+                if (act) {
+#pragma unroll
+                    for (int e = 0; e < EC; ++e)
+#pragma unroll
+                        for (int jj = 0; jj < J; ++jj) v[jj][e] = ks_act(v[jj][e], act);
+                }
                 if constexpr (OUTL == KS_LAYOUT_BSL) {    // Y^T row r0 + e d + jj: lanes = 32 batch rows
                     const int64_t n = (int64_t)tc.n0 + lq * 32 + lane;
                     if (n < B && !(dbg & 1)) {
@@ -769,7 +783,7 @@ struct HalfJCfg {
 template <typename T, int J, int BN, int JB = J, int HK = 16>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                    T* __restrict__ Y, const T* __restrict__ bias, int64_t B, int a, int b, int c, int d,
+                    T* __restrict__ Y, const T* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d,
                     int64_t ntiles) {
     using C = HalfJCfg<J, BN, JB, HK>;
     constexpr int AH_BYTES = C::AH_BYTES;
@@ -978,6 +992,12 @@ ks_half_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
                         for (int jj = 0; jj < J; ++jj) v[jj][e] += ElemTraits<T>::to_f(bias[r0 + (int64_t)e * d + jj]);
                 }
+                if (act) {
+#pragma unroll
+                    for (int e = 0; e < EC; ++e)
+#pragma unroll
+                        for (int jj = 0; jj < J; ++jj) v[jj][e] = ks_act(v[jj][e], act);
+                }
                 if constexpr (JB != J) {
                     // J = 4 of an 8-wide box (d % 8 != 0): the 4 outputs of one k are one
                     // 8-byte run, the next k is d away -- per-row stores (units of the
@@ -1069,7 +1089,7 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
                                          kmap_lo, reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias),
-                                         call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags());
+                                         call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags() | (call.act << 8));
     ks::count_launch();
     return e;
 }
@@ -1196,7 +1216,7 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
                                          kmap_lo, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
-                                         ntiles, debug_flags());
+                                         ntiles, debug_flags() | (call.act << 8));
     ks::count_launch();
     return e;
 }
@@ -1295,7 +1315,7 @@ cudaError_t launch_halfj(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
-                                         reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias), call.B,
+                                         reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias), call.act, call.B,
                                          (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles);
     ks::count_launch();
     return e;

@@ -67,7 +67,8 @@ template <int LAYOUT, int BN>
 __global__ void __launch_bounds__(V2_THREADS, 1)
 ks_tf32v2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ CUtensorMap ymap, const float* __restrict__ bias, int64_t B, int a, int b,
-                 int c, int d, int64_t ntiles, int S, int NKB, uint32_t KT, int order, float* __restrict__ Yd) {
+                 int c, int d, int64_t ntiles, int S, int NKB, uint32_t KT, int order_act, float* __restrict__ Yd) {
+    const int order = order_act & 0xFF, act = (order_act >> 8) & 0xFF;   // bits 8-15: epilogue activation
     constexpr int CW = BN % 32 == 0 ? 32 : 16;          // output columns per store box
     constexpr uint32_t EBOX = 32 * CW * 4;               // one warp's staged box
     constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -244,6 +245,10 @@ ks_tf32v2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
                         v[e] += __ldg(bias + (BSL ? kg * d + tc.j : kg));
                     }
                 }
+                if (act) {                               // epilogue activation (NEXT-2)
+#pragma unroll
+                    for (int e = 0; e < CW; ++e) v[e] = ks_act(v[e], act);
+                }
                 if (BSL && (order & 2)) {                // experiment: direct coalesced stores (no TMA store)
                     const int64_t n = (int64_t)tc.n0 + wq * 32 + lane;
                     if (n < B) {
@@ -407,7 +412,7 @@ cudaError_t v2_launch_bn(const ks_handle_s& h, const KsCall& call, const V2Plan&
     const cudaError_t e =
         ks::launch_pdl(kern, dim3((unsigned)grid), dim3(V2_THREADS), (size_t)p.smem, call.stream, xmap, kmap, ymap,
                        call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles, p.S, p.NKB, p.KT,
-                       v2_order(call.B), call.Y);
+                       v2_order(call.B) | (call.act << 8), call.Y);
     ks::count_launch();
     return e;
 }

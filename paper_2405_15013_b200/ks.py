@@ -47,7 +47,7 @@ EXPORTS = ["ks_pack_weights", "ks_pack_weights_ex", "ks_get_dtype", "ks_matmul_a
            "ks_kernel_launch_count", "ks_abi_version",
            "ks_chain_graph", "ks_graph_launch", "ks_graph_kernel_count", "ks_graph_free", "ks_peak_ffma",
            "ks_set_knobs", "ks_plan_knobs", "ks_preset_count",
-           "ks_matmul_io", "ks_set_chain_mixed_layouts", "ks_chain_layouts"]
+           "ks_matmul_io", "ks_set_chain_mixed_layouts", "ks_chain_layouts", "ks_matmul_act", "ks_chain_act"]
 
 
 class KSError(RuntimeError):
@@ -102,6 +102,10 @@ def load_library(path: str = LIB_PATH):
     lib.ks_set_chain_fusion.argtypes = [ctypes.c_int]
     lib.ks_set_chain_fusion.restype = st
     lib.ks_chain_fusion_eligible.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int]
+    lib.ks_matmul_act.argtypes = [vp, fp, fp, fp, ctypes.c_int, i64, ctypes.c_int, vp]
+    lib.ks_matmul_act.restype = ctypes.c_int
+    lib.ks_chain_act.argtypes = [ctypes.POINTER(vp), ctypes.c_int, fp, fp, fp, ctypes.c_int, i64, ctypes.c_int, vp]
+    lib.ks_chain_act.restype = ctypes.c_int
     lib.ks_matmul_io.argtypes = [vp, fp, ctypes.c_int, fp, ctypes.c_int, i64, vp]
     lib.ks_matmul_io.restype = ctypes.c_int
     lib.ks_set_chain_mixed_layouts.argtypes = [ctypes.c_int]
@@ -319,9 +323,19 @@ def _check_io(dtype_id, n_in, n_out, X, Y, B, lay, bias=None):
             raise ValueError(f"bias is on {bias.device}, X on {X.device}")
 
 
-def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None, bias=None):
-    """Y = X K^T (+ bias) through ks_matmul / ks_matmul_bias.  X: CUDA tensor of
-    the factor's element type, (B, N) for BSF or (N, B) for BSL; bias: (M,) or None."""
+ACTIVATIONS = {None: 0, "none": 0, "gelu": 1}
+
+
+def _act(act) -> int:
+    if act not in ACTIVATIONS:
+        raise ValueError(f"activation must be one of {sorted(k for k in ACTIVATIONS if k)} or None, got {act!r}")
+    return ACTIVATIONS[act]
+
+
+def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None, bias=None, act=None):
+    """Y = act(X K^T (+ bias)) through ks_matmul / ks_matmul_bias / ks_matmul_act.
+    X: CUDA tensor of the factor's element type, (B, N) for BSF or (N, B) for
+    BSL; bias: (M,) or None; act: None or "gelu" (fused into the epilogue)."""
     import torch
     lay = _layout(layout)
     if B is None:
@@ -329,7 +343,12 @@ def matmul(f: Factor, X, Y=None, layout="bsf", stream=None, B: int | None = None
     if Y is None:
         Y = torch.empty((B, f.M) if lay == BSF else (f.M, B), device=X.device, dtype=_torch_dtype(f.dtype))
     _check_io(f.dtype, f.N, f.M, X, Y, int(B), lay, bias)
-    if f.dtype != DTYPE_F32:
+    a = _act(act)
+    if a:
+        bp = _dev_ptr(bias, "bias") if bias is not None else None
+        _check(_lib.ks_matmul_act(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, a, int(B), lay,
+                                  _stream_ptr(stream)))
+    elif f.dtype != DTYPE_F32:
         bp = _dev_ptr(bias, "bias") if bias is not None else None
         _check(_lib.ks_matmul_any(f.handle, _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, int(B), lay,
                                   _stream_ptr(stream)))
@@ -346,9 +365,9 @@ def _handles(factors):
     return arr
 
 
-def chain(factors, X, Y=None, layout="bsf", stream=None, bias=None):
-    """Y = X K_L^T ... K_1^T (+ bias) through ks_chain_ex / ks_chain_bias; factors
-    in paper order K_1..K_L."""
+def chain(factors, X, Y=None, layout="bsf", stream=None, bias=None, act=None):
+    """Y = act(X K_L^T ... K_1^T (+ bias)) through ks_chain_ex / ks_chain_bias /
+    ks_chain_act; factors in paper order K_1..K_L."""
     import torch
     lay = _layout(layout)
     if not factors:
@@ -360,7 +379,12 @@ def chain(factors, X, Y=None, layout="bsf", stream=None, bias=None):
     if any(f.dtype != factors[0].dtype for f in factors):
         raise TypeError("all factors of a chain must have the same element type")
     _check_io(factors[0].dtype, factors[-1].N, M, X, Y, int(B), lay, bias)
-    if factors[0].dtype != DTYPE_F32:
+    a = _act(act)
+    if a:
+        bp = _dev_ptr(bias, "bias") if bias is not None else None
+        _check(_lib.ks_chain_act(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp, a,
+                                 int(B), lay, _stream_ptr(stream)))
+    elif factors[0].dtype != DTYPE_F32:
         bp = _dev_ptr(bias, "bias") if bias is not None else None
         _check(_lib.ks_chain_any(_handles(factors), len(factors), _dev_ptr(X, "X"), _dev_ptr(Y, "Y"), bp,
                                  int(B), lay, _stream_ptr(stream)))

@@ -2,8 +2,9 @@
 weight is a product of Kronecker-sparse factors W = K_1 ... K_L (the paper's
 layer).
 
-forward(x) = x W^T + bias, computed by ks_chain_bias (all factors on the GPU
-kernels of libks.so, the bias fused into the last factor's epilogue).  Both
+forward(x) = act(x W^T + bias), computed by ks_chain_bias / ks_chain_act (all
+factors on the GPU kernels of libks.so, the bias and the optional GELU -- the
+FFN row of Table 7, PAPER.md:1568 -- fused into the last factor's epilogue).  Both
 batch layouts are supported: ``layout="bsf"`` takes x of
 shape (..., in_features); ``layout="bsl"`` takes x of shape (in_features, B).
 Inference only (the paper's scope): no autograd.
@@ -23,7 +24,8 @@ def _chainable(patterns) -> bool:
 
 class KSLinear(torch.nn.Module):
     def __init__(self, patterns, weights=None, bias: bool | torch.Tensor = True, layout: str = "bsf",
-                 math_mode: str = "fp32", device="cuda", generator: torch.Generator | None = None):
+                 math_mode: str = "fp32", device="cuda", generator: torch.Generator | None = None,
+                 activation: str | None = None):
         """patterns: [(a,b,c,d), ...] in product order K_1..K_L (a_l c_l d_l ==
         a_{l+1} b_{l+1} d_{l+1}).  math_mode: "fp32" (CUDA cores),
         "tf32" or "f32x3" (FP32-accurate 3xTF32) on the tensor cores for factors
@@ -31,6 +33,8 @@ class KSLinear(torch.nn.Module):
         canonical (a,b,c,d) float32 tensors/arrays, or None for the paper's
         initialisation U[-1/sqrt(c), 1/sqrt(c)]."""
         super().__init__()
+        ks._act(activation)
+        self.activation = activation
         patterns = [tuple(int(v) for v in p) for p in patterns]
         if not patterns or not _chainable(patterns):
             raise ValueError(f"patterns are not a chain: {patterns}")
@@ -70,12 +74,12 @@ class KSLinear(torch.nn.Module):
         if self.layout == "bsl":
             if x.dim() != 2 or x.shape[0] != self.in_features:
                 raise ValueError(f"BSL input must be ({self.in_features}, B)")
-            return ks.chain(self.factors, x.contiguous(), layout="bsl", bias=self.bias)
+            return ks.chain(self.factors, x.contiguous(), layout="bsl", bias=self.bias, act=self.activation)
         lead = x.shape[:-1]
         if x.shape[-1] != self.in_features:
             raise ValueError(f"last dimension must be {self.in_features}")
         x2 = x.reshape(-1, self.in_features).contiguous()
-        y = ks.chain(self.factors, x2, layout="bsf", bias=self.bias)
+        y = ks.chain(self.factors, x2, layout="bsf", bias=self.bias, act=self.activation)
         return y.reshape(*lead, self.out_features)
 
     def extra_repr(self) -> str:

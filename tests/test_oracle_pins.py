@@ -467,3 +467,18 @@ def test_model_bytes_and_pattern_check_hand_values():
         with pytest.raises(ValueError):
             O.check_pattern(bad)
     assert O.check_pattern((2, 3, 4, 5)) == (2, 3, 4, 5)
+
+
+def test_gelu_hand_values_and_identity():
+    """oracle.gelu against y * Phi(y) with Phi from the standard library's
+    NormalDist (not math.erf), hand values, and gelu(y) - gelu(-y) = y."""
+    from statistics import NormalDist
+    phi = NormalDist().cdf
+    ys = np.array([-6.0, -3.0, -1.0, -0.5, 0.0, 0.25, 1.0, 2.0, 5.0])
+    g = O.gelu(ys)
+    for y, v in zip(ys, g):
+        assert abs(v - y * phi(y)) <= 1e-15 * max(1.0, abs(y))
+    assert O.gelu(np.array([0.0]))[0] == 0.0
+    assert abs(O.gelu(np.array([1.0]))[0] - 0.8413447460685429) < 1e-15
+    assert abs(O.gelu(np.array([-1.0]))[0] + 0.15865525393145705) < 1e-15
+    assert np.allclose(O.gelu(ys) - O.gelu(-ys), ys, rtol=0, atol=1e-15)
