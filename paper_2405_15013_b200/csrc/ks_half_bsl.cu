@@ -68,7 +68,7 @@ __device__ __forceinline__ HbTile hb_decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-template <typename T, int NT>
+template <typename T, int NT, bool ACT = false>
 __global__ void __launch_bounds__(HB_THREADS, HalfBslCfg<NT>::CTAS)
 ks_half_bsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                    T* __restrict__ Y, const T* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d, int BN,
@@ -185,8 +185,12 @@ ks_half_bsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
                     uint32_t pk[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        const T lo = ElemTraits<T>::from_f(ks_act(v[2 * e] + bv, act)),
-                                hi = ElemTraits<T>::from_f(ks_act(v[2 * e + 1] + bv, act));
+                        float y0 = v[2 * e] + bv, y1 = v[2 * e + 1] + bv;
+                        if constexpr (ACT) {                 // epilogue activation (compile-time switch)
+                            y0 = ks_act(y0, act);
+                            y1 = ks_act(y1, act);
+                        }
+                        const T lo = ElemTraits<T>::from_f(y0), hi = ElemTraits<T>::from_f(y1);
                         pk[e] = (uint32_t)reinterpret_cast<const uint16_t&>(lo) |
                                 ((uint32_t)reinterpret_cast<const uint16_t&>(hi) << 16);
                     }
@@ -228,7 +232,7 @@ int hb_pick_bn(int64_t b) {
     return 0;
 }
 
-template <typename T, int NT>
+template <typename T, int NT, bool ACT = false>
 cudaError_t launch_hb(const ks_handle_s& h, const KsCall& call) {
     using C = HalfBslCfg<NT>;
     const CUtensorMapDataType dt = ElemTraits<T>::tma;
@@ -246,7 +250,7 @@ cudaError_t launch_hb(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t xb[3] = {64, 1, HB_BK};
         if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_half_bsl_kernel<T, NT>;
+    auto kern = ks_half_bsl_kernel<T, NT, ACT>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -283,6 +287,10 @@ cudaError_t half_bsl_launch(const ks_handle_s& h, const KsCall& call) {
         return e ? atoi(e) : 128;
     }();
     const bool bf = h.dtype == KS_DTYPE_BF16;
+    if (call.act) {
+        if (nt == 256) return bf ? launch_hb<__nv_bfloat16, 256, true>(h, call) : launch_hb<__half, 256, true>(h, call);
+        return bf ? launch_hb<__nv_bfloat16, 128, true>(h, call) : launch_hb<__half, 128, true>(h, call);
+    }
     if (nt == 256) return bf ? launch_hb<__nv_bfloat16, 256>(h, call) : launch_hb<__half, 256>(h, call);
     return bf ? launch_hb<__nv_bfloat16, 128>(h, call) : launch_hb<__half, 128>(h, call);
 }

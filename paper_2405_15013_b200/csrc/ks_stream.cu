@@ -62,7 +62,7 @@ __device__ __forceinline__ float4 vact(float4 a, int act) {
 }
 
 // ---------------------------------------------------------------- BSF ------
-template <int BB, int CC, int V, int RT>
+template <int BB, int CC, int V, int RT, bool ACT = false>
 __global__ void __launch_bounds__(256) ks_stream_bsf(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
     const float* __restrict__ bias, int act, int64_t B, int a, int d) {
@@ -110,14 +110,14 @@ __global__ void __launch_bounds__(256) ks_stream_bsf(
 #pragma unroll
             for (int l = 0; l < CC; ++l) acc = vfma(xr[r][l], kr[k][l], acc);
             if (bias) acc = vadd(acc, br[k]);
-            if (act) acc = vact(acc, act);
+            if constexpr (ACT) acc = vact(acc, act);     // epilogue activation (compile-time switch)
             __stcs(reinterpret_cast<T*>(yb + r * M + k * d), acc);
         }
     }
 }
 
 // ---------------------------------------------------------------- BSL ------
-template <int BB, int CC, int V, int RT>
+template <int BB, int CC, int V, int RT, bool ACT = false>
 __global__ void __launch_bounds__(256) ks_stream_bsl(
     const float* __restrict__ X, const float* __restrict__ K4, float* __restrict__ Y,
     const float* __restrict__ bias, int act, int64_t B, int a, int d, int64_t nblocks) {
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) ks_stream_bsl(
 #pragma unroll
             for (int l = 0; l < CC; ++l) acc = vfmas(xr[r][l], kr[k][l], acc);
             if (bias) acc = vadds(acc, __ldg(bias + (int64_t)i * BB * d + k * d + j));
-            if (act) acc = vact(acc, act);
+            if constexpr (ACT) acc = vact(acc, act);     // epilogue activation (compile-time switch)
             __stcs(reinterpret_cast<T*>(yb + k * rowx) + nv, acc);
         }
     }
@@ -173,7 +173,8 @@ cudaError_t launch_bsf(const ks_handle_s& h, const KsCall& call) {
     const int64_t P = h.a * (h.d / V);
     const int64_t items = P * ((call.B + RT - 1) / RT);
     const int64_t blocks = (items + threads - 1) / threads;
-    cudaError_t e = ks::launch_pdl(ks_stream_bsf<BB, CC, V, RT>, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
+    auto kern = call.act ? ks_stream_bsf<BB, CC, V, RT, true> : ks_stream_bsf<BB, CC, V, RT, false>;
+    cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
                                    call.X, (const float*)h.k_canon, call.Y, call.bias, call.act, call.B, (int)h.a, (int)h.d);
     ks::count_launch();
     return e;
@@ -187,7 +188,8 @@ cudaError_t launch_bsl(const ks_handle_s& h, const KsCall& call) {
     if (NV < 256) threads = (int)((NV + 31) / 32 * 32);
     const int64_t nblocks = (NV + (int64_t)threads * RT - 1) / ((int64_t)threads * RT);
     const int64_t blocks = h.a * h.d * nblocks;
-    cudaError_t e = ks::launch_pdl(ks_stream_bsl<BB, CC, V, RT>, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
+    auto kern = call.act ? ks_stream_bsl<BB, CC, V, RT, true> : ks_stream_bsl<BB, CC, V, RT, false>;
+    cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, call.stream,
                                    call.X, (const float*)h.k_canon, call.Y, call.bias, call.act, call.B, (int)h.a,
                                    (int)h.d, nblocks);
     ks::count_launch();
