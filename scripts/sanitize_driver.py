@@ -20,7 +20,7 @@ dev = torch.device("cuda:0")
 bad = []
 
 
-def run(p, lay, math="fp32", kernel=None, B=260, bias=False):
+def run(p, lay, math="fp32", kernel=None, B=260, bias=False, knobs=None, act=None):
     M, N, _ = O.dims(p)
     K4 = ksgen.k4_uniform(*p, seed=7)
     X = ksgen.x_normal(B, N, seed=8)
@@ -31,12 +31,16 @@ def run(p, lay, math="fp32", kernel=None, B=260, bias=False):
         f.set_math(ksb.MATH_F32X3)
     if kernel is not None:
         f.set_kernel(kernel)
+    if knobs is not None:
+        f.set_knobs(knobs | f.plan_knobs(B, lay)[0])
     bv = ksgen.x_normal(1, M, seed=9)[0] if bias else None
     Xd = torch.from_numpy(X if lay == "bsf" else ksgen.to_bsl(X)).to(dev)
-    Y = ksb.matmul(f, Xd, layout=lay, bias=torch.from_numpy(bv).to(dev) if bias else None)
+    Y = ksb.matmul(f, Xd, layout=lay, bias=torch.from_numpy(bv).to(dev) if bias else None, act=act)
     torch.cuda.synchronize()
     Yh = Y.cpu().numpy() if lay == "bsf" else Y.cpu().numpy().T
     ref = O.matmul(p, K4, X) + (bv[None, :] if bias else 0)
+    if act == "gelu":
+        ref = O.gelu(ref)
     e = O.normwise_error(Yh, ref)
     tol = 5e-3 if math == "tf32" else 1e-5
     plan = f.plan(B, lay)
@@ -60,6 +64,25 @@ for lay in ("bsf", "bsl"):
     run((1, 128, 128, 3), lay, "tf32", bias=True)               # densified (BSF, a = 1, d = 3)
     run((1, 768, 192, 2), lay, "tf32", B=200)                   # BN = 256 (BSF) / densified
     run((1, 64, 64, 4), lay, "f32x3")                           # 3xTF32
+# round 2: MN-major TF32 BSL, lane-j FFMA BSF, split-c (small B), GELU epilogues, mixed layouts
+from paper_2405_15013_b200 import ks  # noqa: E402
+run((2, 48, 48, 4), "bsl", "tf32", knobs=ks.KNOB_TF32_MN, bias=True)
+run((2, 64, 64, 8), "bsf", knobs=ks.KNOB_FFMA_WS | ks.KNOB_FFMA_WSG | ks.KNOB_FFMA_WSL, bias=True)
+run((2, 64, 64, 2), "bsf", B=24, bias=True)
+run((1, 64, 64, 4), "bsf", "tf32", bias=True, act="gelu")
+run((6, 64, 64, 1), "bsl", bias=True, act="gelu")
+for p, (xl, yl) in [((6, 64, 64, 1), ("bsf", "bsl")), ((1, 64, 256, 16), ("bsl", "bsf")), ((1, 256, 64, 16), ("bsf", "bsl"))]:
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_uniform(*p, seed=11)
+    X = ksgen.x_normal(256, N, seed=12)
+    f = ksb.Factor(*p, K4).set_math(ksb.MATH_TF32)
+    Y = ksb.matmul_io(f, torch.from_numpy(X if xl == "bsf" else ksgen.to_bsl(X)).to(dev), xl, y_layout=yl)
+    torch.cuda.synchronize()
+    Yh = Y.cpu().numpy() if yl == "bsf" else Y.cpu().numpy().T
+    e = O.normwise_error(Yh, O.matmul(p, K4, X))
+    print(f"{p} {xl}->{yl} tf32 err={e:.2e}", flush=True)
+    if e > 5e-3:
+        bad.append((p, xl, yl, e))
 # half precision (kind::f16): BSL swap-AB, BSF d = 1 and J-gather
 for p, lay in [((2, 96, 96, 3), "bsl"), ((1, 64, 64, 1), "bsf"), ((2, 48, 48, 8), "bsf")]:
     M, N, _ = O.dims(p)
