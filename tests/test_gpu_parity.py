@@ -344,7 +344,7 @@ def test_sweep_full_size_sampled_rows(ksb, p, layout):
     check_fp32(Yg[rows], Yref, env, p[2])
 
 
-@pytest.mark.parametrize("name", ["VIT_UP", "GPT2_DOWN"])
+@pytest.mark.parametrize("name", ["VIT_UP", "VIT_DOWN", "GPT2_DOWN", "GPT2_UP"])
 def test_model_chain_full_size_sampled_rows(ksb, name):
     pats = getattr(configs, name)
     B = configs.VIT_BATCH if name.startswith("VIT") else configs.GPT2_BATCH
@@ -354,7 +354,7 @@ def test_model_chain_full_size_sampled_rows(ksb, name):
     fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
     Y = ksb.chain(fs, to_dev(X))
     torch.cuda.synchronize()
-    rows = np.array([0, 1, B // 2, B - 1])
+    rows = np.array([0, 1, 127, 128, B // 2, B - 2, B - 1])
     Yref = O.chain(pats, K4s, X, rows=rows)
     assert O.normwise_error(Y.cpu().numpy()[rows], Yref) <= FP32_TOL
 
