@@ -352,7 +352,10 @@ ks_ffma_wsg_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         const int l0 = (int)(gx % nk) * WS_BK;
         const uint32_t sa = slot0 + st * C::SLOT;
         mbar_expect_tx(full0 + 8 * st, C::A_BYTES + 4 * C::BJ_BYTES);
-        tma_3d(sa, &xmap, j0, i * c + l0, (int)n0, full0 + 8 * st);
+        if (d == 4)          // the 17 l x 4 j of a row are one contiguous run: one 272-byte box row
+            tma_2d(sa, &xmap, (i * c + l0) * 4, (int)n0, full0 + 8 * st);
+        else
+            tma_3d(sa, &xmap, j0, i * c + l0, (int)n0, full0 + 8 * st);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj)
             tma_2d(sa + C::A_BYTES + jj * C::BJ_BYTES, &kmap, k0, (i * d + j0 + jj) * c + l0, full0 + 8 * st);
@@ -505,7 +508,12 @@ cudaError_t launch_wsg(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t kb[2] = {BN, WS_BK};
         if (!encode(&kmap, h.k_tile, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    {
+    if (h.d == 4) {        // d = 4: 2-D box {17 l x 4 j floats, rows} over the contiguous run (same smem image)
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
+        const cuuint32_t xb[2] = {4 * (WS_BK + 1), WSG_BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    } else {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
         const cuuint32_t xb[3] = {4, WS_BK + 1, WSG_BM};
@@ -602,7 +610,10 @@ ks_ffma_wsl_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         const int l0 = (int)(gx % nk) * WS_BK;
         const uint32_t sa = slot0 + st * C::SLOT;
         mbar_expect_tx(full0 + 8 * st, C::A_BYTES + C::B_BYTES);
-        tma_3d(sa, &xmap, j0, i * c + l0, (int)n0, full0 + 8 * st);
+        if (d == 4)          // the 17 l x 4 j of a row are one contiguous run: one 272-byte box row
+            tma_2d(sa, &xmap, (i * c + l0) * 4, (int)n0, full0 + 8 * st);
+        else
+            tma_3d(sa, &xmap, j0, i * c + l0, (int)n0, full0 + 8 * st);
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
             ::"r"(sa + C::A_BYTES), "l"(&kmap), "r"(0), "r"(i * d + j0), "r"(k0 / 8), "r"(l0), "r"(full0 + 8 * st)
@@ -708,7 +719,12 @@ cudaError_t launch_wsl(const ks_handle_s& h, const KsCall& call) {
     using C = WslCfg<NW>;
     constexpr int BN = C::BN;
     CUtensorMap xmap, kmap;
-    {
+    if (h.d == 4) {        // d = 4: 2-D box {17 l x 4 j floats, rows} over the contiguous run (same smem image)
+        const cuuint64_t xd[2] = {(cuuint64_t)h.N, (cuuint64_t)call.B};
+        const cuuint64_t xs[1] = {(cuuint64_t)h.N * 4};
+        const cuuint32_t xb[2] = {4 * (WS_BK + 1), WSL_BM};
+        if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    } else {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
         const cuuint32_t xb[3] = {4, WS_BK + 1, WSL_BM};
