@@ -57,6 +57,7 @@ struct FusedParams {
     int res_pass[2];       // which passes (the TMEM slot is the index in this list)
     int part_pass;         // a third pass whose first two factors live in the last 128 columns, or -1
     int act;               // epilogue activation after the bias (ks_activation_t, NEXT-2)
+    int pf_pass;           // the next group's load is issued after this pass (-1: before the first)
 };
 
 // Weights of one radix-2^T item (T consecutive dyadic factors, b = c = 2, with
@@ -424,11 +425,17 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
     }
     __syncthreads();
     for (int64_t k = 0; k < mine; ++k) {
-        if (threadIdx.x == 0 && k + 1 < mine) {
-            // the other buffer's previous contents (group k-1) must have left for HBM
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            issue_load(k + 1);
-        }
+        // Prefetch of group k+1 into the other buffer, whose previous contents (group
+        // k-1) must have left for HBM first: thread 0 waits for that store's reads
+        // after the second pass of group k (KS_FUSED_PF_PASS), not before it, so the
+        // whole CTA does not idle while the store drains.
+        auto prefetch = [&]() {
+            if (threadIdx.x == 0 && k + 1 < mine) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                issue_load(k + 1);
+            }
+        };
+        if (P.pf_pass < 0) prefetch();
         {
             const uint32_t bar = smem_u32(&full[k & 1]);
             const uint32_t par = (uint32_t)((k >> 1) & 1);
@@ -460,6 +467,7 @@ ks_chain_fused_kernel(const float* __restrict__ X, float* __restrict__ Y, const 
             else if (BB == 2 && len == 2) dyadic_pass<2, SWZ>(sm, rows, N, &P.f[f]);
             else block_pass<BB, SWZ>(sm, rows, N, P.f[f]);
             f += len;
+            if (ps == P.pf_pass) prefetch();
             __syncthreads();
         }
         if (bias || P.act) {                        // KSLinear bias / activation after the last factor (NEXT-2)
@@ -611,6 +619,11 @@ cudaError_t fused_chain_launch(const ks_handle_t* hs, int L, const KsCall& call)
         swz = encode(&xmap, call.X, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B) &&
               encode(&ymap, call.Y, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
+    static const int pf_pass = [] {                 // KS_FUSED_PF_PASS (experiments): -1 = before pass 0
+        const char* e = getenv("KS_FUSED_PF_PASS");
+        return e ? atoi(e) : 1;     // measured (N = 4096, L = 12): -1 111.7 us, 0 / 1 107.5, 2 115.6
+    }();
+    P.pf_pass = pf_pass < P.npass ? pf_pass : P.npass - 1;
     cudaError_t e;
     auto kern = hs[0]->b == 2 ? (swz ? ks_chain_fused_kernel<2, true> : ks_chain_fused_kernel<2, false>)
                               : (swz ? ks_chain_fused_kernel<4, true> : ks_chain_fused_kernel<4, false>);

@@ -83,6 +83,37 @@ def test_fused_fft_full_size_sampled_rows(ksb):
     assert O.normwise_error(Yf[rows], O.chain(pats, K4s, X, rows=rows)) <= 1e-5
 
 
+@pytest.mark.parametrize("L,B", [(12, 1036), (12, 1500), (12, 8191), (11, 2072), (11, 2999), (9, 2100)])
+def test_fused_register_blocked_rows(ksb, L, B):
+    """Enough rows per SM for row groups of 7 / 14 (the register-blocked radix-8
+    passes, chunks of 7 rows): bit-identical to the per-factor launches, with a
+    ragged last group (rows past B are computed on zero fill and not stored)."""
+    pats = configs.dyadic_patterns(L)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    X = ksgen.x_normal(B, 2 ** L, seed=L)
+    Yf, Yu, nl = both(ksb, fs, X)
+    assert nl == 1 and np.array_equal(Yf, Yu)
+    rows = np.array([0, 6, 7, B // 2, B - 1])
+    assert O.normwise_error(Yf[rows], O.chain(pats, K4s, X, rows=rows)) <= 1e-5
+
+
+def test_fused_register_blocked_bias_gelu(ksb):
+    """Bias + GELU epilogue after the register-blocked passes (N = 4096, R = 7)."""
+    L, B = 12, 1500
+    pats = configs.dyadic_patterns(L)
+    K4s = [ksgen.k4_uniform(*p, seed=1000 + l) for l, p in enumerate(pats, 1)]
+    fs = [ksb.Factor(*p, k) for p, k in zip(pats, K4s)]
+    X = ksgen.x_normal(B, 2 ** L, seed=3)
+    bias = ksgen.x_normal(1, 2 ** L, seed=4)[0]
+    ksb.set_chain_fusion(True)
+    Yf = ksb.chain(fs, to_dev(X), bias=to_dev(bias), act="gelu").cpu().numpy()
+    ksb.set_chain_fusion(False)
+    Yu = ksb.chain(fs, to_dev(X), bias=to_dev(bias), act="gelu").cpu().numpy()
+    ksb.set_chain_fusion(True)
+    assert np.array_equal(Yf, Yu)
+
+
 def test_fusion_eligibility(ksb):
     pats = configs.dyadic_patterns(4)
     fs = [ksb.Factor(*p, ksgen.k4_uniform(*p, seed=1)) for p in pats]
