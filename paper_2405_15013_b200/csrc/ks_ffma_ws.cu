@@ -40,9 +40,12 @@ constexpr int WS_THREADS = 32 * WS_CWARPS;
 // tile would leave TN = 3 / 4: 3 shared loads per 32 FFMA instead of 4 per 64).
 // KB = l per chunk: 16, or 32 for BN = 96 tiles when c % 32 == 0 (half the ring
 // waits / refills per FFMA; the BSF A rows become 128 bytes, SWIZZLE_128B).
-template <int LAYOUT, int BN, int KB = WS_BK>
+// WMX > 0 overrides the warps along the rows (WM x WN = 8): fewer rows per tile for
+// problems whose default tiles do not fill the machine (a = d = 1: one b x b block,
+// B / 128 tiles for 2 x 148 CTA slots).
+template <int LAYOUT, int BN, int KB = WS_BK, int WMX = 0>
 struct WsCfg {
-    static constexpr int WM = BN <= 64 ? 4 : 2;            // warps along the batch rows
+    static constexpr int WM = WMX > 0 ? WMX : BN <= 64 ? 4 : 2;   // warps along the batch rows
     static constexpr int WN = 8 / WM;                      // warps along the outputs
     static constexpr int BMW = 64 * WM;                    // batch rows per tile
     static constexpr int TN = BN / (4 * WN);               // outputs per thread
@@ -52,17 +55,18 @@ struct WsCfg {
     static constexpr int S = (108 * 1024) / SLOT > 8 ? 8 : (108 * 1024) / SLOT;
     static constexpr int BAR_OFF = S * SLOT;
     static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;     // full barriers, counters, align pad
-    static_assert(BN == 48 || BN == 64 || BN == 96 || BN == 128, "TN in {6, 8}");
+    static_assert(BN == 48 || BN == 64 || BN == 96 || BN == 128, "BN");
+    static_assert(TN % 2 == 0 && BN % (4 * WN) == 0, "TN even (FFMA2 pairs)");
     static_assert(SLOT % 1024 == 0, "slot alignment (SWIZZLE_64B A tiles)");
     static_assert(S * KB >= 64, "ring depth (l in flight)");
 };
 
-template <int LAYOUT, int BN, int KB = WS_BK>
+template <int LAYOUT, int BN, int KB = WS_BK, int WMX = 0>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                   float* __restrict__ Y, const float* __restrict__ bias, int act, int64_t B, int a, int b, int c, int d,
                   int64_t ntiles) {
-    using C = WsCfg<LAYOUT, BN, KB>;
+    using C = WsCfg<LAYOUT, BN, KB, WMX>;
     constexpr int S = C::S;
     constexpr int TN = C::TN;
     extern __shared__ uint8_t smem_raw[];
@@ -1036,9 +1040,9 @@ cudaError_t launch_wsc_tk(const ks_handle_s& h, const KsCall& call) {
     return cudaErrorInvalidValue;
 }
 
-template <int LAYOUT, int BN, int KB = WS_BK>
+template <int LAYOUT, int BN, int KB = WS_BK, int WMX = 0>
 cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
-    using C = WsCfg<LAYOUT, BN, KB>;
+    using C = WsCfg<LAYOUT, BN, KB, WMX>;
     CUtensorMap xmap, kmap;
     {
         // k_tile: [(i*d + j)*c + l][k], b floats per row
@@ -1059,7 +1063,7 @@ cudaError_t launch_ws(const ks_handle_s& h, const KsCall& call) {
         if (!encode(&xmap, call.X, 2, xd, xs, xb, KB == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
     }
-    auto kern = ks_ffma_ws_kernel<LAYOUT, BN, KB>;
+    auto kern = ks_ffma_ws_kernel<LAYOUT, BN, KB, WMX>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1082,9 +1086,30 @@ int pick_bn_ws(int64_t b) {
     return 0;
 }
 
+// Underfilled launches (fewer default tiles than 2 CTAs x SMs, e.g. a = d = 1 with
+// B = 25088: 196 tiles of 128 rows for 296 slots, the last 48 SMs running two
+// tiles while 100 run one) take tiles of half the rows (BN = 128: 64 x 128,
+// thread micro-tile 8 x 4; BN = 64: 128 x 64): the busiest SM then holds 1.5
+// default tiles' work instead of 2.  KS_FFMA_SPLITM=0 disables (experiments).
+bool ws_split_rows(const ks_handle_s& h, const KsCall& call, int bn) {
+    static const bool on = [] {
+        const char* e = getenv("KS_FFMA_SPLITM");
+        return !(e && atoi(e) == 0);
+    }();
+    if (!on || (bn != 128 && bn != 64)) return false;
+    const int64_t rows = bn == 128 ? 128 : 256;
+    const int64_t tiles = (h.b / bn) * ((call.B + rows - 1) / rows) * (h.a * h.d);
+    int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
+    if (max_grid() > 0) slots = max_grid();
+    return tiles < slots;
+}
+
 template <int LAYOUT, int KB>
 cudaError_t launch_ws_kb(const ks_handle_s& h, const KsCall& call) {
-    switch (pick_bn_ws(h.b)) {
+    const int bn = pick_bn_ws(h.b);
+    if (KB == WS_BK && ws_split_rows(h, call, bn))
+        return bn == 128 ? launch_ws<LAYOUT, 128, KB, 1>(h, call) : launch_ws<LAYOUT, 64, KB, 2>(h, call);
+    switch (bn) {
         case 128: return launch_ws<LAYOUT, 128, KB>(h, call);
         case 96: return launch_ws<LAYOUT, 96, KB>(h, call);
         case 64: return launch_ws<LAYOUT, 64, KB>(h, call);
