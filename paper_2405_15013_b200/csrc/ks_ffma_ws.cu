@@ -1099,9 +1099,7 @@ bool ws_split_rows(const ks_handle_s& h, const KsCall& call, int bn) {
     if (!on || (bn != 128 && bn != 64)) return false;
     const int64_t rows = bn == 128 ? 128 : 256;
     const int64_t tiles = (h.b / bn) * ((call.B + rows - 1) / rows) * (h.a * h.d);
-    int64_t slots = 2 * (int64_t)ks::num_sms(h.device);
-    if (max_grid() > 0) slots = max_grid();
-    return tiles < slots;
+    return tiles < 2 * (int64_t)ks::num_sms(h.device);   // (not the KS_TF32_MAXGRID test cap: the shape stays)
 }
 
 template <int LAYOUT, int KB>
