@@ -416,8 +416,13 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 // batch values is 512 contiguous bytes: no gather), and the transposers read
 // it with conflict-free 4-byte loads.  OUTL = BSL: the epilogue writes each
 // output row r = (i, k, j) of Y^T as 128-byte warp stores (lane = batch row).
+// TST (BSF out): the epilogue stages each warp's 32-row x EC-output x J chunk in a
+// dense box buffer (one per warp, <= warp_store_rows' scratch) and stores it with one TMA tensor store
+// (cp.async.bulk.tensor shared -> global), instead of warp_store_rows' 16-byte
+// warp stores: the d-strided 16/32-byte runs of Y are written by the TMA engine
+// and the epilogue warps move on to the next chunk (SURVEY 8a-6 "TMA store").
 template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false, int INL = KS_LAYOUT_BSF,
-          int OUTL = KS_LAYOUT_BSF>
+          int OUTL = KS_LAYOUT_BSF, bool TST = false>
 struct Tf32JCfg {
     static constexpr int RB = BKJ * 4;                    // operand row bytes (SW32 / SW64)
     static constexpr int NA = X3 ? 2 : 1;                 // hi (+ lo) tiles
@@ -430,7 +435,8 @@ struct Tf32JCfg {
     static constexpr int STG = BM * STG_ROW;
     static constexpr int NACC = 2 * J * BN <= 512 ? 2 : 1;
     static constexpr int EC = J > 2 ? 8 : 16;             // epilogue columns per TMEM load
-    static constexpr int SCR = OUTL == KS_LAYOUT_BSL ? 0 : 4 * WarpStore<float, J, EC>::BYTES;    // store scratch
+    static constexpr int TBOX = 32 * EC * J * 4;                        // TMA store box (TST), 1 KB multiple
+    static constexpr int SCR = OUTL == KS_LAYOUT_BSL ? 0 : TST ? 4 * TBOX : 4 * WarpStore<float, J, EC>::BYTES;
     // X staging ring: ~96 KB of X loads in flight per SM (Little's law: ~45 GB/s
     // per SM x ~2 us loaded latency), leaving room for 2 operand slots; measured:
     // P = 2 at BKJ = 8 (36 KB in flight) left the J = 3 kernel latency-bound.
@@ -440,12 +446,13 @@ struct Tf32JCfg {
     static constexpr int P = P_MIN < 2 ? 2 : P_MIN > 8 ? 8 : P_MIN;
     static constexpr int S_FIT = (214 * 1024 - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 6 ? 6 : S_FIT;
-    static constexpr int SCR_OFF = S * SLOT + P * STG;
+    static constexpr int SCR_OFF = (S * SLOT + P * STG + 1023) / 1024 * 1024;   // TMA store boxes: 1 KB aligned
     static constexpr int BAR_OFF = SCR_OFF + SCR;
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
     static constexpr int COLS = NACC * J * BN;
     static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
     static_assert(SMEM <= 227 * 1024, "shared memory");
+    static_assert(!TST || (OUTL == KS_LAYOUT_BSF && J == 8 && TBOX % 1024 == 0), "TMA store boxes");
     static_assert(J * BN <= 512 && BN % 16 == 0 && BN <= 256, "J accumulators in TMEM");
     static_assert(BKJ == 8 || BKJ == 16, "SW32 / SW64 operand rows");
     static_assert((BKJ * J) % 4 == 0, "whole 16-byte staging reads");
@@ -475,15 +482,16 @@ __device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_
 }
 
 template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false, int INL = KS_LAYOUT_BSF,
-          int OUTL = KS_LAYOUT_BSF>
+          int OUTL = KS_LAYOUT_BSF, bool TST = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                    const __grid_constant__ CUtensorMap kmap_lo, float* __restrict__ Y,
+                    const __grid_constant__ CUtensorMap kmap_lo, const __grid_constant__ CUtensorMap ymap,
+                    float* __restrict__ Y,
                     const float* __restrict__ bias, int64_t B, int a, int b, int c, int d, int64_t ntiles,
                     int flags) {
     // flags: bits 0-7 = KS_TF32_DEBUG experiment switches, bits 8-15 = epilogue activation
     const int dbg = flags & 0xFF, act = (flags >> 8) & 0xFF;
-    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL>;
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL, TST>;
     static_assert(INL == KS_LAYOUT_BSF || !GATHER, "BSL input needs no gather");
     constexpr int S = C::S;
     constexpr int P = C::P;
@@ -512,6 +520,23 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     const int lane = tid & 31;
     const int nkc = b / BN;
     const int njg = d / J;
+    // KS_TF32_DEBUG bit 3 (profiling only, results overwritten): per-role clock64
+    // barrier-wait counters written over Y[blockIdx.x * 32 ..] at the end
+    // (scripts/prof_roles.py)
+    const bool prof = dbg & 8;
+    __shared__ unsigned long long pc[16];
+    if (prof && tid < 16) pc[tid] = 0;
+    unsigned long long w0 = 0, w1 = 0;
+    const unsigned long long tk0 = clock64();
+    auto pwait = [&](uint32_t bar, uint32_t par, unsigned long long& acc) {
+        if (prof) {
+            const unsigned long long t0 = clock64();
+            mbar_wait(bar, par);
+            acc += clock64() - t0;
+        } else {
+            mbar_wait(bar, par);
+        }
+    };
     const int64_t nnb = (B + BM - 1) / BM;
     const int64_t M = (int64_t)a * b * d;
     const int nk = c / BKJ;                       // c % BKJ == 0
@@ -554,7 +579,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 const TileJ tc = decode_j(blockIdx.x + (gx / nk) * gridDim.x, nkc, njg, nnb, BN, J);
                 const int l0 = (int)(gx % nk) * BKJ;
                 const int p = (int)(gx % P);
-                if (gx >= P) mbar_wait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1));
+                if (gx >= P) pwait(sempty0 + 8 * p, (uint32_t)(((gx / P) - 1) & 1), w0);
                 mbar_expect_tx(sfull0 + 8 * p, C::STG);
                 if constexpr (INL == KS_LAYOUT_BSL)
                     tma_3d(stg0 + p * C::STG, &xmap, tc.n0, tc.j0, tc.i * c + l0, sfull0 + 8 * p);
@@ -569,7 +594,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
                 const int l0 = (int)(g % nk) * BKJ;
                 const int st = (int)(g % S);
-                if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+                if (g >= S) pwait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1), w1);
                 mbar_expect_tx(full0 + 8 * st, J * C::NA * C::BJ_TILE);
                 const uint32_t sb = slot0 + st * C::SLOT + A_ALL;
                 for (int jj = 0; jj < J; ++jj) {
@@ -586,7 +611,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         const int sw = RB == 64 ? (r % 8) / 2 : (r % 8) / 4;       // SW64 / SW32 chunk XOR
         for (int64_t g = 0; g < G; ++g) {
             const int p = (int)(g % P);
-            mbar_wait(sfull0 + 8 * p, (uint32_t)((g / P) & 1));
+            pwait(sfull0 + 8 * p, (uint32_t)((g / P) & 1), w0);
             float v[BKJ * J];                     // v[l * J + j]
             const uint32_t src = stg0 + p * C::STG + r * C::STG_ROW;
             if (dbg & 2) {                // profiling experiment: skip the staging reads
@@ -605,7 +630,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             fence_proxy_async();          // generic reads before the TMA (async proxy) refill
             mbar_arrive(sempty0 + 8 * p);
             const int st = (int)(g % S);
-            if (g >= S) mbar_wait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1));
+            if (g >= S) pwait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1), w1);
             const uint32_t sa = slot0 + st * C::SLOT + rowoff;
 #pragma unroll
             for (int jj = 0; jj < J; ++jj)
@@ -637,11 +662,11 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             int64_t g = 0, it = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int ab = (int)(it % NACC);
-                if (it >= NACC) mbar_wait(acce0 + 8 * ab, (uint32_t)(((it / NACC) - 1) & 1));
+                if (it >= NACC) pwait(acce0 + 8 * ab, (uint32_t)(((it / NACC) - 1) & 1), w0);
                 tc_fence_after();
                 for (int t = 0; t < nk; ++t, ++g) {
                     const int st = (int)(g % S);
-                    mbar_wait(full0 + 8 * st, (uint32_t)((g / S) & 1));
+                    pwait(full0 + 8 * st, (uint32_t)((g / S) & 1), w1);
                     tc_fence_after();
                     const uint32_t sa = slot0 + st * C::SLOT;
                     const uint32_t sb = sa + A_ALL;
@@ -674,7 +699,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const TileJ tc = decode_j(tile, nkc, njg, nnb, BN, J);
             const int ab = (int)(it % NACC);
-            mbar_wait(accf0 + 8 * ab, (uint32_t)((it / NACC) & 1));
+            pwait(accf0 + 8 * ab, (uint32_t)((it / NACC) & 1), w0);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * J * BN);
 #pragma unroll 1
@@ -712,6 +737,49 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     }
                 } else if ((dbg & 4) && (J == d || J % 4 == 0)) {   // experiment: direct stores
                     direct_store_rows<J, EC>(v, Y, (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
+                } else if constexpr (TST) {
+                    // box buffer of this warp: [32 n][EC k][J j] floats, dense (SWIZZLE_NONE:
+                    // a 128-byte-swizzled box with 16-byte rows faults in the TMA unit).  Lane n's
+                    // row is NU 16-byte chunks at n * ROWB, ROWB a multiple of 128 bytes, so chunk u of
+                    // every lane would hit the same 4 banks: lane n writes chunk (u + n) mod NU at step
+                    // u (8 lanes of a phase on 8 bank groups), its chunks rotated by n mod 8 in
+                    // registers first (3 conditional rotations, no dynamic register indexing).
+                    // The previous chunk's store must have read the buffer.
+                    constexpr int NU = EC * J / 4;
+                    static_assert(NU % 8 == 0, "rows of whole 128-byte bank sweeps");
+                    const uint32_t buf = scr0 + (uint32_t)(warp - 6) * C::TBOX;
+                    float w[NU][4];
+#pragma unroll
+                    for (int u = 0; u < NU; ++u)
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) w[u][x] = v[(u * 4 + x) % J][(u * 4 + x) / J];
+                    const int rot = lane & 7;
+#pragma unroll
+                    for (int sb = 1; sb < 8; sb <<= 1) {
+                        const bool on = rot & sb;
+                        float t[NU][4];
+#pragma unroll
+                        for (int u = 0; u < NU; ++u)
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) t[u][x] = on ? w[(u + sb) % NU][x] : w[u][x];
+#pragma unroll
+                        for (int u = 0; u < NU; ++u)
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) w[u][x] = t[u][x];
+                    }
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < NU; ++u) {
+                        const uint32_t c = (uint32_t)((u + rot) % NU);
+                        sts128(buf + (uint32_t)lane * (NU * 16) + c * 16, w[u][0], w[u][1], w[u][2], w[u][3]);
+                    }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0 && !(dbg & 1)) {     // Y viewed [B][a b][d]: box {J j, EC k, 32 n}
+                        tma_store_3d(&ymap, tc.j0, (int)(r0 / d), tc.n0 + lq * 32, buf);
+                        bulk_commit();
+                    }
                 } else if (!(dbg & 1)) {          // profiling experiment: skip the stores
                     warp_store_rows<float, J, EC>(scr0 + (uint32_t)(warp - 6) * WarpStore<float, J, EC>::BYTES, v, Y,
                                                   (int64_t)tc.n0 + lq * 32, B, M, r0, d, lane);
@@ -719,8 +787,19 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             }
         }
     }
+    if constexpr (TST) {
+        if (warp >= 6 && lane == 0) bulk_wait_all();     // this thread's TMA stores have completed
+    }
+    if (prof) {       // [0,1] producer (sempty, empty) [2,3] transposer 0 (sfull, empty) [4,5] MMA (acce, full)
+        const unsigned long long tot = clock64() - tk0;      // [6] epilogue warp 6 (accf); [8..11] role run times
+        if (tid == 0) { pc[0] = w0; pc[1] = w1; pc[8] = tot; }
+        if (tid == 32) { pc[2] = w0; pc[3] = w1; pc[9] = tot; }
+        if (tid == 160) { pc[4] = w0; pc[5] = w1; pc[10] = tot; }
+        if (tid == 192) { pc[6] = w0; pc[11] = tot; }
+    }
     tc_fence_before();
     __syncthreads();
+    if (prof && tid < 16) reinterpret_cast<unsigned long long*>(Y)[blockIdx.x * 16 + tid] = pc[tid];
     if (warp == 5) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
@@ -1108,8 +1187,12 @@ struct BsfjPlan {
 // (scripts/probe_tma_gather.cu); BN then halves (J x BN <= 512 TMEM columns) and the
 // b / BN output chunks of one X tile run on adjacent CTAs at the same time (L2 hits).
 // 3xTF32 doubles every operand tile: J <= 4 there (d = 6 runs FFMA).
-BsfjPlan pick_bsfj(const ks_handle_s& h, uint32_t knobs) {
+// bsl_out (mixed BSF-in / BSL-out calls): Y's rows are 512-byte runs whatever J is,
+// so the J8 knob's 32-byte runs buy nothing there while halving BN doubles the X
+// re-reads: (1,256,64,16) BSF -> BSL J = 4 320 us, J = 8 424 us (profiles/r03/tst2_j8.jsonl).
+BsfjPlan pick_bsfj(const ks_handle_s& h, uint32_t knobs, bool bsl_out = false) {
     BsfjPlan p;
+    if (bsl_out) knobs &= ~(uint32_t)KS_KNOB_J8;
     const bool x3 = h.math == KS_MATH_F32X3;
     if (h.c % 16 != 0) return p;
     if (h.d >= 2 && h.d <= (x3 ? 4 : 8) && h.d != 5 && h.d != 7) {
@@ -1173,10 +1256,33 @@ constexpr int bsfj_bkj() {
     return 214 * 1024 - p16 * stg16 - scr >= 2 * slot16 ? 16 : 8;
 }
 
+// TMA-store epilogue (TST) for J = 8 (32-byte runs of Y, d % 8 == 0; Y viewed
+// [B][a b][d]): measured over the configs[2] sweep, J = 8 tiles 1.05-1.20x faster
+// with it, J = 4 tiles (16-byte runs) 0.68-0.94x -- there the 16-byte warp stores
+// of warp_store_rows stay (profiles/r03/tst_time.jsonl).  KS_TF32_TMASTORE=0
+// disables (experiments).
+bool bsfj_tst_on() {
+    static const bool on = [] {
+        const char* e = getenv("KS_TF32_TMASTORE");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+template <int J, int BN, bool X3, bool GATHER, int INL, int OUTL, bool TST>
+cudaError_t launch_bsfj_t(const ks_handle_s& h, const KsCall& call);
+
 template <int J, int BN, bool X3, bool GATHER, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
+    if constexpr (OUTL == KS_LAYOUT_BSF && J == 8)
+        if (bsfj_tst_on()) return launch_bsfj_t<J, BN, X3, GATHER, INL, OUTL, true>(h, call);
+    return launch_bsfj_t<J, BN, X3, GATHER, INL, OUTL, false>(h, call);
+}
+
+template <int J, int BN, bool X3, bool GATHER, int INL, int OUTL, bool TST>
+cudaError_t launch_bsfj_t(const ks_handle_s& h, const KsCall& call) {
     constexpr int BKJ = bsfj_bkj<J, BN, X3, GATHER, INL, OUTL>();
-    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL>;
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL, TST>;
     constexpr CUtensorMapSwizzle SW = C::RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUtensorMap xmap, kmap, kmap_lo;
     {
@@ -1203,7 +1309,15 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t xb[2] = {(cuuint32_t)(BKJ * J + 4), BM};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER, INL, OUTL>;
+    CUtensorMap ymap{};
+    if constexpr (TST) {
+        const int64_t M = h.a * h.b * h.d;           // Y viewed [B][a b][d] (d % 8 == 0)
+        const cuuint64_t yd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.b), (cuuint64_t)call.B};
+        const cuuint64_t ys[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)M * 4};
+        const cuuint32_t yb[3] = {(cuuint32_t)J, (cuuint32_t)C::EC, 32};
+        if (!encode(&ymap, call.Y, 3, yd, ys, yb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER, INL, OUTL, TST>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1215,8 +1329,8 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
-                                         kmap_lo, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d,
-                                         ntiles, debug_flags() | (call.act << 8));
+                                         kmap_lo, ymap, call.Y, call.bias, call.B, (int)h.a, (int)h.b, (int)h.c,
+                                         (int)h.d, ntiles, debug_flags() | (call.act << 8));
     ks::count_launch();
     return e;
 }
@@ -1238,7 +1352,8 @@ cudaError_t launch_bsfj_bn(const ks_handle_s& h, const KsCall& call, int BN) {
 // INL / OUTL: BSF / BSF (X3 or TF32), BSF / BSL or BSL / BSF (TF32 mixed-layout calls)
 template <bool X3, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
-    const BsfjPlan p = INL == KS_LAYOUT_BSL ? pick_bslj(h, call.knobs) : pick_bsfj(h, call.knobs);
+    const BsfjPlan p = INL == KS_LAYOUT_BSL ? pick_bslj(h, call.knobs)
+                                            : pick_bsfj(h, call.knobs, OUTL == KS_LAYOUT_BSL);
     if constexpr (INL == KS_LAYOUT_BSF) {
         if (p.gather) {
             if (p.J == 4) return launch_bsfj_bn<4, X3, true, INL, OUTL>(h, call, p.BN);
