@@ -10,6 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 INC = os.path.join(ROOT, "paper_2405_15013_b200", "csrc", "ks_presets.inc")
 # the table is generated from these records; later ones replace earlier rows with the same key
 JSNS = [os.path.join(ROOT, "profiles", "r02", n) for n in ("autotune.json", "autotune_tf32_bsl.json", "autotune_fp32_bsf.json")]
+JSNS.append(os.path.join(ROOT, "profiles", "r03", "autotune_tf32_bsf.json"))   # TF32 BSF re-tune after the TMA-store epilogue
 
 
 def _rows():
