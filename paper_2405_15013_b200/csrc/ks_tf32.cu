@@ -421,10 +421,15 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 // (cp.async.bulk.tensor shared -> global), instead of warp_store_rows' 16-byte
 // warp stores: the d-strided 16/32-byte runs of Y are written by the TMA engine
 // and the epilogue warps move on to the next chunk (SURVEY 8a-6 "TMA store").
+// MNJ (BSL in, FP32 TF32): each j's A tile [32 l][128 n] arrives MN-major straight
+// from TMA (4 boxes {32 n, 1 j, 32 l}, SWIZZLE_128B_ATOM_32B, as the d = 1 kernel's
+// MNA) -- no staging ring, no transposer warps: the whole ring is operand slots,
+// so X in flight is S - 1 stages of J x 16 KB instead of one 32 KB staging chunk
+// (the transposers of the staged kernel waited for X half of their time).  BKJ = 32.
 template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false, int INL = KS_LAYOUT_BSF,
-          int OUTL = KS_LAYOUT_BSF, bool TST = false>
+          int OUTL = KS_LAYOUT_BSF, bool TST = false, bool MNJ = false>
 struct Tf32JCfg {
-    static constexpr int RB = BKJ * 4;                    // operand row bytes (SW32 / SW64)
+    static constexpr int RB = BKJ * 4;                    // operand row bytes (SW32 / SW64; SW128 for MNJ)
     static constexpr int NA = X3 ? 2 : 1;                 // hi (+ lo) tiles
     static constexpr int AJ_TILE = BM * RB;               // per j
     static constexpr int BJ_TILE = BN * RB;
@@ -432,7 +437,7 @@ struct Tf32JCfg {
     // staged row: [BKJ l][J j] + padding: 4 floats past the run (2-D box), or one
     // more l (3-D box; J = 8 then gives an even pitch: 2-way read conflicts)
     static constexpr int STG_ROW = INL == KS_LAYOUT_BSL ? BKJ * J * 4 : GATHER ? (BKJ + 1) * J * 4 : BKJ * J * 4 + 16;
-    static constexpr int STG = BM * STG_ROW;
+    static constexpr int STG = MNJ ? 0 : BM * STG_ROW;
     static constexpr int NACC = 2 * J * BN <= 512 ? 2 : 1;
     static constexpr int EC = J > 2 ? 8 : 16;             // epilogue columns per TMEM load
     static constexpr int TBOX = 32 * EC * J * 4;                        // TMA store box (TST), 1 KB multiple
@@ -440,10 +445,10 @@ struct Tf32JCfg {
     // X staging ring: ~96 KB of X loads in flight per SM (Little's law: ~45 GB/s
     // per SM x ~2 us loaded latency), leaving room for 2 operand slots; measured:
     // P = 2 at BKJ = 8 (36 KB in flight) left the J = 3 kernel latency-bound.
-    static constexpr int P_WANT = (96 * 1024 + STG - 1) / STG;
-    static constexpr int P_ROOM = (214 * 1024 - 2 * SLOT - SCR) / STG;
+    static constexpr int P_WANT = MNJ ? 1 : (96 * 1024 + STG - 1) / STG;
+    static constexpr int P_ROOM = MNJ ? 1 : (214 * 1024 - 2 * SLOT - SCR) / STG;
     static constexpr int P_MIN = P_WANT < P_ROOM ? P_WANT : P_ROOM;
-    static constexpr int P = P_MIN < 2 ? 2 : P_MIN > 8 ? 8 : P_MIN;
+    static constexpr int P = MNJ ? 1 : P_MIN < 2 ? 2 : P_MIN > 8 ? 8 : P_MIN;   // (MNJ: barriers only)
     static constexpr int S_FIT = (214 * 1024 - P * STG - SCR) / SLOT;
     static constexpr int S = S_FIT > 6 ? 6 : S_FIT;
     static constexpr int SCR_OFF = (S * SLOT + P * STG + 1023) / 1024 * 1024;   // TMA store boxes: 1 KB aligned
@@ -454,7 +459,7 @@ struct Tf32JCfg {
     static_assert(SMEM <= 227 * 1024, "shared memory");
     static_assert(!TST || (OUTL == KS_LAYOUT_BSF && J == 8 && TBOX % 1024 == 0), "TMA store boxes");
     static_assert(J * BN <= 512 && BN % 16 == 0 && BN <= 256, "J accumulators in TMEM");
-    static_assert(BKJ == 8 || BKJ == 16, "SW32 / SW64 operand rows");
+    static_assert(MNJ ? (BKJ == 32 && INL == KS_LAYOUT_BSL && !X3) : (BKJ == 8 || BKJ == 16), "operand rows");
     static_assert((BKJ * J) % 4 == 0, "whole 16-byte staging reads");
     static_assert(S >= 2, "pipeline too shallow");
     static_assert((2 * S + 2 * NACC + 2 * P) * 8 + 4 <= 256, "barrier area");
@@ -462,7 +467,8 @@ struct Tf32JCfg {
 
 template <int RB>
 __device__ __forceinline__ uint64_t kmajor_desc_j(uint32_t addr) {
-    if constexpr (RB == 64) return sw64_desc(addr);
+    if constexpr (RB == 128) return sw128_desc(addr);
+    else if constexpr (RB == 64) return sw64_desc(addr);
     else return sw32_desc(addr);
 }
 
@@ -482,7 +488,7 @@ __device__ __forceinline__ TileJ decode_j(int64_t tile, int nkc, int njg, int64_
 }
 
 template <int J, int BN, int BKJ, bool X3 = false, bool GATHER = false, int INL = KS_LAYOUT_BSF,
-          int OUTL = KS_LAYOUT_BSF, bool TST = false>
+          int OUTL = KS_LAYOUT_BSF, bool TST = false, bool MNJ = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                     const __grid_constant__ CUtensorMap kmap_lo, const __grid_constant__ CUtensorMap ymap,
@@ -491,7 +497,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                     int flags) {
     // flags: bits 0-7 = KS_TF32_DEBUG experiment switches, bits 8-15 = epilogue activation
     const int dbg = flags & 0xFF, act = (flags >> 8) & 0xFF;
-    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL, TST>;
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL, TST, MNJ>;
     static_assert(INL == KS_LAYOUT_BSF || !GATHER, "BSL input needs no gather");
     constexpr int S = C::S;
     constexpr int P = C::P;
@@ -545,7 +551,7 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, 1 + NTRANS);
+            mbar_init(full0 + 8 * s, MNJ ? 2 : 1 + NTRANS);      // MNJ: the two expect_tx arrivals (B, A)
             mbar_init(empty0 + 8 * s, 1);
         }
         for (int s = 0; s < NACC; ++s) {
@@ -588,14 +594,25 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                 else
                     tma_2d(stg0 + p * C::STG, &xmap, (tc.i * c + l0) * d, tc.n0, sfull0 + 8 * p);
             };
-            for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
+            if constexpr (!MNJ)
+                for (int64_t gx = 0; gx < P - 1 && gx < G; ++gx) issue_x(gx);
             for (int64_t g = 0; g < G; ++g) {
-                if (g + P - 1 < G) issue_x(g + P - 1);
+                if constexpr (!MNJ)
+                    if (g + P - 1 < G) issue_x(g + P - 1);
                 const TileJ tc = decode_j(blockIdx.x + (g / nk) * gridDim.x, nkc, njg, nnb, BN, J);
                 const int l0 = (int)(g % nk) * BKJ;
                 const int st = (int)(g % S);
                 if (g >= S) pwait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1), w1);
                 mbar_expect_tx(full0 + 8 * st, J * C::NA * C::BJ_TILE);
+                if constexpr (MNJ) {      // A of each j: 4 boxes of 32 batch columns x 32 l, MN-major
+                    mbar_expect_tx(full0 + 8 * st, A_ALL);
+                    const uint32_t sa = slot0 + st * C::SLOT;
+                    for (int jj = 0; jj < J; ++jj)
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4)
+                            tma_3d(sa + jj * C::AJ_TILE + q4 * 4096, &xmap, tc.n0 + 32 * q4, tc.j0 + jj,
+                                   tc.i * c + l0, full0 + 8 * st);
+                }
                 const uint32_t sb = slot0 + st * C::SLOT + A_ALL;
                 for (int jj = 0; jj < J; ++jj) {
                     const int row = ((tc.i * d + tc.j0 + jj) * b) + tc.k0;
@@ -605,60 +622,62 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             }
         }
     } else if (warp <= 4) {
-        // staging row r: [BKJ l][J j] floats -> J K-major A rows of BKJ l (+ J lo rows for X3)
-        const int r = tid - 32;
-        const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
-        const int sw = RB == 64 ? (r % 8) / 2 : (r % 8) / 4;       // SW64 / SW32 chunk XOR
-        for (int64_t g = 0; g < G; ++g) {
-            const int p = (int)(g % P);
-            pwait(sfull0 + 8 * p, (uint32_t)((g / P) & 1), w0);
-            float v[BKJ * J];                     // v[l * J + j]
-            const uint32_t src = stg0 + p * C::STG + r * C::STG_ROW;
-            if (dbg & 2) {                // profiling experiment: skip the staging reads
-#pragma unroll
-                for (int q = 0; q < 4 * NV; ++q) v[q] = 0.f;
-            } else if constexpr (INL == KS_LAYOUT_BSL) {   // staged [l][j][n]: column r
-#pragma unroll
-                for (int q = 0; q < BKJ * J; ++q) v[q] = lds32(stg0 + p * C::STG + (uint32_t)(q * BM + r) * 4);
-            } else {
-#pragma unroll
-                for (int q = 0; q < NV; ++q)
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
-                                 : "r"(src + q * 16));
-            }
-            fence_proxy_async();          // generic reads before the TMA (async proxy) refill
-            mbar_arrive(sempty0 + 8 * p);
-            const int st = (int)(g % S);
-            if (g >= S) pwait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1), w1);
-            const uint32_t sa = slot0 + st * C::SLOT + rowoff;
-#pragma unroll
-            for (int jj = 0; jj < J; ++jj)
-#pragma unroll
-                for (int ch = 0; ch < NCH; ++ch) {
-                    const uint32_t off = jj * C::AJ_TILE + ((ch ^ sw) * 16);
-                    const float x0 = v[(4 * ch) * J + jj], x1 = v[(4 * ch + 1) * J + jj];
-                    const float x2 = v[(4 * ch + 2) * J + jj], x3 = v[(4 * ch + 3) * J + jj];
-                    if constexpr (X3) {
-                        uint32_t hi[4], lo[4];
-                        tf32_split(__float_as_uint(x0), hi[0], lo[0]);
-                        tf32_split(__float_as_uint(x1), hi[1], lo[1]);
-                        tf32_split(__float_as_uint(x2), hi[2], lo[2]);
-                        tf32_split(__float_as_uint(x3), hi[3], lo[3]);
-                        sts128(sa + off, __uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(hi[2]),
-                               __uint_as_float(hi[3]));
-                        sts128(sa + J * C::AJ_TILE + off, __uint_as_float(lo[0]), __uint_as_float(lo[1]),
-                               __uint_as_float(lo[2]), __uint_as_float(lo[3]));
-                    } else {
-                        sts128(sa + off, x0, x1, x2, x3);
-                    }
+        if constexpr (!MNJ) {     // (MNJ: no staging, A arrives MN-major)
+            // staging row r: [BKJ l][J j] floats -> J K-major A rows of BKJ l (+ J lo rows for X3)
+            const int r = tid - 32;
+            const uint32_t rowoff = (uint32_t)((r / 8) * (8 * RB) + (r % 8) * RB);
+            const int sw = RB == 64 ? (r % 8) / 2 : (r % 8) / 4;       // SW64 / SW32 chunk XOR
+            for (int64_t g = 0; g < G; ++g) {
+                const int p = (int)(g % P);
+                pwait(sfull0 + 8 * p, (uint32_t)((g / P) & 1), w0);
+                float v[BKJ * J];                     // v[l * J + j]
+                const uint32_t src = stg0 + p * C::STG + r * C::STG_ROW;
+                if (dbg & 2) {                // profiling experiment: skip the staging reads
+    #pragma unroll
+                    for (int q = 0; q < 4 * NV; ++q) v[q] = 0.f;
+                } else if constexpr (INL == KS_LAYOUT_BSL) {   // staged [l][j][n]: column r
+    #pragma unroll
+                    for (int q = 0; q < BKJ * J; ++q) v[q] = lds32(stg0 + p * C::STG + (uint32_t)(q * BM + r) * 4);
+                } else {
+    #pragma unroll
+                    for (int q = 0; q < NV; ++q)
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                                     : "r"(src + q * 16));
                 }
-            fence_proxy_async();
-            mbar_arrive(full0 + 8 * st);
+                fence_proxy_async();          // generic reads before the TMA (async proxy) refill
+                mbar_arrive(sempty0 + 8 * p);
+                const int st = (int)(g % S);
+                if (g >= S) pwait(empty0 + 8 * st, (uint32_t)(((g / S) - 1) & 1), w1);
+                const uint32_t sa = slot0 + st * C::SLOT + rowoff;
+    #pragma unroll
+                for (int jj = 0; jj < J; ++jj)
+    #pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) {
+                        const uint32_t off = jj * C::AJ_TILE + ((ch ^ sw) * 16);
+                        const float x0 = v[(4 * ch) * J + jj], x1 = v[(4 * ch + 1) * J + jj];
+                        const float x2 = v[(4 * ch + 2) * J + jj], x3 = v[(4 * ch + 3) * J + jj];
+                        if constexpr (X3) {
+                            uint32_t hi[4], lo[4];
+                            tf32_split(__float_as_uint(x0), hi[0], lo[0]);
+                            tf32_split(__float_as_uint(x1), hi[1], lo[1]);
+                            tf32_split(__float_as_uint(x2), hi[2], lo[2]);
+                            tf32_split(__float_as_uint(x3), hi[3], lo[3]);
+                            sts128(sa + off, __uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(hi[2]),
+                                   __uint_as_float(hi[3]));
+                            sts128(sa + J * C::AJ_TILE + off, __uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                                   __uint_as_float(lo[2]), __uint_as_float(lo[3]));
+                        } else {
+                            sts128(sa + off, x0, x1, x2, x3);
+                        }
+                    }
+                fence_proxy_async();
+                mbar_arrive(full0 + 8 * st);
+            }
         }
     } else if (warp == 5) {
         if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(BN);
+            constexpr uint32_t idesc = make_idesc(BN) | (MNJ ? 1u << 15 : 0u);   // bit 15: A MN-major
             int64_t g = 0, it = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int ab = (int)(it % NACC);
@@ -681,6 +700,9 @@ ks_tf32_bsfj_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
                                 mma_tf32(dtm, kmajor_desc_j<RB>(ah + J * C::AJ_TILE), kmajor_desc_j<RB>(bh), idesc, acc);
                                 mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh + J * C::BJ_TILE), idesc, 1u);
                                 mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh), idesc, 1u);
+                            } else if constexpr (MNJ) {   // k-step s = l rows 8s.. of each 32-l box; boxes 4 KB apart
+                                mma_tf32(dtm, mn_sw128_32b_desc(sa + jj * C::AJ_TILE + 1024 * s, 4096, 512),
+                                         kmajor_desc_j<RB>(bh), idesc, acc);
                             } else {
                                 mma_tf32(dtm, kmajor_desc_j<RB>(ah), kmajor_desc_j<RB>(bh), idesc, acc);
                             }
@@ -1269,7 +1291,7 @@ bool bsfj_tst_on() {
     return on;
 }
 
-template <int J, int BN, bool X3, bool GATHER, int INL, int OUTL, bool TST>
+template <int J, int BN, bool X3, bool GATHER, int INL, int OUTL, bool TST, bool MNJ = false>
 cudaError_t launch_bsfj_t(const ks_handle_s& h, const KsCall& call);
 
 template <int J, int BN, bool X3, bool GATHER, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
@@ -1279,11 +1301,12 @@ cudaError_t launch_bsfj(const ks_handle_s& h, const KsCall& call) {
     return launch_bsfj_t<J, BN, X3, GATHER, INL, OUTL, false>(h, call);
 }
 
-template <int J, int BN, bool X3, bool GATHER, int INL, int OUTL, bool TST>
+template <int J, int BN, bool X3, bool GATHER, int INL, int OUTL, bool TST, bool MNJ>
 cudaError_t launch_bsfj_t(const ks_handle_s& h, const KsCall& call) {
-    constexpr int BKJ = bsfj_bkj<J, BN, X3, GATHER, INL, OUTL>();
-    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL, TST>;
-    constexpr CUtensorMapSwizzle SW = C::RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    constexpr int BKJ = MNJ ? 32 : bsfj_bkj<J, BN, X3, GATHER, INL, OUTL>();
+    using C = Tf32JCfg<J, BN, BKJ, X3, GATHER, INL, OUTL, TST, MNJ>;
+    constexpr CUtensorMapSwizzle SW = C::RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                    : C::RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUtensorMap xmap, kmap, kmap_lo;
     {
         const cuuint64_t kd[2] = {(cuuint64_t)h.c, (cuuint64_t)(h.a * h.d * h.b)};
@@ -1296,8 +1319,13 @@ cudaError_t launch_bsfj_t(const ks_handle_s& h, const KsCall& call) {
     if (INL == KS_LAYOUT_BSL) {
         const cuuint64_t xd[3] = {(cuuint64_t)call.B, (cuuint64_t)h.d, (cuuint64_t)(h.a * h.c)};
         const cuuint64_t xs[2] = {(cuuint64_t)call.B * 4, (cuuint64_t)(h.d * call.B) * 4};
-        const cuuint32_t xb[3] = {BM, (cuuint32_t)J, (cuuint32_t)BKJ};
-        if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+        if constexpr (MNJ) {               // {32 n, 1 j, 32 l} boxes, MN-major operand atoms
+            const cuuint32_t xb[3] = {32, 1, 32};
+            if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+        } else {
+            const cuuint32_t xb[3] = {BM, (cuuint32_t)J, (cuuint32_t)BKJ};
+            if (!encode(&xmap, call.X, 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+        }
     } else if (GATHER) {
         const cuuint64_t xd[3] = {(cuuint64_t)h.d, (cuuint64_t)(h.a * h.c), (cuuint64_t)call.B};
         const cuuint64_t xs[2] = {(cuuint64_t)h.d * 4, (cuuint64_t)h.N * 4};
@@ -1317,7 +1345,7 @@ cudaError_t launch_bsfj_t(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t yb[3] = {(cuuint32_t)J, (cuuint32_t)C::EC, 32};
         if (!encode(&ymap, call.Y, 3, yd, ys, yb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER, INL, OUTL, TST>;
+    auto kern = ks_tf32_bsfj_kernel<J, BN, BKJ, X3, GATHER, INL, OUTL, TST, MNJ>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1350,8 +1378,35 @@ cudaError_t launch_bsfj_bn(const ks_handle_s& h, const KsCall& call, int BN) {
 }
 
 // INL / OUTL: BSF / BSF (X3 or TF32), BSF / BSL or BSL / BSF (TF32 mixed-layout calls)
+// MN-major A for BSL in / BSF out (MNJ): J = 4 (four j's 16 KB A tiles + BN <= 64 weight
+// rows fit two 32-l operand slots), d % 4 == 0 and d <= 16: measured (1,64,256,16)
+// 349 -> 273 us, (1,128,128,16) 166 -> 100 us, (1,96,96,8) 69 -> 46 us; at d = 32 the
+// 16-byte output runs of J = 4 cost more than the staged J = 8 kernel's TMA-stored
+// 32-byte runs ((1,128,128,32) 296 -> 423 us), profiles/r03/mnj_time.jsonl.
+// KS_TF32_MNJ=0 disables (experiments).
+bool bsfj_mnj_on() {
+    static const bool on = [] {
+        const char* e = getenv("KS_TF32_MNJ");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 template <bool X3, int INL = KS_LAYOUT_BSF, int OUTL = KS_LAYOUT_BSF>
 cudaError_t launch_bsfj_any(const ks_handle_s& h, const KsCall& call) {
+    if constexpr (INL == KS_LAYOUT_BSL && OUTL == KS_LAYOUT_BSF && !X3) {
+        if (bsfj_mnj_on() && h.d % 4 == 0 && h.d <= 16 && h.c % 32 == 0) {
+            for (int bn : {64, 48, 32, 16}) {
+                if (h.b % bn != 0) continue;
+                switch (bn) {
+                    case 64: return launch_bsfj_t<4, 64, false, false, INL, OUTL, false, true>(h, call);
+                    case 48: return launch_bsfj_t<4, 48, false, false, INL, OUTL, false, true>(h, call);
+                    case 32: return launch_bsfj_t<4, 32, false, false, INL, OUTL, false, true>(h, call);
+                    case 16: return launch_bsfj_t<4, 16, false, false, INL, OUTL, false, true>(h, call);
+                }
+            }
+        }
+    }
     const BsfjPlan p = INL == KS_LAYOUT_BSL ? pick_bslj(h, call.knobs)
                                             : pick_bsfj(h, call.knobs, OUTL == KS_LAYOUT_BSL);
     if constexpr (INL == KS_LAYOUT_BSF) {

@@ -41,6 +41,26 @@ if os.environ.get("KS_MULTITILE_MATH") == "fp32":
         ok = ok and same and err <= 1e-5 and inside
     sys.exit(0 if ok else 1)
 
+if os.environ.get("KS_MULTITILE_MATH") == "tf32mixed":
+    # ks_matmul_io BSL in / BSF out and BSF in / BSL out (J-kernels: MN-major A for
+    # d <= 16, staged J = 8 + TMA-store epilogue above; J = 4 gather to BSL out)
+    worst = 0.0
+    for p, xl, yl, B in [((1, 64, 256, 16), "bsl", "bsf", 1024), ((3, 96, 96, 4), "bsl", "bsf", 772),
+                         ((1, 128, 128, 12), "bsl", "bsf", 516), ((1, 64, 64, 32), "bsl", "bsf", 600),
+                         ((1, 256, 64, 16), "bsf", "bsl", 520), ((1, 48, 48, 64), "bsf", "bsf", 388)]:
+        M, N, _ = O.dims(p)
+        K4 = ksgen.k4_uniform(*p, seed=3)
+        X = ksgen.x_normal(B, N, seed=4)
+        f = ksb.Factor(*p, K4).set_math(ksb.MATH_TF32)
+        Xd = torch.from_numpy(X if xl == "bsf" else ksgen.to_bsl(X)).cuda()
+        Y = ksb.matmul_io(f, Xd, xl, y_layout=yl)
+        torch.cuda.synchronize()
+        Yh = Y.cpu().numpy() if yl == "bsf" else Y.cpu().numpy().T
+        e = O.normwise_error(Yh, O.matmul(p, K4, X))
+        print(p, xl, yl, B, "tf32 mixed maxgrid", os.environ.get("KS_TF32_MAXGRID"), "err", e)
+        worst = max(worst, e)
+    sys.exit(0 if worst <= 5e-3 else 1)
+
 if os.environ.get("KS_MULTITILE_MATH") == "f32x3":
     # 3xTF32 (FP32 contract, normwise <= 1e-5), BSL transposer and BSF splitter paths
     worst = 0.0

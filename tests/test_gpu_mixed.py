@@ -193,3 +193,18 @@ def test_chain_graph_replays_mixed_plan_bit_identical(ksb):
     torch.cuda.synchronize()
     assert torch.equal(Yg, Y)
     g.free()
+
+
+@pytest.mark.parametrize("grid", [1, 3])
+def test_tf32_mixed_many_tiles_per_cta(grid):
+    """Mixed-layout J-kernels (MN-major A for BSL in, TMA-store epilogue) with a capped
+    persistent grid (KS_TF32_MAXGRID): every CTA runs several tiles, so the operand
+    ring, the accumulator double buffer and the store buffers all wrap."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KS_TF32_MAXGRID=str(grid), KS_MULTITILE_MATH="tf32mixed")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "multitile_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
