@@ -114,10 +114,15 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, int nkc, int64_t nnb, 
     return t;
 }
 
-template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT, bool MNA = false>
+// TSTD (FP32 Y in BSF, d = 1): each epilogue warp's 32-row x 16-output chunk goes out by
+// one TMA tensor store of a dense [32][16] box (2 KB, in the warp_store_rows scratch)
+// instead of warp_store_rows' shared-memory transpose + 16-byte warp stores.
+template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT, bool MNA = false,
+          bool TSTD = false>
 __global__ void __launch_bounds__(NTHREADS, Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>::CTAS)
 ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-               const __grid_constant__ CUtensorMap kmap_lo, T* __restrict__ Y, const T* __restrict__ bias,
+               const __grid_constant__ CUtensorMap kmap_lo, const __grid_constant__ CUtensorMap ymap,
+               T* __restrict__ Y, const T* __restrict__ bias,
                int64_t B, int a, int b, int c, int d, int64_t ntiles, int flags) {
     // flags: bits 0-7 = KS_TF32_DEBUG experiment switches, bits 8-15 = epilogue activation
     const int dbg = flags & 0xFF, act = (flags >> 8) & 0xFF;
@@ -358,7 +363,43 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = ks_act(v[e], act);
                 }
-                if constexpr (OUTL != KS_LAYOUT_BSL) {
+                if constexpr (OUTL != KS_LAYOUT_BSL && TSTD) {
+                    // dense box [32 rows][16 floats]: lane = row, 64-byte rows; lane n writes its
+                    // 4 chunks rotated by n mod 4 (a phase's 8 lanes on 4+4 bank groups)
+                    static_assert(sizeof(T) == 4, "FP32 Y");
+                    const uint32_t buf = scr0 + (uint32_t)(warp - 6) * 2048u;
+                    float w[4][4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) w[u][x] = v[4 * u + x];
+                    const int rot = lane & 3;
+#pragma unroll
+                    for (int sb = 1; sb < 4; sb <<= 1) {
+                        const bool on = rot & sb;
+                        float t[4][4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) t[u][x] = on ? w[(u + sb) & 3][x] : w[u][x];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) w[u][x] = t[u][x];
+                    }
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        sts128(buf + (uint32_t)lane * 64u + (uint32_t)((u + rot) & 3) * 16u, w[u][0], w[u][1], w[u][2],
+                               w[u][3]);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0 && !(dbg & 1)) {
+                        tma_store_2d(&ymap, tc.i * b + tc.k0 + col, tc.n0 + lq * 32, buf);
+                        bulk_commit();
+                    }
+                } else if constexpr (OUTL != KS_LAYOUT_BSL) {
                     // BSF out (d = 1): row n's 16 outputs are contiguous; coalesce through scratch
                     if constexpr (sizeof(T) == 4) {
                         if (dbg & 4) {            // experiment: direct stores, no shared-memory staging
@@ -381,6 +422,9 @@ ks_tf32_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             tc_fence_before();
             mbar_arrive(acce0 + 8 * ab);
         }
+    }
+    if constexpr (TSTD) {
+        if (warp >= 6 && lane == 0) bulk_wait_all();     // this thread's TMA stores have completed
     }
     tc_fence_before();
     __syncthreads();
@@ -1145,8 +1189,21 @@ int pick_bn(int64_t b) {
     return 0;
 }
 
+template <int LAYOUT, int BN, typename T, bool X3, int OUTL, bool MNA, bool TSTD>
+cudaError_t launch_bn_t(const ks_handle_s& h, const KsCall& call);
+
+bool bsfj_tst_on();
+
+// FP32 BSF-out launches take the TMA-store epilogue (TSTD); KS_TF32_TMASTORE=0 disables
 template <int LAYOUT, int BN, typename T = float, bool X3 = false, int OUTL = LAYOUT, bool MNA = false>
 cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
+    if constexpr (OUTL == KS_LAYOUT_BSF && sizeof(T) == 4)
+        if (bsfj_tst_on()) return launch_bn_t<LAYOUT, BN, T, X3, OUTL, MNA, true>(h, call);
+    return launch_bn_t<LAYOUT, BN, T, X3, OUTL, MNA, false>(h, call);
+}
+
+template <int LAYOUT, int BN, typename T, bool X3, int OUTL, bool MNA, bool TSTD>
+cudaError_t launch_bn_t(const ks_handle_s& h, const KsCall& call) {
     using C = Tf32Cfg<LAYOUT, BN, X3, OUTL, MNA>;
     constexpr cuuint32_t BK = C::RB / sizeof(T);
     constexpr cuuint64_t ES = sizeof(T);
@@ -1177,7 +1234,15 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
         const cuuint32_t xb[2] = {BK, BM};
         if (!encode(&xmap, call.X, 2, xd, xs, xb, SW, dt)) return cudaErrorInvalidValue;
     }
-    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3, OUTL, MNA>;
+    CUtensorMap ymap{};
+    if constexpr (TSTD) {                        // Y viewed [B][M] (d = 1): box {16 outputs, 32 rows}
+        const int64_t M = h.a * h.b * h.d;
+        const cuuint64_t yd[2] = {(cuuint64_t)M, (cuuint64_t)call.B};
+        const cuuint64_t ys[1] = {(cuuint64_t)M * 4};
+        const cuuint32_t yb[2] = {16, 32};
+        if (!encode(&ymap, call.Y, 2, yd, ys, yb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    }
+    auto kern = ks_tf32_kernel<LAYOUT, BN, T, X3, OUTL, MNA, TSTD>;
     static bool attr[64] = {false};
     if (!attr[h.device & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1189,7 +1254,7 @@ cudaError_t launch_bn(const ks_handle_s& h, const KsCall& call) {
     if (max_grid() > 0) slots = max_grid();
     const int64_t grid = ntiles < slots ? ntiles : slots;
     const cudaError_t e = ks::launch_pdl(kern, dim3((unsigned)grid), dim3(NTHREADS), C::SMEM, call.stream, xmap, kmap,
-                                         kmap_lo, reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias),
+                                         kmap_lo, ymap, reinterpret_cast<T*>(call.Y), reinterpret_cast<const T*>(call.bias),
                                          call.B, (int)h.a, (int)h.b, (int)h.c, (int)h.d, ntiles, debug_flags() | (call.act << 8));
     ks::count_launch();
     return e;
