@@ -45,7 +45,7 @@ for cs in args.cases.split(";"):
         e.record()
         e.synchronize()
         ts.append(s.elapsed_time(e))
-    q = statistics.quantiles(ts, n=4)
+    q = statistics.quantiles(ts, n=4) if len(ts) >= 2 else [ts[0]] * 3
     t = statistics.median(ts)
     byts = 4 * (B * f.N + f.nnz + B * f.M)
     print(json.dumps({"tag": args.tag, "pattern": list(p), "B": B, "io": f"{xl}->{yl}", "knobs": args.knobs,
