@@ -11,6 +11,7 @@ INC = os.path.join(ROOT, "paper_2405_15013_b200", "csrc", "ks_presets.inc")
 # the table is generated from these records; later ones replace earlier rows with the same key
 JSNS = [os.path.join(ROOT, "profiles", "r02", n) for n in ("autotune.json", "autotune_tf32_bsl.json", "autotune_fp32_bsf.json")]
 JSNS.append(os.path.join(ROOT, "profiles", "r03", "autotune_tf32_bsf.json"))   # TF32 BSF re-tune after the TMA-store epilogue
+JSNS.append(os.path.join(ROOT, "profiles", "r03", "autotune_tf32_bsf_v2.json"))  # ... and after MNJ / the d = 1 TMA store
 
 
 def _rows():
