@@ -208,3 +208,22 @@ def test_tf32_mixed_many_tiles_per_cta(grid):
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "multitile_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("p,dirn,B", [((1, 64, 256, 16), "lf", 65536), ((1, 256, 64, 16), "fl", 65536),
+                                      ((1, 128, 128, 16), "lf", 25088), ((64, 64, 64, 1), "lf", 65536)])
+def test_tf32_mixed_full_size_sampled_rows(ksb, p, dirn, B):
+    """configs[4]-size mixed-layout calls in the launch configuration the chains use
+    (MN-major BSL-in J-kernel, J = 4 BSF-in/BSL-out, the d = 1 TMA-store epilogue):
+    sampled rows against the oracle, inside the per-element envelope."""
+    xl, yl = DIRS[dirn]
+    M, N, _ = O.dims(p)
+    K4 = ksgen.k4_uniform(*p, seed=4000 + p[1])
+    X = ksgen.x_normal(B, N, seed=11)
+    f = ksb.Factor(*p, K4).set_math(ksb.MATH_TF32)
+    Yt, fam = run_io(ksb, f, X, xl, yl)
+    assert fam == [FAMILY_TF32], fam
+    rows = np.array([0, 1, 127, 128, B // 2 + 3, B - 129, B - 1])
+    Yref, env = O.matmul(p, K4, X, rows=rows, want_env=True)
+    assert O.normwise_error(Yt[rows], Yref) <= TF32_TOL
+    assert np.all(np.abs(Yt[rows] - Yref) <= O.envelope_delta(p[2], 2.0 ** -10) * env)
