@@ -56,7 +56,10 @@ struct WsCfg {
     static constexpr int BAR_OFF = S * SLOT;
     static constexpr int SMEM = BAR_OFF + 8 * 8 + 4 * 8 + 1024;     // full barriers, counters, align pad
     static_assert(BN == 48 || BN == 64 || BN == 96 || BN == 128, "BN");
-    static_assert(TN % 2 == 0 && BN % (4 * WN) == 0, "TN even (FFMA2 pairs)");
+    static_assert(BN % (4 * WN) == 0, "whole thread columns");
+    // odd TN (the split-row tiles of BN = 48 / 96): FFMA2 lanes pair two rows of one
+    // output instead of two outputs of one row (same fmaf chain per output)
+    static constexpr bool RP = TN % 2 != 0;
     static_assert(SLOT % 1024 == 0, "slot alignment (SWIZZLE_64B A tiles)");
     static_assert(S * KB >= 64, "ring depth (l in flight)");
 };
@@ -133,12 +136,13 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
         int64_t n0;
         decode(tile, q, k0, n0);
         const int i = q / d, j = q % d;
-        static_assert(TN % 2 == 0, "FFMA2 pairs of outputs");
-        uint64_t acc2[8][TN / 2];                 // (acc[m][2p], acc[m][2p+1]) packed for FFMA2
+        constexpr bool RP = C::RP;
+        constexpr int A2M = RP ? 4 : 8, A2N = RP ? TN : TN / 2;
+        uint64_t acc2[A2M][A2N];                  // (acc[m][2p], acc[m][2p+1]), or (acc[2q][e], acc[2q+1][e]) if RP
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+        for (int m = 0; m < A2M; ++m)
 #pragma unroll
-            for (int p = 0; p < TN / 2; ++p) acc2[m][p] = 0;
+            for (int p = 0; p < A2N; ++p) acc2[m][p] = 0;
 
         for (int t = 0; t < nk; ++t, ++g) {
             const int st = (int)(g % S);
@@ -162,16 +166,27 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                          : "=f"(bv[e]), "=f"(bv[e + 1]), "=f"(bv[e + 2]), "=f"(bv[e + 3])
                                          : "r"(pb + e * 4));
+                    } else if constexpr (RP) {        // odd TN: 4-byte aligned columns
+#pragma unroll
+                        for (int e = 0; e < TN; ++e) bv[e] = lds32(pb + e * 4);
                     } else {
 #pragma unroll
                         for (int e = 0; e < TN; e += 2)
                             asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(bv[e]), "=f"(bv[e + 1]) : "r"(pb + e * 4));
                     }
+                    if constexpr (RP) {               // rows (2q, 2q+1): av[] is 4 consecutive rows per float4
 #pragma unroll
-                    for (int m = 0; m < 8; ++m)
+                        for (int q = 0; q < 4; ++q)
 #pragma unroll
-                        for (int p = 0; p < TN / 2; ++p)
-                            acc2[m][p] = ffma2(f2pack(av[m], av[m]), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
+                            for (int e = 0; e < TN; ++e)
+                                acc2[q][e] = ffma2(f2pack(av[2 * q], av[2 * q + 1]), f2pack(bv[e], bv[e]), acc2[q][e]);
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < 8; ++m)
+#pragma unroll
+                            for (int p = 0; p < TN / 2; ++p)
+                                acc2[m][p] = ffma2(f2pack(av[m], av[m]), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
+                    }
                 }
             } else {
                 // A[n][l] (64-byte rows, SWIZZLE_64B: 16-byte chunk u of row n at u ^ ((n >> 1) & 3)):
@@ -198,17 +213,32 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                              : "=f"(bv[e]), "=f"(bv[e + 1]), "=f"(bv[e + 2]), "=f"(bv[e + 3])
                                              : "r"(pb + e * 4));
+                        } else if constexpr (RP) {    // odd TN: 4-byte aligned columns
+#pragma unroll
+                            for (int e = 0; e < TN; ++e) bv[e] = lds32(pb + e * 4);
                         } else {
 #pragma unroll
                             for (int e = 0; e < TN; e += 2)
                                 asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(bv[e]), "=f"(bv[e + 1]) : "r"(pb + e * 4));
                         }
+                        auto comp = [&](int m) {
+                            return e4 == 0 ? av[m].x : e4 == 1 ? av[m].y : e4 == 2 ? av[m].z : av[m].w;
+                        };
+                        if constexpr (RP) {           // rows (2q, 2q+1) = ty + 16q, ty + 16q + 8
 #pragma unroll
-                        for (int m = 0; m < 8; ++m) {
-                            const float x = e4 == 0 ? av[m].x : e4 == 1 ? av[m].y : e4 == 2 ? av[m].z : av[m].w;
+                            for (int q = 0; q < 4; ++q) {
+                                const uint64_t xp = f2pack(comp(2 * q), comp(2 * q + 1));
 #pragma unroll
-                            for (int p = 0; p < TN / 2; ++p)
-                                acc2[m][p] = ffma2(f2pack(x, x), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
+                                for (int e = 0; e < TN; ++e) acc2[q][e] = ffma2(xp, f2pack(bv[e], bv[e]), acc2[q][e]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int m = 0; m < 8; ++m) {
+                                const float x = comp(m);
+#pragma unroll
+                                for (int p = 0; p < TN / 2; ++p)
+                                    acc2[m][p] = ffma2(f2pack(x, x), f2pack(bv[2 * p], bv[2 * p + 1]), acc2[m][p]);
+                            }
                         }
                     }
                 }
@@ -230,13 +260,23 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
 
         // ---- epilogue: each owned Y element written exactly once ----------------
         float acc[8][TN];
+        if constexpr (RP) {
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+            for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int p = 0; p < TN / 2; ++p) {
-                acc[m][2 * p] = f2lo(acc2[m][p]);
-                acc[m][2 * p + 1] = f2hi(acc2[m][p]);
-            }
+                for (int e = 0; e < TN; ++e) {
+                    acc[2 * q][e] = f2lo(acc2[q][e]);
+                    acc[2 * q + 1][e] = f2hi(acc2[q][e]);
+                }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int p = 0; p < TN / 2; ++p) {
+                    acc[m][2 * p] = f2lo(acc2[m][p]);
+                    acc[m][2 * p + 1] = f2hi(acc2[m][p]);
+                }
+        }
         if (bias) {                               // KSLinear bias (NEXT-2)
 #pragma unroll
             for (int e = 0; e < TN; ++e) {
@@ -274,6 +314,9 @@ ks_ffma_ws_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
                     for (int e = 0; e < TN; e += 4)
                         __stcs(reinterpret_cast<float4*>(yr + e),
                                make_float4(acc[m][e], acc[m][e + 1], acc[m][e + 2], acc[m][e + 3]));
+                } else if constexpr (RP) {
+#pragma unroll
+                    for (int e = 0; e < TN; ++e) __stcs(yr + e, acc[m][e]);
                 } else {
 #pragma unroll
                     for (int e = 0; e < TN; e += 2)
@@ -1088,16 +1131,17 @@ int pick_bn_ws(int64_t b) {
 
 // Underfilled launches (fewer default tiles than 2 CTAs x SMs, e.g. a = d = 1 with
 // B = 25088: 196 tiles of 128 rows for 296 slots, the last 48 SMs running two
-// tiles while 100 run one) take tiles of half the rows (BN = 128: 64 x 128,
-// thread micro-tile 8 x 4; BN = 64: 128 x 64): the busiest SM then holds 1.5
-// default tiles' work instead of 2.  KS_FFMA_SPLITM=0 disables (experiments).
+// tiles while 100 run one) take tiles of half the rows (BN = 128: 64 rows, thread
+// micro-tile 8 x 4; BN = 96, BSL: 64 rows, 8 x 3 with row-pair FFMA2; BN = 64: 128
+// rows): the busiest SM then holds 1.5 default tiles' work instead of 2
+// (BN = 48 splits measured 0.85-1.13x: not used).  KS_FFMA_SPLITM=0 disables (experiments).
 bool ws_split_rows(const ks_handle_s& h, const KsCall& call, int bn) {
     static const bool on = [] {
         const char* e = getenv("KS_FFMA_SPLITM");
         return !(e && atoi(e) == 0);
     }();
-    if (!on || (bn != 128 && bn != 64)) return false;
-    const int64_t rows = bn == 128 ? 128 : 256;
+    if (!on || bn == 0) return false;
+    const int64_t rows = bn > 64 ? 128 : 256;
     const int64_t tiles = (h.b / bn) * ((call.B + rows - 1) / rows) * (h.a * h.d);
     return tiles < 2 * (int64_t)ks::num_sms(h.device);   // (not the KS_TF32_MAXGRID test cap: the shape stays)
 }
@@ -1105,8 +1149,16 @@ bool ws_split_rows(const ks_handle_s& h, const KsCall& call, int bn) {
 template <int LAYOUT, int KB>
 cudaError_t launch_ws_kb(const ks_handle_s& h, const KsCall& call) {
     const int bn = pick_bn_ws(h.b);
-    if (KB == WS_BK && ws_split_rows(h, call, bn))
-        return bn == 128 ? launch_ws<LAYOUT, 128, KB, 1>(h, call) : launch_ws<LAYOUT, 64, KB, 2>(h, call);
+    if (KB == WS_BK && ws_split_rows(h, call, bn)) {
+        switch (bn) {
+            case 128: return launch_ws<LAYOUT, 128, KB, 1>(h, call);
+            case 96:         // TN = 3: row-pair FFMA2; BSL only (BSF's A rows need a pack per pair:
+                             // (1,96,96,1) BSF 0.93x, BSL 1.16x, profiles/r03/oddtn_time.jsonl)
+                if constexpr (LAYOUT == KS_LAYOUT_BSL) return launch_ws<LAYOUT, 96, KB, 1>(h, call);
+                break;
+            case 64: return launch_ws<LAYOUT, 64, KB, 2>(h, call);
+        }
+    }
     switch (bn) {
         case 128: return launch_ws<LAYOUT, 128, KB>(h, call);
         case 96: return launch_ws<LAYOUT, 96, KB>(h, call);
@@ -1122,7 +1174,8 @@ cudaError_t launch_ws_layout(const ks_handle_s& h, const KsCall& call) {
     // BSF (64,96,96,1) 839 -> 745 us); elsewhere it is 0-10 % slower
     // (profiles/r01_ffma_kb32_negative.txt).  KS_FFMA_KB32=0 disables.
     if ((call.knobs & KS_KNOB_KB32) && h.c % 32 == 0 && pick_bn_ws(h.b) == 96)
-        return launch_ws<LAYOUT, 96, 32>(h, call);
+        return LAYOUT == KS_LAYOUT_BSL && ws_split_rows(h, call, 96) ? launch_ws<LAYOUT, 96, 32, 1>(h, call)
+                                                                     : launch_ws<LAYOUT, 96, 32>(h, call);
     return launch_ws_kb<LAYOUT, WS_BK>(h, call);
 }
 
